@@ -1,0 +1,134 @@
+/*
+ * libmcf -- C-ABI of the B200-native ALS / MFITR sweep (sm_100a).
+ *
+ * The drop-in boundary for the reference's numba operators.  Every pointer
+ * is caller-owned CUDA device memory (the Python host passes
+ * torch.Tensor.data_ptr()), `stream` is a cudaStream_t passed as void*, no
+ * call allocates device memory, and every call returns 0 on success or a
+ * negative MCF_E* code with a message readable through mcf_last_error().
+ * Calls are safe from any host thread on their own stream with disjoint
+ * outputs.  Factor matrices are row-major [rows][ld] float32 with
+ * ld = mcf_factor_ld(D) = round_up(D, 4) and zero padding columns.
+ *
+ * Reference operator each entry point replaces (paths relative to
+ * /root/reference/pkg/src/multicf):
+ *   mcf_csr_build      factor._side_csr                 factor.py:493-509
+ *                      (+ np.bincount degrees, data.Dataset.by_user data.py:132-142)
+ *   mcf_als_plan       parallel.run_blocks/even_bounds   parallel.py:134-145
+ *   mcf_als_half_step  _kernels.als_solve_rows           _kernels.py:151-215
+ *                      driven as factor.als_half_step    factor.py:512-538
+ *   mcf_taxonomy_terms the graph term of mfitr.grad_mfitr mfitr.py:269-273
+ *                      (ALS form of _kernels.edge_pass_range _kernels.py:128-148)
+ *   mcf_predict_sse    _kernels.mf_predict_batch         _kernels.py:331-375
+ *                      + clip + squared error (factor.py:613-616, evaluation.py:11-18)
+ *   mcf_sq_norms       the regulariser of factor.als_objective factor.py:541-547
+ *                      / factor.loss_mf (factor.py:270-278)
+ *   mcf_add_gathered   q_i + q_a[artist(i)] of mfitr._rating_terms mfitr.py:203-216
+ */
+#ifndef MCF_H
+#define MCF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MCF_OK = 0,
+    MCF_E_ARG = -1,        /* invalid argument (null pointer, bad size, bad D) */
+    MCF_E_WORKSPACE = -2,  /* workspace smaller than *_workspace_bytes()      */
+    MCF_E_RANGE = -3,      /* a key / id outside its declared range            */
+    MCF_E_CUDA = -4,       /* a CUDA runtime error (message has the details)   */
+    MCF_E_UNSUPPORTED = -5 /* D outside the compiled range (1..128)            */
+};
+
+int mcf_version(void);
+const char *mcf_last_error(void);
+int mcf_factor_ld(int D);
+int mcf_max_dim(void);
+
+/* ---- rating layout: stable CSR (by user) / CSC (by item) build ----------
+ * Rows keyed by keys[k] in [0, n_rows); in-row order == record order (the
+ * reference's argsort(kind="stable")).  ptr_out[n_rows+1] int64,
+ * idx_out[nnz] = cols in that order, val_out[nnz] = vals in that order,
+ * perm_out[nnz] (nullable) = the record index of each CSR slot.
+ * Synchronises `stream` once to report out-of-range keys (MCF_E_RANGE). */
+size_t mcf_csr_workspace_bytes(int64_t nnz, int32_t n_rows);
+int mcf_csr_build(const int32_t *keys, const int32_t *cols, const float *vals, int64_t nnz,
+                  int32_t n_rows, int64_t *ptr_out, int32_t *idx_out, float *val_out,
+                  int32_t *perm_out, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- ALS half-step --------------------------------------------------------
+ * Work plan for a set of rows of one layout: the rows row_list[0..n_list)
+ * (or, when row_list is NULL, rows row_lo .. row_lo + n_list), each cut into
+ * chunks of at most `chunk` ratings.  Built once per (layout, row set) and
+ * reused by every half-step.  Synchronises `stream` once and returns on the
+ * host: totals[0] = work items, totals[1] = partial-Gram slots (chunks of
+ * rows that span more than one chunk). */
+size_t mcf_als_plan_bytes(int32_t n_list, int64_t nnz, int32_t chunk);
+int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t n_list, int32_t row_lo,
+                 int32_t chunk, int64_t nnz, void *plan, size_t plan_bytes, int64_t *totals,
+                 void *stream);
+/* Bytes of half-step workspace: n_list row counters + `slots` partial
+ * Grams at dimension D (slots = totals[1] of mcf_als_plan). */
+size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
+
+/* Solve every planned row r exactly (Cholesky of the D x D system):
+ *   A_r = sum_k w_k x_k x_k^T + (lam_c + lam_n * n_r + tau * S_r) I
+ *   b_r = sum_k w_k (val_k - y_shift) x_k + tau * T_r
+ *   out[r] = A_r^{-1} b_r
+ * with x_k = fixed[idx[k]], w_k = wts[k] (wts NULL -> 1), n_r = ptr[r+1]-ptr[r],
+ * S/T (nullable) the taxonomy terms of mcf_taxonomy_terms (T row-major, ld).
+ * Plain ALS: lam_c = lam, lam_n = 0.  Weighted-lambda: lam_c = 0, lam_n = lam.
+ * A row with no ratings and no taxonomy mass becomes 0 when lam_c > 0 or
+ * lam_n > 0.  A row whose pivot is <= 0 or non-finite is left untouched and
+ * *fail_row (device int64) receives the minimum such row (-1 = none); all
+ * other rows still complete (the reference's failing block stops early,
+ * _kernels.py:197-203).  ws: mcf_als_workspace_bytes(n_list, totals[1], D). */
+int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
+                      const float *wts, const float *fixed, float *out, int32_t D,
+                      float lam_c, float lam_n, float y_shift, const float *tax_S,
+                      const float *tax_T, float tau, const int32_t *row_list, int32_t n_list,
+                      int32_t row_lo, int32_t chunk, const void *plan, int64_t total_items,
+                      int64_t *fail_row, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- MFITR taxonomy term (segmented reduction) ---------------------------
+ * For each listed item i (row_list NULL -> all n_items):
+ *   S[i] = sum_{e incident to i} w_e,   T[i] = sum_e w_e * q[other(e)]
+ * over the incident-edge CSR (inc_ptr[n_items+1], inc_edge, inc_other),
+ * summed in CSR order.  Only listed items are written. */
+int mcf_taxonomy_terms(const int64_t *inc_ptr, const int32_t *inc_edge,
+                       const int32_t *inc_other, const float *edge_w, const float *q,
+                       int32_t n_items, int32_t D, const int32_t *row_list, int32_t n_list,
+                       float *S_out, float *T_out, void *stream);
+
+/* ---- prediction / RMSE ----------------------------------------------------
+ * pred = mu + b_u[u] + b_i[i] + b_a[a] + (q_i + q_a[a]) . p_u with the
+ * reference's cold-start rules (unknown user or item keeps only the known
+ * terms); a = art_of_item[i] (nullable -> no artist terms).  b_u/b_i/b_a
+ * nullable (zeros).  pred_out (nullable) gets the unclipped prediction; when
+ * truth is non-NULL, *sse_out (device double) = sum (clip(pred,lo,hi) -
+ * truth)^2, reduced in a fixed order (deterministic).  ws:
+ * mcf_predict_workspace_bytes(n). */
+size_t mcf_predict_workspace_bytes(int64_t n);
+int mcf_predict_sse(const int32_t *users, const int32_t *items, const float *truth, int64_t n,
+                    const float *P, int32_t n_users, const float *Q, int32_t n_items, int32_t D,
+                    float mu, const float *b_u, const float *b_i, const int32_t *art_of_item,
+                    const float *b_a, const float *Q_a, float clip_lo, float clip_hi,
+                    float *pred_out, double *sse_out, void *ws, size_t ws_bytes, void *stream);
+
+/* *out (device double) = sum_r c_r |F_r|^2 with c_r = ptr[r+1]-ptr[r]
+ * (ptr non-NULL: the per-observation regulariser) or 1.  Deterministic. */
+int mcf_sq_norms(const float *F, int32_t n, int32_t D, const int64_t *ptr, double *out,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* out[i] = A[i] + B[map[i]] (map[i] < 0 -> A[i]); out may alias A. */
+int mcf_add_gathered(const float *A, const float *B, const int32_t *map, int32_t n, int32_t D,
+                     float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCF_H */

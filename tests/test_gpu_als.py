@@ -1,0 +1,331 @@
+"""GPU parity of the ALS path against the CPU oracle (which is itself pinned
+bit-exact to the reference, tests/test_oracle.py).
+
+Tolerances (north_star): integer layouts bit-exact; per-half-step factors
+within 1e-4 relative (re-anchored: the oracle restarts every half-step from
+the device's own input factors); held-out RMSE within 1e-4 absolute after
+the configured sweeps."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-4
+
+
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda")
+
+
+def _rel_rows(got, ref):
+    """max row-wise |d_r| / max(|ref_r|, 1e-6 max|ref|) and max|d| / max|ref|."""
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    scale = max(np.abs(ref).max(), 1e-30)
+    rn = np.linalg.norm(ref, axis=1)
+    dn = np.linalg.norm(got - ref, axis=1)
+    row = (dn / np.maximum(rn, 1e-6 * np.linalg.norm(ref, axis=1).max() + 1e-30)).max()
+    return row, np.abs(got - ref).max() / scale
+
+
+def _engine(users, items, scores, U, I, D, chunk=2048, keep_perm=False):
+    from paper_1108_2580_b200.device import AlsEngine, DeviceRatings
+    r = DeviceRatings(users, items, scores, U, I, dev(), keep_perm=keep_perm)
+    return AlsEngine(r, D, chunk=chunk)
+
+
+# ---------------------------------------------------------------------------
+# layout
+
+def test_csr_build_bit_exact_golden(golden):
+    from paper_1108_2580_b200.device import DeviceRatings
+    g = golden("csr.npz")
+    U, I = int(g["U"]), int(g["I"])
+    r = DeviceRatings(g["users"], g["items"], g["scores"].astype(np.float32), U, I, dev(),
+                      keep_perm=True)
+    for side, lay in (("users", r.by_user), ("items", r.by_item)):
+        assert np.array_equal(lay.ptr.cpu().numpy(), g[f"{side}_ptr"])
+        assert np.array_equal(lay.idx.cpu().numpy(), g[f"{side}_idx"])
+        assert np.array_equal(lay.val.cpu().numpy(), g[f"{side}_val"].astype(np.float32))
+
+
+@pytest.mark.parametrize("nnz,n_rows", [(0, 5), (1, 1), (3000, 1), (70_001, 300),
+                                        (2_500_000, 1_000_000), (1_200_000, 3_000_000)])
+def test_csr_build_matches_stable_argsort(nnz, n_rows):
+    from paper_1108_2580_b200.device import SideLayout
+    rng = np.random.default_rng(nnz + n_rows)
+    keys = (rng.zipf(1.3, nnz) * 7919 % n_rows).astype(np.int32)
+    cols = rng.integers(0, 1 << 30, nnz).astype(np.int32)
+    vals = rng.integers(0, 101, nnz).astype(np.float32)
+    d = dev()
+    lay = SideLayout(torch.from_numpy(keys).to(d), torch.from_numpy(cols).to(d),
+                     torch.from_numpy(vals).to(d), n_rows, keep_perm=True)
+    ptr, idx, val, _, perm = oracle.side_csr(keys, cols, vals, n_rows)
+    assert np.array_equal(lay.ptr.cpu().numpy(), ptr)
+    assert np.array_equal(lay.perm.cpu().numpy(), perm)
+    assert np.array_equal(lay.idx.cpu().numpy(), idx)
+    assert np.array_equal(lay.val.cpu().numpy(), val.astype(np.float32))
+
+
+def test_csr_build_rejects_out_of_range_keys():
+    from paper_1108_2580_b200.device import SideLayout
+    from paper_1108_2580_b200.errors import DeviceError
+    d = dev()
+    k = torch.tensor([0, 5, 2], dtype=torch.int32, device=d)
+    with pytest.raises(DeviceError, match="outside"):
+        SideLayout(k, k, k.float(), 5)
+
+
+# ---------------------------------------------------------------------------
+# known answers through the drop-in entry point
+
+def test_spec_scalars_drop_in():
+    from paper_1108_2580_b200 import factor
+    from paper_1108_2580_b200.data import Dataset
+    spec = json.load(open(os.path.join(GOLDEN, "spec_scalars.json")))
+    for lam, key in ((0.0, "p_lam0"), (1.0, "p_lam1")):
+        ds = Dataset.from_arrays([0], [0], [8.0])
+        m = factor.init_model("als", ds, factor.HyperParams(D=1), 0)
+        m.q[:] = 2.0
+        factor.als_half_step(m, ds, "users", lam)
+        assert abs(m.p[0, 0] - spec[key]) < 1e-6
+    ds = Dataset.from_arrays([0], [0], [8.0])
+    m = factor.init_model("als", ds, factor.HyperParams(D=1), 0)
+    m.q[:] = 2.0
+    factor.als_half_step(m, ds, "users", 1.0, weights=np.zeros(1))
+    assert m.p[0, 0] == spec["p_w0"] == 0.0
+
+
+def test_singular_row_raises_min_row():
+    from paper_1108_2580_b200 import SingularSystemError, factor
+    from paper_1108_2580_b200.data import Dataset
+    # users 3 and 5 see a single item with D=2 -> rank-1 systems at lam = 0
+    ds = Dataset.from_arrays([0, 0, 3, 5, 1, 1], [0, 1, 0, 1, 0, 1], [1, 2, 3, 4, 5, 6.0])
+    m = factor.init_model("als", ds, factor.HyperParams(D=2), 0)
+    with pytest.raises(SingularSystemError, match="users row 2"):
+        factor.als_half_step(m, ds, "users", 0.0)      # row 2 is empty -> min failing row
+    m = factor.init_model("als", ds, factor.HyperParams(D=2), 0)
+    factor.als_half_step(m, ds, "users", 0.5)          # regularised: fine, empty rows -> 0
+    assert np.all(m.p[2] == 0) and np.all(m.p[4] == 0)
+
+
+# ---------------------------------------------------------------------------
+# config 0 parity (re-anchored and free-running)
+
+@pytest.mark.parametrize("chunk", [2048, 64])
+def test_cfg0_weighted_lambda_reanchored(golden, chunk):
+    g = golden("als_cfg0.npz")
+    u, i, s = g["train_users"], g["train_items"], g["train_scores"]
+    U, I, D, lam = int(g["U"]), int(g["I"]), int(g["D"]), float(g["lam"])
+    eng = _engine(u, i, s, U, I, D, chunk=chunk)
+    eng.set_factors(g["P0"], g["Q0"])
+    for sweep in range(int(g["sweeps"])):
+        for side in ("items", "users"):
+            P, Q = (t.double().cpu().numpy() for t in eng.factors())
+            ref, failed = oracle.als_half_step(P, Q, u, i, s, side, lam_n=lam)
+            assert failed == -1
+            eng.half_step(side, 0.0, lam)
+            eng.check()
+            got = eng.factors()[0 if side == "users" else 1].double().cpu().numpy()
+            row, mx = _rel_rows(got, ref)
+            assert row < REL_TOL and mx < REL_TOL, (sweep, side, row, mx)
+    # free-running held-out RMSE vs the reference's own (golden) RMSE
+    vu = torch.as_tensor(g["valid_users"], dtype=torch.int32, device=dev())
+    vi = torch.as_tensor(g["valid_items"], dtype=torch.int32, device=dev())
+    vs = torch.as_tensor(g["valid_scores"], dtype=torch.float32, device=dev())
+    rm = float(eng.rmse(vu, vi, vs).item())
+    assert abs(rm - float(g["rmse"][-1])) < 1e-4, (rm, g["rmse"][-1])
+
+
+def test_cfg0_first_half_steps_vs_reference(golden):
+    """Device vs the reference's own factors after the first half-steps
+    (fp32 device, f64 reference; same initial factors)."""
+    g = golden("als_cfg0.npz")
+    eng = _engine(g["train_users"], g["train_items"], g["train_scores"], int(g["U"]),
+                  int(g["I"]), int(g["D"]))
+    eng.set_factors(g["P0"], g["Q0"])
+    lam = float(g["lam"])
+    for key in ("Q1", "P1", "Q2", "P2"):
+        side = "items" if key[0] == "Q" else "users"
+        eng.half_step(side, 0.0, lam)
+        got = eng.factors()[0 if side == "users" else 1].double().cpu().numpy()
+        row, mx = _rel_rows(got, g[key])
+        assert row < REL_TOL and mx < REL_TOL, (key, row, mx)
+    eng.check()
+
+
+def test_train_drop_in_cfg0(golden):
+    from paper_1108_2580_b200 import factor
+    from paper_1108_2580_b200.data import Dataset
+    g = golden("als_cfg0.npz")
+    U, I = int(g["U"]), int(g["I"])
+    tr = Dataset.from_arrays(g["train_users"], g["train_items"], g["train_scores"],
+                             num_users=U, num_items=I)
+    va = Dataset.from_arrays(g["valid_users"], g["valid_items"], g["valid_scores"],
+                             num_users=U, num_items=I)
+    hp = factor.HyperParams(lam=float(g["lam"]), D=int(g["D"]), iters=int(g["sweeps"]))
+    model, rep = factor.train("wals", tr, va, hp, reg="weighted", init=(g["P0"], g["Q0"]))
+    assert len(rep) == hp.iters
+    for s, row in enumerate(rep):
+        assert abs(row.valid_rmse - float(g["rmse"][s])) < 1e-4
+    assert np.all(np.diff([r.objective for r in rep]) <= 1e-6 * rep[0].objective)
+    row, mx = _rel_rows(model.p, g["P_final"])
+    assert mx < 1e-3
+    pred = factor.predict_batch(model, g["valid_users"], g["valid_items"])
+    ref = oracle.predict(g["P_final"], g["Q_final"], g["valid_users"], g["valid_items"])
+    assert np.abs(pred - ref).max() < 1e-3 * np.abs(ref).max()
+
+
+def test_wals_weights_path_reanchored(golden):
+    """The reference-oracle form: lam * I with per-observation w = 1/n_row
+    (HAS_W kernel), bit-for-bit the reference's wALS hook in f64."""
+    g = golden("als_cfg0.npz")
+    u, i, s = g["train_users"], g["train_items"], g["train_scores"]
+    U, I, D, lam = int(g["U"]), int(g["I"]), int(g["D"]), float(g["lam"])
+    eng = _engine(u, i, s, U, I, D, keep_perm=True)
+    eng.set_factors(g["P0"], g["Q0"])
+    wi = oracle.weighted_lambda_weights(u, i, U, I, "items")
+    eng.set_weights(wi)
+    eng.half_step("items", lam, 0.0)
+    eng.check()
+    got = eng.factors()[1].double().cpu().numpy()
+    row, mx = _rel_rows(got, g["Q1"])
+    assert row < REL_TOL and mx < REL_TOL, (row, mx)
+
+
+def test_plain_lambda_small_monotone(golden):
+    """SPEC.md:346 instance: plain lam = 1, D = 5, 25 iterations; every
+    half-step matches the reference and the objective never increases."""
+    g = golden("als_small.npz")
+    u, i, s = g["users"], g["items"], g["scores"]
+    eng = _engine(u, i, s, 20, 30, int(g["D"]))
+    eng.set_factors(g["P0"], g["Q0"])
+    objs = []
+    for it in range(25):
+        for side, key in (("items", "Q"), ("users", "P")):
+            eng.half_step(side, 1.0, 0.0)
+            got = eng.factors()[0 if side == "users" else 1].double().cpu().numpy()
+            row, mx = _rel_rows(got, g[key][it])
+            assert mx < 1e-3, (it, side, mx)          # free-running fp32 vs f64
+            objs.append(float(eng.objective(1.0, "plain").item()))
+    eng.check()
+    objs = np.array(objs)
+    assert np.all(np.diff(objs) <= 1e-5 * objs[:-1])
+    np.testing.assert_allclose(objs, g["obj"], rtol=1e-3)
+
+
+# ---------------------------------------------------------------------------
+# dimensions, heavy rows, determinism
+
+def _random_split(U, I, nnz, seed, hot=None):
+    rng = np.random.default_rng(seed)
+    keys = np.unique(rng.integers(0, U * I, nnz))
+    if hot is not None:   # one very hot item rated by every user
+        keys = np.unique(np.concatenate([keys, np.arange(U) * I + hot]))
+    keys = rng.permutation(keys)
+    return ((keys // I).astype(np.int32), (keys % I).astype(np.int32),
+            rng.integers(0, 101, keys.size).astype(np.float32))
+
+
+@pytest.mark.parametrize("D", [1, 3, 5, 8, 16, 20, 28, 29, 32, 50, 64, 100, 128])
+@pytest.mark.parametrize("reg", ["plain", "weighted"])
+def test_dims_reanchored(D, reg):
+    U, I = 400, 300
+    u, i, s = _random_split(U, I, 30_000, D, hot=7)
+    eng = _engine(u, i, s, U, I, D, chunk=256)
+    rng = np.random.default_rng(1)
+    eng.set_factors(rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D)))
+    lam = 0.065
+    lc, ln = (lam, 0.0) if reg == "plain" else (0.0, lam)
+    for side in ("items", "users", "items"):
+        P, Q = (t.double().cpu().numpy() for t in eng.factors())
+        ref, failed = oracle.als_half_step(P, Q, u, i, s, side, lam_c=lc, lam_n=ln)
+        eng.half_step(side, lc, ln)
+        eng.check()
+        got = eng.factors()[0 if side == "users" else 1].double().cpu().numpy()
+        row, mx = _rel_rows(got, ref)
+        assert row < REL_TOL and mx < REL_TOL, (D, reg, side, row, mx)
+    # padding columns stay zero
+    assert torch.all(eng.P[:, D:] == 0) and torch.all(eng.Q[:, D:] == 0)
+
+
+def test_heavy_row_multi_chunk_and_determinism():
+    U, I, D = 20_000, 500, 20
+    u, i, s = _random_split(U, I, 400_000, 3, hot=11)
+    outs = []
+    for chunk in (2048, 2048, 128):
+        eng = _engine(u, i, s, U, I, D, chunk=chunk)
+        rng = np.random.default_rng(2)
+        eng.set_factors(rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D)))
+        eng.half_step("items", 0.0, 0.065)
+        eng.check()
+        outs.append(eng.factors()[1].double().cpu().numpy())
+    ref, _ = oracle.als_half_step(eng.factors()[0].double().cpu().numpy(), outs[0], u, i, s,
+                                  "items", lam_n=0.065)
+    assert np.array_equal(outs[0], outs[1])             # run-to-run bit-identical
+    for o in outs:
+        row, mx = _rel_rows(o, ref)
+        assert row < REL_TOL and mx < REL_TOL, (row, mx)
+
+
+def test_empty_rows_and_zero_rating_rows():
+    U, I, D = 50, 40, 6
+    u, i, s = _random_split(U - 10, I - 10, 600, 5)      # last 10 users / items empty
+    eng = _engine(u, i, s, U, I, D)
+    rng = np.random.default_rng(0)
+    eng.set_factors(rng.normal(size=(U, D)), rng.normal(size=(I, D)))
+    eng.half_step("users", 0.0, 0.1)
+    eng.half_step("items", 0.3, 0.0)
+    eng.check()
+    P, Q = (t.cpu().numpy() for t in eng.factors())
+    assert np.all(P[U - 10:] == 0) and np.all(Q[I - 10:] == 0)
+
+
+def test_predict_golden_cold_start(golden):
+    from paper_1108_2580_b200.device import AlsEngine, DeviceRatings
+    g = golden("predict.npz")
+    P, Q = g["P"], g["Q"]
+    z = np.zeros(0, np.int32)
+    r = DeviceRatings(z, z, np.zeros(0, np.float32), P.shape[0], Q.shape[0], dev())
+    eng = AlsEngine(r, P.shape[1])
+    eng.set_factors(P, Q)
+    d = dev()
+    pred, _ = eng.predict(torch.as_tensor(g["qu"], dtype=torch.int32, device=d),
+                          torch.as_tensor(g["qi"], dtype=torch.int32, device=d))
+    ref = g["als_pred"]
+    assert np.abs(pred.cpu().numpy() - ref).max() < 1e-5 * np.abs(ref).max()
+    # MFITR branch: mu + b_u + b_i + b_a + (q_i + q_a) . p_u
+    mP, mQ, mQa = g["mP"], g["mQ"], g["mQa"]
+    r2 = DeviceRatings(z, z, np.zeros(0, np.float32), mP.shape[0], mQ.shape[0], d)
+    e2 = AlsEngine(r2, mP.shape[1])
+    e2.set_factors(mP, mQ)
+    qa = torch.zeros_like(e2.Q)
+    qa[:, : mP.shape[1]] = torch.as_tensor(mQa, dtype=torch.float32)
+    f = lambda a: torch.as_tensor(a, dtype=torch.float32, device=d)  # noqa: E731
+    pred, _ = e2.predict(torch.as_tensor(g["qu"], dtype=torch.int32, device=d),
+                         torch.as_tensor(g["mqi"], dtype=torch.int32, device=d),
+                         mu=float(g["mu"]), b_u=f(g["mbu"]), b_i=f(g["mbi"]),
+                         art=torch.as_tensor(g["art"], dtype=torch.int32, device=d),
+                         b_a=f(g["mba"]), Q_a=qa)
+    ref = g["mfitr_pred"]
+    assert np.abs(pred.cpu().numpy() - ref).max() < 1e-5 * np.abs(ref).max()
+
+
+def test_rmse_known_answer():
+    from paper_1108_2580_b200.device import AlsEngine, DeviceRatings
+    z = np.zeros(0, np.int32)
+    r = DeviceRatings(z, z, np.zeros(0, np.float32), 2, 2, dev())
+    eng = AlsEngine(r, 1)
+    eng.set_factors(np.array([[0.0], [2.0]]), np.array([[0.0], [5.0]]))
+    d = dev()
+    rm = eng.rmse(torch.tensor([0, 1], dtype=torch.int32, device=d),
+                  torch.tensor([0, 1], dtype=torch.int32, device=d),
+                  torch.tensor([0.0, 0.0], device=d))
+    assert abs(float(rm.item()) - np.sqrt(50.0)) < 1e-6
