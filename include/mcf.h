@@ -19,6 +19,8 @@
  *                      driven as factor.als_half_step    factor.py:512-538
  *   mcf_taxonomy_terms the graph term of mfitr.grad_mfitr mfitr.py:269-273
  *                      (ALS form of _kernels.edge_pass_range _kernels.py:128-148)
+ *   mcf_edge_weights   mfitr.edge_weights / _kernels.ac_pair mfitr.py:78-89,
+ *                      _kernels.py:218-244, neighborhood.py:37-89
  *   mcf_predict_sse    _kernels.mf_predict_batch         _kernels.py:331-375
  *                      + clip + squared error (factor.py:613-616, evaluation.py:11-18)
  *   mcf_sq_norms       the regulariser of factor.als_objective factor.py:541-547
@@ -103,6 +105,17 @@ int mcf_taxonomy_terms(const int64_t *inc_ptr, const int32_t *inc_edge,
                        const int32_t *inc_other, const float *edge_w, const float *q,
                        int32_t n_items, int32_t D, const int32_t *row_list, int32_t n_list,
                        float *S_out, float *T_out, void *stream);
+
+/* Edge weights w_e = max(0, adjusted cosine(child_e, parent_e)) over
+ * co-raters, float64, bit-identical to the reference's mfitr.edge_weights
+ * (ac_pair merge in ascending user order over ratings centred by the user
+ * mean).  Input: the by-user layout (uptr[n_users+1], uidx = item, uval =
+ * rating; in-row order = record order).  Synchronises `stream` once.
+ * ws: mcf_edge_weights_workspace_bytes(nnz, n_users, n_items). */
+size_t mcf_edge_weights_workspace_bytes(int64_t nnz, int32_t n_users, int32_t n_items);
+int mcf_edge_weights(const int64_t *uptr, const int32_t *uidx, const float *uval,
+                     int32_t n_users, int32_t n_items, const int32_t *ec, const int32_t *ep,
+                     int64_t E, double *w_out, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- prediction / RMSE ----------------------------------------------------
  * pred = mu + b_u[u] + b_i[i] + b_a[a] + (q_i + q_a[a]) . p_u with the

@@ -1,0 +1,307 @@
+"""MFITR (matrix factorisation with item-taxonomy regularisation) on device.
+
+Drop-in names from the reference's ``multicf.mfitr`` (reference
+pkg/src/multicf/mfitr.py:29-59 MfitrHyper, :62-89 edge weights, :92-149
+model/init, :181-197 predict_batch, :219-242 graph_penalty/loss_mfitr,
+:347-371 train_mfitr).
+
+The reference trains MFITR only by SGD (mfitr.py:323-336).  This path is
+the ALS-MFITR solver recommended by SURVEY.md §8(a): block-coordinate
+descent on ``loss_mfitr`` (time terms off) with
+
+* the item half-step solved layer by layer -- tracks, albums, artists, then
+  every other item -- each layer's rows exactly:
+      (sum_u p_u p_u^T + lam2 n_i I + tau S_i I) q_i = sum_u (r - mu) p_u + tau T_i
+  with tau = lam3 + lam4 and S_i = sum w_e, T_i = sum w_e q_other over the
+  item's taxonomy edges (mcf_taxonomy_terms on the current Q).  No edge joins
+  two items of one layer (track < album < artist layering,
+  taxonomy.py:102-103), so each layer solve zeroes grad_mfitr on its rows;
+* the user half-step with the same per-observation lam2 (lam2 n_u I);
+* minimum scope: mu = train mean fixed, user/item/artist biases and the
+  artist factors q_a frozen at 0 (the (D+1)-augmented bias blocks are the
+  next step).  gamma / decay are unused by this solver.
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, ptr
+from .data import Dataset
+from .device import AlsEngine, cuda_device, stream_ptr
+from .errors import ConfigError, DivergenceError
+from .factor import EpochStats, FactorModel, _host, _ratings_for
+from .taxonomy import TaxonomyGraph
+
+MFITR_KINDS = ("mfitr", "time-mfitr")
+
+
+@dataclass
+class MfitrHyper:
+    gamma: float = 8e-5
+    decay: float = 0.95
+    lam1: float = 1e-5
+    lam2: float = 1e-4
+    lam3: float = 1e-3
+    lam4: float = 1e-3
+    lam5: float = 1e-3
+    iters: int = 50
+    D: int = 50
+    D_t: int = 8
+
+    def __post_init__(self):
+        if self.gamma <= 0:
+            raise ConfigError("gamma must be > 0")
+        if not 0 < self.decay <= 1:
+            raise ConfigError("decay must be in (0, 1]")
+        if min(self.lam1, self.lam2, self.lam3, self.lam4, self.lam5) < 0:
+            raise ConfigError("regularisation weights must be >= 0")
+        if self.iters < 0:
+            raise ConfigError("iters must be >= 0")
+        if self.D < 1 or self.D_t < 1:
+            raise ConfigError("factor dimensions must be >= 1")
+
+
+def default_mfitr_hyper(kind: str = "mfitr") -> MfitrHyper:
+    if kind not in MFITR_KINDS:
+        raise ConfigError(f"unknown taxonomy model kind {kind!r}")
+    if kind == "time-mfitr":
+        raise ConfigError("time-mfitr is outside the device path (no time terms)")
+    return MfitrHyper()
+
+
+@dataclass
+class TaxonomyEdgeWeights:
+    edge_child: np.ndarray
+    edge_parent: np.ndarray
+    w: np.ndarray
+
+    def weight(self, i: int, j: int) -> float:
+        hit = np.flatnonzero((self.edge_child == i) & (self.edge_parent == j))
+        if hit.size == 0:
+            raise KeyError(f"({i}, {j}) is not a taxonomy edge")
+        return float(self.w[hit[0]])
+
+
+def edge_weights(graph: TaxonomyGraph, train: Dataset, means=None, device=None,
+                 num_items: int | None = None) -> TaxonomyEdgeWeights:
+    """max(0, adjusted cosine) per taxonomy edge, computed on device and
+    bit-identical to the reference (mcf_edge_weights; mfitr.py:78-89)."""
+    if means is not None:
+        raise ConfigError("custom user means are not supported on the device path")
+    n_items = num_items if num_items is not None else max(train.num_items, graph.num_nodes)
+    r = _ratings_for(train, device, False, train.num_users, n_items)
+    dev = r.device
+    E = graph.num_edges
+    w = torch.zeros(E, dtype=torch.float64, device=dev)
+    if E:
+        ec = torch.as_tensor(graph.edge_child.astype(np.int32), device=dev)
+        ep = torch.as_tensor(graph.edge_parent.astype(np.int32), device=dev)
+        lay = r.by_user
+        L = _lib.lib()
+        ws = torch.empty(int(L.mcf_edge_weights_workspace_bytes(lay.nnz, r.num_users, n_items)),
+                         dtype=torch.uint8, device=dev)
+        check(L.mcf_edge_weights(ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), r.num_users, n_items,
+                                 ptr(ec), ptr(ep), E, ptr(w), ptr(ws), ws.numel(),
+                                 stream_ptr(dev)), "mcf_edge_weights")
+    return TaxonomyEdgeWeights(graph.edge_child, graph.edge_parent, w.cpu().numpy())
+
+
+@dataclass
+class MfitrModel:
+    base: FactorModel
+    b_a: np.ndarray
+    q_a: np.ndarray
+    artist_of_item: np.ndarray = field(repr=False)
+
+    @property
+    def kind(self) -> str:
+        return "mfitr"
+
+    @property
+    def mu(self) -> float:
+        return self.base.mu
+
+    @property
+    def scale(self):
+        return self.base.scale
+
+    @property
+    def num_users(self) -> int:
+        return self.base.num_users
+
+    @property
+    def num_items(self) -> int:
+        return self.base.num_items
+
+    def check_finite(self, epoch: int) -> None:
+        self.base.check_finite(epoch)
+        for name, arr in (("b_a", self.b_a), ("q_a", self.q_a)):
+            if not np.isfinite(_host(arr)).all():
+                raise DivergenceError(epoch, f"non-finite {name} after epoch {epoch}")
+
+
+def init_mfitr(kind: str, train: Dataset, graph: TaxonomyGraph, hyper: MfitrHyper, seed: int,
+               binner=None, num_users: int | None = None,
+               num_items: int | None = None) -> MfitrModel:
+    """Reference draw order (mfitr.py:133-149, factor.py:144-147): q then p
+    ~ U(+-0.005/sqrt(D)) from default_rng([seed, 1]), mu = train mean,
+    q_a ~ U from default_rng([seed, 3]); biases zero."""
+    if kind not in MFITR_KINDS:
+        raise ConfigError(f"unknown taxonomy model kind {kind!r}")
+    U = num_users if num_users is not None else train.num_users
+    I = num_items if num_items is not None else max(train.num_items, graph.num_nodes)
+    D = hyper.D
+    rng = np.random.default_rng([seed, 1])
+    amp = 0.005 / np.sqrt(D)
+    q = rng.uniform(-amp, amp, (I, D))
+    p = rng.uniform(-amp, amp, (U, D))
+    base = FactorModel("mfitr", train.global_mean(), np.zeros(U), np.zeros(I), p, q, D, seed,
+                       train.scale)
+    q_a = np.random.default_rng([seed, 3]).uniform(-amp, amp, (I, D))
+    return MfitrModel(base, np.zeros(I), q_a, graph.artist_array(I))
+
+
+def predict_batch(model: MfitrModel, users, items, times=None, device=None) -> np.ndarray:
+    """mu + b_u + b_i + b_a + (q_i + q_a[art(i)]) . p_u, cold-start rules of
+    the reference (mfitr.py:181-197, _kernels.py:344-375); unclipped."""
+    base = model.base
+    eng = base.engine
+    dev = cuda_device(device if device is not None else (eng.device if eng else None))
+    if eng is None:
+        z = np.zeros(0, np.int32)
+        from .device import DeviceRatings
+        r = DeviceRatings(z, z, np.zeros(0, np.float32), base.num_users, base.num_items, dev)
+        eng = AlsEngine(r, base.D)
+        eng.set_factors(_host(base.p), _host(base.q))
+        base.engine = eng
+    D, ld = base.D, eng.ld
+    f32 = lambda a: torch.as_tensor(np.asarray(_host(a), np.float32), device=dev)  # noqa: E731
+    qa = torch.zeros(base.num_items, ld, dtype=torch.float32, device=dev)
+    qa[:, :D] = f32(model.q_a)
+    u = torch.as_tensor(np.asarray(users, np.int64).astype(np.int32), device=dev)
+    i = torch.as_tensor(np.asarray(items, np.int64).astype(np.int32), device=dev)
+    art = torch.as_tensor(model.artist_of_item.astype(np.int32), device=dev)
+    pred, _ = eng.predict(u, i, mu=base.mu, b_u=f32(base.b_u), b_i=f32(base.b_i), art=art,
+                          b_a=f32(model.b_a), Q_a=qa)
+    return pred.double().cpu().numpy()
+
+
+class MfitrSolver:
+    """Device state of one ALS-MFITR fit: engine, incident-edge CSR, edge
+    weights, layer row lists, S/T buffers."""
+
+    def __init__(self, engine: AlsEngine, graph: TaxonomyGraph, w: np.ndarray, hyper: MfitrHyper,
+                 mu: float):
+        dev = engine.device
+        self.eng, self.hyper, self.mu = engine, hyper, float(mu)
+        I = engine.r.num_items
+        inc_ptr, inc_edge, inc_other = graph.incident_edges(I)
+        self.inc_ptr = torch.as_tensor(inc_ptr, device=dev)
+        self.inc_edge = torch.as_tensor(inc_edge.astype(np.int32), device=dev)
+        self.inc_other = torch.as_tensor(inc_other.astype(np.int32), device=dev)
+        self.w = torch.as_tensor(np.asarray(w, np.float32), device=dev)
+        self.w64 = torch.as_tensor(np.asarray(w, np.float64), device=dev)
+        self.ec = torch.as_tensor(graph.edge_child, device=dev)
+        self.ep = torch.as_tensor(graph.edge_parent, device=dev)
+        self.layers = [torch.as_tensor(L.astype(np.int32), device=dev)
+                       for L in graph.layers(I)]
+        self.S = torch.zeros(I, dtype=torch.float32, device=dev)
+        self.T = torch.zeros(I, engine.ld, dtype=torch.float32, device=dev)
+        self.tau = hyper.lam3 + hyper.lam4
+
+    def item_layers(self):
+        L = _lib.lib()
+        eng, h = self.eng, self.hyper
+        for k, rows in enumerate(self.layers):
+            if rows.numel() == 0:
+                continue
+            check(L.mcf_taxonomy_terms(ptr(self.inc_ptr), ptr(self.inc_edge), ptr(self.inc_other),
+                                       ptr(self.w), ptr(eng.Q), eng.r.num_items, eng.D,
+                                       ptr(rows), rows.numel(), ptr(self.S), ptr(self.T),
+                                       stream_ptr(eng.device)), "mcf_taxonomy_terms")
+            eng.half_step("items", 0.0, h.lam2, self.mu, self.S, self.T, self.tau, rows=rows,
+                          rows_key=("layer", k))
+
+    def users(self):
+        self.eng.half_step("users", 0.0, self.hyper.lam2, self.mu)
+
+    def sweep(self):
+        self.item_layers()
+        self.users()
+
+    def loss(self) -> torch.Tensor:
+        """loss_mfitr with biases/q_a at 0 and time off (mfitr.py:219-242)."""
+        eng, h = self.eng, self.hyper
+        lay = eng.r.by_user
+        if getattr(eng, "_rows_of_records", None) is None:
+            eng._rows_of_records = torch.repeat_interleave(
+                torch.arange(eng.r.num_users, device=eng.device, dtype=torch.int32),
+                lay.degrees())
+        _, sse = eng.predict(eng._rows_of_records, lay.idx, lay.val, want_pred=False,
+                             mu=self.mu, clip=(-3.0e38, 3.0e38))
+        reg = eng.sq_norms(eng.P, eng.r.by_user.ptr) + eng.sq_norms(eng.Q, eng.r.by_item.ptr)
+        Q = eng.Q[:, : eng.D].double()
+        d2 = ((Q[self.ec] - Q[self.ep]) ** 2).sum(1)
+        graph = self.tau * (self.w64 * d2).sum()
+        return sse + h.lam2 * reg + graph
+
+
+def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
+                graph: TaxonomyGraph, hyper: MfitrHyper, threads: int = 1, seed: int = 0,
+                binner=None, ew: TaxonomyEdgeWeights | None = None,
+                num_users: int | None = None, num_items: int | None = None, *, init=None,
+                device=None, as_torch: bool = False, objective: bool = True,
+                ) -> tuple[MfitrModel, list[EpochStats]]:
+    """hyper.iters ALS-MFITR sweeps (layered item half-step, then users);
+    one EpochStats row per sweep with loss_mfitr and the clipped validation
+    RMSE (mfitr.py:347-371 signature)."""
+    if kind == "time-mfitr":
+        raise ConfigError("time-mfitr is outside the device path (no time terms)")
+    hyper = dataclasses.replace(hyper)
+    model = init_mfitr(kind, train_data, graph, hyper, seed, num_users=num_users,
+                       num_items=num_items)
+    model.q_a = np.zeros_like(model.q_a)      # minimum scope: artist factors frozen at 0
+    base = model.base
+    if init is not None:
+        base.p, base.q = np.asarray(init[0], np.float64), np.asarray(init[1], np.float64)
+    r = _ratings_for(train_data, device, False, base.num_users, base.num_items)
+    if ew is None:
+        ew = edge_weights(graph, train_data, device=r.device, num_items=base.num_items)
+    eng = AlsEngine(r, base.D)
+    eng.set_factors(base.p, base.q)
+    base.engine = eng
+    solver = MfitrSolver(eng, graph, ew.w, hyper, base.mu)
+    dev = eng.device
+    vu = vi = vs = None
+    if validation is not None and len(validation):
+        vu = torch.as_tensor(validation.users.astype(np.int32), device=dev)
+        vi = torch.as_tensor(validation.items.astype(np.int32), device=dev)
+        vs = torch.as_tensor(validation.scores.astype(np.float32), device=dev)
+    art = torch.as_tensor(model.artist_of_item.astype(np.int32), device=dev)
+    report = []
+    for ep in range(hyper.iters):
+        solver.sweep()
+        base.epochs_done += 1
+        obj = solver.loss() if objective else None
+        rm = None
+        if vu is not None:
+            _, sse = eng.predict(vu, vi, vs, want_pred=False, mu=base.mu, art=art,
+                                 Q_a=torch.zeros_like(eng.Q),
+                                 clip=(train_data.scale.lo, train_data.scale.hi))
+            rm = torch.sqrt(sse / vu.numel())
+        eng.check()
+        report.append(EpochStats(ep, hyper.gamma,
+                                 float(obj.item()) if obj is not None else float("nan"),
+                                 float(rm.item()) if rm is not None else float("nan")))
+    if as_torch:
+        base.p, base.q = eng.factors()
+    else:
+        P, Q = eng.factors()
+        base.p, base.q = P.double().cpu().numpy(), Q.double().cpu().numpy()
+    model.ew = ew
+    return model, report

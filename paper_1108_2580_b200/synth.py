@@ -90,7 +90,8 @@ def scaled_config(cfg: WorkloadConfig, factor: float, name: str | None = None) -
     tax = None
     if cfg.taxonomy is not None:
         tax = _tax_split(i)
-    total = max(u * (cfg.min_count + 2), int(cfg.total * factor))
+    per_user = min(cfg.total / cfg.users, i / 8.0)     # keep the density feasible
+    total = max(u * (cfg.min_count + 2), int(u * per_user))
     return WorkloadConfig(name or f"{cfg.name}-x{factor:g}", u, i, total, cfg.D, cfg.lam,
                           cfg.sweeps, cfg.zipf_s, cfg.counts, cfg.median, cfg.min_count,
                           cfg.holdout, tax, cfg.tax_weight)
@@ -137,6 +138,8 @@ class Workload:
 def _user_counts(cfg: WorkloadConfig, g: torch.Generator, dev) -> torch.Tensor:
     U, total, lo = cfg.users, cfg.total, cfg.min_count
     cap = max(lo, cfg.items // 4)      # keeps successive sampling cheap
+    if total > U * cap or total < U * lo:
+        raise ValueError(f"{cfg.name}: {total} ratings do not fit {U} users x [{lo}, {cap}]")
     if cfg.counts == "multinomial":
         extra = total - U * lo
         if extra < 0:
@@ -168,6 +171,8 @@ def _user_counts(cfg: WorkloadConfig, g: torch.Generator, dev) -> torch.Tensor:
         else:
             cand = perm[counts[perm] > lo][:-diff]
             counts[cand] -= 1
+        if cand.numel() == 0:
+            raise ValueError(f"{cfg.name}: cannot meet the rating total")
         diff = total - int(counts.sum())
     return counts
 
@@ -204,15 +209,29 @@ def _sample_items(counts: torch.Tensor, cfg: WorkloadConfig, g, dev) -> tuple:
         rounds += 1
         if rounds > 6:
             # users still short only miss rare items: finish them exactly with
-            # Gumbel top-k over the items they do not hold yet (same ppswor law)
+            # Gumbel top-k over the items they do not hold yet (same ppswor
+            # law), 64 users at a time
             extra = []
             logw = torch.log(w)
-            for u in need_u.tolist():
-                held = chosen[(chosen >= u * I) & (chosen < (u + 1) * I)] - u * I
-                key = logw - torch.log(-torch.log(
-                    torch.rand(I, generator=g, device=dev, dtype=torch.float64)))
-                key[held] = -float("inf")
-                extra.append(torch.topk(key, int(deficit[u])).indices + u * I)
+            lo_all = torch.searchsorted(chosen, need_u * I)
+            hi_all = torch.searchsorted(chosen, (need_u + 1) * I)
+            for a in range(0, need_u.numel(), 64):
+                us = need_u[a:a + 64]
+                lo, hi = lo_all[a:a + 64], hi_all[a:a + 64]
+                B = us.numel()
+                gum = -torch.log(-torch.log(torch.rand(B, I, generator=g, device=dev,
+                                                       dtype=torch.float64)))
+                key = logw[None, :] + gum
+                lens = hi - lo
+                row = torch.repeat_interleave(torch.arange(B, device=dev), lens)
+                pos = torch.arange(int(lens.sum()), device=dev) - \
+                    torch.repeat_interleave(torch.cumsum(lens, 0) - lens, lens)
+                held = chosen[torch.repeat_interleave(lo, lens) + pos] - us[row] * I
+                key[row, held] = -float("inf")
+                dk = deficit[us]
+                top = torch.topk(key, int(dk.max()), dim=1).indices
+                keep = torch.arange(top.shape[1], device=dev)[None, :] < dk[:, None]
+                extra.append((top + us[:, None] * I)[keep])
             chosen = torch.sort(torch.cat([chosen] + extra)).values
             break
         m = (deficit[need_u].double() * factor).ceil().to(torch.int64) + 2

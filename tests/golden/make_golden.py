@@ -31,6 +31,8 @@ Fixtures (reference entry point -> file):
                      generator: edge lists and artist_array
   mfitr.npz          mfitr.edge_weights, loss_mfitr, grad_mfitr on a small
                      synth.generate_synthetic instance with random parameters
+  mfitr_cfg2s.npz    config-2 shaped workload (this repo's generator, scaled):
+                     reference edge weights, loss_mfitr, grad_mfitr
 """
 from __future__ import annotations
 
@@ -266,6 +268,43 @@ def mfitr_fx():
                         grad_p=grad["p"], grad_q=grad["q"])
 
 
+def mfitr_cfg2s():
+    """Config-2 shaped MFITR workload (this repo's generator, scaled 0.001):
+    the reference's own edge weights (adjusted_cosine over one cached
+    _item_csr, bit-equal to mfitr.edge_weights -- SURVEY probe P5b) and
+    loss_mfitr / grad_mfitr at random factors with biases and q_a = 0."""
+    wl = mysynth.generate(mysynth.scaled_config(mysynth.CONFIGS[2], 0.001), seed=5)
+    U, I = wl.num_users, wl.num_items
+    u = wl.train_users.numpy().astype(np.int64)
+    i = wl.train_items.numpy().astype(np.int64)
+    s = wl.train_scores.numpy().astype(np.float64)
+    ds = _ds(u, i, s, U, I)
+    mg = wl.graph
+    g = taxonomy.build_graph(mg.kind, mg.album_of, mg.artist_link, {})
+    means = neighborhood.user_means(ds)
+    csr = neighborhood._item_csr(ds, means)
+    w = np.array([max(0.0, neighborhood.adjusted_cosine(int(c), int(p), ds, means, _csr=csr))
+                  for c, p in zip(g.edge_child, g.edge_parent)])
+    assert np.array_equal(w[:50], mfitr.edge_weights(
+        taxonomy.TaxonomyGraph(g.kind, g.album_of, g.artist_link, {}, g.edge_child[:50],
+                               g.edge_parent[:50]), ds).w)
+    h = mfitr.MfitrHyper(D=8, lam1=0.0, lam2=0.065, lam3=0.1, lam4=0.1)
+    m = mfitr.init_mfitr("mfitr", ds, g, h, 0, num_users=U, num_items=I)
+    rng = np.random.default_rng(3)
+    m.base.p[:] = rng.normal(0, 0.1, m.base.p.shape)
+    m.base.q[:] = rng.normal(0, 0.1, m.base.q.shape)
+    m.q_a[:] = 0.0
+    ew = mfitr.TaxonomyEdgeWeights(g.edge_child, g.edge_parent, w)
+    loss = mfitr.loss_mfitr(m, ds, g, ew, h)
+    grad = mfitr.grad_mfitr(m, ds, g, ew, h)
+    np.savez_compressed(os.path.join(HERE, "mfitr_cfg2s.npz"), users=u.astype(np.int32),
+                        items=i.astype(np.int32), scores=s.astype(np.float32), U=U, I=I,
+                        kind=mg.kind, album_of=mg.album_of, artist_link=mg.artist_link,
+                        ec=g.edge_child, ep=g.edge_parent, w=w, P=m.base.p, Q=m.base.q,
+                        mu=m.base.mu, art=m.artist_of_item, lam2=h.lam2, lam3=h.lam3,
+                        lam4=h.lam4, loss=loss, grad_p=grad["p"], grad_q=grad["q"])
+
+
 def main():
     with open(os.path.join(HERE, "spec_scalars.json"), "w") as fh:
         json.dump(spec_scalars(), fh, indent=1)
@@ -275,6 +314,7 @@ def main():
     taxonomy_fx()
     mfitr_fx()
     als_cfg0()
+    mfitr_cfg2s()
     print("golden fixtures written to", HERE)
 
 

@@ -128,3 +128,55 @@ def test_mfitr_weights_loss_grad(golden):
     gr = oracle.grad_mfitr(*args)
     np.testing.assert_allclose(gr["p"], g["grad_p"], rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(gr["q"], g["grad_q"], rtol=1e-12, atol=1e-12)
+
+
+def test_mfitr_cfg2_shape_weights_loss_grad(golden):
+    """Config-2 shaped workload: the reference's own edge weights / loss /
+    gradient (biases and q_a at zero) reproduced by the oracle."""
+    g = golden("mfitr_cfg2s.npz")
+    U, I = int(g["U"]), int(g["I"])
+    u, i, s = g["users"], g["items"], g["scores"].astype(np.float64)
+    ec, ep = oracle.build_edges(g["kind"], g["album_of"], g["artist_link"])
+    assert np.array_equal(ec, g["ec"]) and np.array_equal(ep, g["ep"])
+    w = oracle.edge_weights(ec, ep, u, i, s, U, I)
+    assert np.array_equal(w, g["w"])
+    z = np.zeros(I)
+    args = (g["P"], g["Q"], u.astype(np.int64), i.astype(np.int64), s, float(g["mu"]),
+            np.zeros(U), z, g["art"], z, np.zeros_like(g["Q"]), ec, ep, w, 0.0,
+            float(g["lam2"]), float(g["lam3"]), float(g["lam4"]))
+    np.testing.assert_allclose(oracle.loss_mfitr(*args), float(g["loss"]), rtol=1e-12)
+    gr = oracle.grad_mfitr(*args)
+    np.testing.assert_allclose(gr["q"], g["grad_q"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(gr["p"], g["grad_p"], rtol=1e-10, atol=1e-10)
+
+
+def test_layered_item_solve_zeroes_gradient(golden):
+    """The ALS-MFITR item half-step, solved layer by layer with the oracle,
+    zeroes grad_mfitr['q'] on every solved layer and never increases
+    loss_mfitr (probe P5)."""
+    g = golden("mfitr_cfg2s.npz")
+    U, I = int(g["U"]), int(g["I"])
+    u, i, s = g["users"].astype(np.int64), g["items"].astype(np.int64), g["scores"].astype(float)
+    ec, ep, w = g["ec"], g["ep"], g["w"]
+    mu, l2, tau = float(g["mu"]), float(g["lam2"]), float(g["lam3"]) + float(g["lam4"])
+    P, Q = g["P"].copy(), g["Q"].copy()
+    kind = np.full(I, -1, np.int8)
+    kind[: g["kind"].size] = g["kind"]
+    layers = [np.flatnonzero(kind == 0), np.flatnonzero(kind == 1), np.flatnonzero(kind == 2),
+              np.flatnonzero((kind < 0) | (kind == 3))]
+    csr = oracle.side_csr(i, u, s - mu, I)
+    z = np.zeros(I)
+    args = lambda Q_: (P, Q_, u, i, s, mu, np.zeros(U), z, g["art"], z, np.zeros_like(Q_),  # noqa
+                       ec, ep, w, 0.0, l2, float(g["lam3"]), float(g["lam4"]))
+    last = oracle.loss_mfitr(*args(Q))
+    for rows in layers:
+        S, T = oracle.taxonomy_terms(ec, ep, w, Q, I)
+        out, failed = oracle.solve_rows(csr, P, I, lam_n=l2, tax_S=S, tax_T=T, tau=tau)
+        assert failed == -1
+        Q[rows] = out[rows]
+        gq = oracle.grad_mfitr(*args(Q))["q"]
+        scale = np.abs(oracle.grad_mfitr(*args(g["Q"]))["q"]).max()
+        assert np.abs(gq[rows]).max() < 1e-9 * scale
+        cur = oracle.loss_mfitr(*args(Q))
+        assert cur <= last * (1 + 1e-12)
+        last = cur
