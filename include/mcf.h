@@ -65,16 +65,21 @@ int mcf_csr_build(const int32_t *keys, const int32_t *cols, const float *vals, i
 /* ---- ALS half-step --------------------------------------------------------
  * Work plan for a set of rows of one layout: the rows row_list[0..n_list)
  * (or, when row_list is NULL, rows row_lo .. row_lo + n_list), each cut into
- * chunks of at most `chunk` ratings.  Built once per (layout, row set) and
- * reused by every half-step.  Synchronises `stream` once and returns on the
- * host: totals[0] = work items, totals[1] = partial-Gram slots (chunks of
- * rows that span more than one chunk). */
+ * chunks of at most `chunk` ratings and (D <= 20 path) sorted by length,
+ * hot-row chunks first.  Built once per (layout, row set) and reused by
+ * every half-step.  Synchronises `stream` once and fills the HOST array
+ * totals[MCF_PLAN_INFO_LEN], which mcf_als_half_step takes as plan_info:
+ *   [0] work items (D > 20 paths)   [1] partial slots (D > 20 paths)
+ *   [2] tasks (D <= 20 path)        [3] partial slots (D <= 20 path)
+ *   [4] hot rows (D <= 20 path)     [5] nnz the plan was sized for */
+#define MCF_PLAN_INFO_LEN 6
 size_t mcf_als_plan_bytes(int32_t n_list, int64_t nnz, int32_t chunk);
 int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t n_list, int32_t row_lo,
                  int32_t chunk, int64_t nnz, void *plan, size_t plan_bytes, int64_t *totals,
                  void *stream);
 /* Bytes of half-step workspace: n_list row counters + `slots` partial
- * Grams at dimension D (slots = totals[1] of mcf_als_plan). */
+ * Grams at dimension D (slots = plan_info[3] when D <= 20, else
+ * plan_info[1]). */
 size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
 
 /* Solve every planned row r exactly (Cholesky of the D x D system):
@@ -88,12 +93,12 @@ size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
  * lam_n > 0.  A row whose pivot is <= 0 or non-finite is left untouched and
  * *fail_row (device int64) receives the minimum such row (-1 = none); all
  * other rows still complete (the reference's failing block stops early,
- * _kernels.py:197-203).  ws: mcf_als_workspace_bytes(n_list, totals[1], D). */
+ * _kernels.py:197-203). */
 int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
                       const float *wts, const float *fixed, float *out, int32_t D,
                       float lam_c, float lam_n, float y_shift, const float *tax_S,
                       const float *tax_T, float tau, const int32_t *row_list, int32_t n_list,
-                      int32_t row_lo, int32_t chunk, const void *plan, int64_t total_items,
+                      int32_t row_lo, int32_t chunk, const void *plan, const int64_t *plan_info,
                       int64_t *fail_row, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- MFITR taxonomy term (segmented reduction) ---------------------------

@@ -579,6 +579,350 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// pair path, D <= 20 (the hot kernel of configs 0-2)
+//
+// Row-parallel: a warp takes 16 tasks (rows, or CHUNK-long chunks of hot
+// rows) of similar length -- the plan sorts tasks by length, longest first,
+// and warps pull groups of 16 from an atomic counter (persistent grid, LPT
+// order).  A lane PAIR owns one task and walks its ratings one per step, so
+// no cross-lane reduction is ever needed.  The pair splits the lower
+// triangle of [A | b] by a cyclic block symmetry: NBK (odd) 4-wide blocks,
+// lane h holds register block p = memory block (p + h) mod NBK; the static
+// FMA list covers block pairs {p, p + d} for even p and d = 0..(NBK-1)/2
+// plus the rhs blocks y * x_p for even p, so lane 0 and lane 1 together
+// cover every entry (NBK = 5: 138 FMA per lane per rating for the 230
+// useful ones, one instruction stream, no divergence).
+//
+// Partner rows (+ rating, + weight) are gathered into a 4-stage shared
+// memory ring with 16-byte cp.async, NS-1 steps ahead of the FMAs.  After a
+// light task, the pair writes its packed Gram to shared memory and lane 0
+// solves it (thread-level Cholesky, reference row-oriented order,
+// _kernels.py:187-213); a hot-row chunk instead writes its packed partial
+// Gram to the workspace and k_als_heavy sums the chunks in chunk order and
+// solves.
+
+template <int NBK>
+struct PairCfg {
+    static_assert(NBK % 2 == 1, "odd block count");
+    static constexpr int LDK = 4 * NBK;
+    static constexpr int SLOT = LDK + 4;          // x | y, w, pad, pad
+    static constexpr int NS = 4;                  // pipeline stages
+    static constexpr int PAIRS = 16;
+    static constexpr int STAGE = PAIRS * SLOT;
+    static constexpr int HALF = (NBK + 1) / 2;    // even block starts per orbit
+    static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
+    static constexpr int RHS0 = LDK * (LDK + 1) / 2;
+    static constexpr int GRAM = RHS0 + LDK;        // packed lower + rhs
+    static constexpr int GSTRIDE = (GRAM + LDK) | 1;  // + 1/L_ii scratch, odd stride
+    static constexpr int WARP_FLOATS = NS * STAGE + PAIRS * GSTRIDE;
+    static constexpr int WARPS = 4;
+};
+
+__device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// Packed in-place Cholesky + both substitutions by ONE thread.  g holds the
+// packed lower triangle (row-major, pidx) and the rhs at rhs0; inv has room
+// for D floats.  Returns false on a non-positive / non-finite pivot.
+__device__ bool thread_solve(float *g, float *inv, int D, int rhs0, float diag_add) {
+    for (int i = 0; i < D; ++i) {
+        const int ii = pidx(i, 0);
+        for (int j = 0; j < i; ++j) {
+            const int jj = pidx(j, 0);
+            float s = g[ii + j];
+            for (int k = 0; k < j; ++k) s = fmaf(-g[ii + k], g[jj + k], s);
+            g[ii + j] = s * inv[j];
+        }
+        float s = g[ii + i] + diag_add;
+        for (int k = 0; k < i; ++k) s = fmaf(-g[ii + k], g[ii + k], s);
+        if (!(s > 0.f) || !isfinite(s)) return false;
+        const float l = sqrtf(s);
+        g[ii + i] = l;
+        inv[i] = 1.f / l;
+    }
+    for (int i = 0; i < D; ++i) {
+        const int ii = pidx(i, 0);
+        float b = g[rhs0 + i];
+        for (int k = 0; k < i; ++k) b = fmaf(-g[ii + k], g[rhs0 + k], b);
+        g[rhs0 + i] = b * inv[i];
+    }
+    for (int i = D - 1; i >= 0; --i) {
+        float b = g[rhs0 + i];
+        for (int k = i + 1; k < D; ++k) b = fmaf(-g[pidx(k, i)], g[rhs0 + k], b);
+        g[rhs0 + i] = b * inv[i];
+    }
+    return true;
+}
+
+struct PairPlan {
+    const int32_t *task_row;
+    const int64_t *task_k0;
+    const int32_t *task_n;
+    const int32_t *task_slot;
+    int64_t n_tasks;
+    const int32_t *sorted_j;   // heavy list indices first
+    const int32_t *hoff;       // [n_list + 1] first chunk slot of list entry j
+    int64_t n_heavy;
+    int32_t *group_counter;
+};
+
+// regularise + solve one packed system and write the output row; returns
+// false (and reports) on failure.  Called by one thread.
+__device__ void finish_row(const AlsParams &p, float *g, float *inv, int rhs0, int r, int64_t n) {
+    const int D = p.D;
+    const float S = p.tax_S ? p.tax_S[r] : 0.f;
+    float *orow = p.out + (size_t)r * p.ld;
+    if (n == 0 && S == 0.f) {
+        if (p.lam_c > 0.f || p.lam_n > 0.f) {
+            for (int i = 0; i < p.ld; ++i) orow[i] = 0.f;
+        } else {
+            report_fail(p.fail, r);
+        }
+        return;
+    }
+    const float diag = p.lam_c + p.lam_n * (float)n + p.tau * S;
+    if (p.tax_T)
+        for (int i = 0; i < D; ++i) g[rhs0 + i] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], g[rhs0 + i]);
+    if (!thread_solve(g, inv, D, rhs0, diag)) {
+        report_fail(p.fail, r);
+        return;
+    }
+    for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? g[rhs0 + i] : 0.f;
+}
+
+template <int NBK, bool HAS_W>
+__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams p, PairPlan q) {
+    using C = PairCfg<NBK>;
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = lane >> 1, h = lane & 1;
+    float *ring = smem + warp * C::WARP_FLOATS;
+    float *gbuf = ring + C::NS * C::STAGE;
+    float *my_g = gbuf + pair * C::GSTRIDE;
+    const int nb_real = (p.D + 3) / 4;   // memory blocks that exist in `fixed`
+    int boff[NBK];                        // smem offset of register block p
+#pragma unroll
+    for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
+    const int64_t n_groups = (q.n_tasks + C::PAIRS - 1) / C::PAIRS;
+
+    for (;;) {
+        int64_t grp = 0;
+        if (lane == 0) grp = atomicAdd(q.group_counter, 1);
+        grp = __shfl_sync(FULL, grp, 0);
+        if (grp >= n_groups) break;
+        const int64_t task = grp * C::PAIRS + pair;
+        int row = 0, slot = -1, n = 0;
+        int64_t k0 = 0;
+        if (task < q.n_tasks) {
+            row = q.task_row[task];
+            k0 = q.task_k0[task];
+            n = q.task_n[task];
+            slot = q.task_slot[task];
+        }
+        int nmax = n;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, o));
+
+        float acc[C::NACC];
+#pragma unroll
+        for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
+
+        // issue the gathers of step s (idx already known)
+        auto issue = [&](int s, int col) {
+            float *sl = ring + (s % C::NS) * C::STAGE + pair * C::SLOT;
+            const bool ok = col >= 0;
+            const float *src = p.fixed + (size_t)(ok ? col : 0) * p.ld;
+#pragma unroll
+            for (int b = h; b < NBK; b += 2)
+                cp_async16(sl + 4 * b, src + 4 * b, (ok && b < nb_real) ? 16 : 0);
+            if (h == 0) {
+                const float *vs = p.val + (ok ? k0 + s : 0);
+                unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sl + C::LDK));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(vs),
+                             "r"(ok ? 4 : 0));
+            } else if (HAS_W) {
+                const float *ws = p.wts + (ok ? k0 + s : 0);
+                unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sl + C::LDK + 1));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(ws),
+                             "r"(ok ? 4 : 0));
+            }
+            cp_async_commit();
+        };
+        int nidx = n > 0 ? p.idx[k0] : -1;
+#pragma unroll
+        for (int s = 0; s < C::NS - 1; ++s) {
+            if (s < nmax) issue(s, nidx);
+            else cp_async_commit();
+            nidx = (s + 1 < n) ? p.idx[k0 + s + 1] : -1;
+        }
+        for (int t = 0; t < nmax; ++t) {
+            const int sn = t + C::NS - 1;
+            if (sn < nmax) issue(sn, nidx);
+            else cp_async_commit();
+            nidx = (sn + 1 < n) ? p.idx[k0 + sn + 1] : -1;
+            cp_async_wait<C::NS - 1>();
+            __syncwarp();
+            const float *sl = ring + (t % C::NS) * C::STAGE + pair * C::SLOT;
+            float4 xr[NBK];
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(sl + boff[b]);
+            float y = sl[C::LDK] - p.y_shift;
+            float4 xa[NBK];
+#pragma unroll
+            for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
+            if (HAS_W) {
+                const float w = sl[C::LDK + 1];
+#pragma unroll
+                for (int b = 0; b < NBK; ++b) {
+                    xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
+                }
+            }
+            int e = 0;
+#pragma unroll
+            for (int d = 0; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+                for (int b = 0; b < NBK; b += 2) {
+                    const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+                    const float4 bq = xr[(b + d) % NBK];
+                    const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
+                    if (d == 0) {
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+#pragma unroll
+                            for (int nn = 0; nn <= m; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+#pragma unroll
+                            for (int nn = 0; nn < 4; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < NBK; b += 2) {
+                const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+#pragma unroll
+                for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
+            }
+            __syncwarp();
+        }
+        cp_async_wait<0>();
+
+        // scatter the lane's accumulators into the pair's packed [A | b]
+        {
+            int e = 0;
+#pragma unroll
+            for (int d = 0; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+                for (int b = 0; b < NBK; b += 2) {
+                    const int A = (b + h) % NBK, B = (b + d + h) % NBK;
+                    if (d == 0) {
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+#pragma unroll
+                            for (int nn = 0; nn <= m; ++nn, ++e) my_g[pidx(4 * A + m, 4 * A + nn)] = acc[e];
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+#pragma unroll
+                            for (int nn = 0; nn < 4; ++nn, ++e) {
+                                const int r_ = 4 * A + m, c_ = 4 * B + nn;
+                                my_g[r_ >= c_ ? pidx(r_, c_) : pidx(c_, r_)] = acc[e];
+                            }
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < NBK; b += 2) {
+                const int A = (b + h) % NBK;
+#pragma unroll
+                for (int m = 0; m < 4; ++m, ++e) my_g[C::RHS0 + 4 * A + m] = acc[e];
+            }
+        }
+        __syncwarp();
+        if (task < q.n_tasks) {
+            if (slot >= 0) {
+                float *dst = p.partials + (size_t)slot * C::GRAM;
+                for (int i = h; i < C::GRAM; i += 2) dst[i] = my_g[i];
+            } else if (h == 0) {
+                finish_row(p, my_g, my_g + C::GRAM, C::RHS0, row, n);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Hot rows: one warp per row sums its chunk partials in chunk order, then
+// lane 0 solves.
+template <int NBK>
+__global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
+    using C = PairCfg<NBK>;
+    __shared__ float g[4][C::GSTRIDE];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t hr = (int64_t)blockIdx.x * 4 + warp;
+    if (hr >= q.n_heavy) return;
+    const int j = q.sorted_j[hr];
+    const int r = p.row_list ? p.row_list[j] : p.row_lo + j;
+    const int s0 = q.hoff[j], s1 = q.hoff[j + 1];
+    for (int i = lane; i < C::GRAM; i += 32) {
+        float a = 0.f;
+        for (int s = s0; s < s1; ++s) a += __ldcg(p.partials + (size_t)s * C::GRAM + i);
+        g[warp][i] = a;
+    }
+    __syncwarp();
+    if (lane == 0) finish_row(p, g[warp], g[warp] + C::GRAM, C::RHS0, r, p.ptr[r + 1] - p.ptr[r]);
+}
+
+// --- plan kernels for the pair path
+__global__ void k_pair_keys(const int64_t *ptr, const int32_t *row_list, int32_t n_list,
+                            int32_t row_lo, int32_t chunk, int32_t *keys, int32_t *jcols,
+                            float *dvals, int32_t *hch) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= n_list; j += gridDim.x * blockDim.x) {
+        if (j == n_list) {
+            hch[j] = 0;
+            continue;
+        }
+        const int r = row_list ? row_list[j] : row_lo + j;
+        const int64_t n = ptr[r + 1] - ptr[r];
+        keys[j] = n > chunk ? 0 : (int32_t)(chunk + 1 - n);
+        jcols[j] = j;
+        dvals[j] = 0.f;
+        hch[j] = n > chunk ? (int32_t)((n + chunk - 1) / chunk) : 0;
+    }
+}
+
+__global__ void k_pair_fill(const int64_t *ptr, const int32_t *row_list, int32_t n_list,
+                            int32_t row_lo, int32_t chunk, const int32_t *sorted_j,
+                            const int64_t *kptr, const int32_t *hoff, int32_t *task_row,
+                            int64_t *task_k0, int32_t *task_n, int32_t *task_slot) {
+    const int64_t nh = kptr[1];               // rows with key 0 = hot rows
+    const int64_t H = hoff[n_list];           // hot chunks (tasks 0..H-1)
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_list; q += gridDim.x * blockDim.x) {
+        const int j = sorted_j[q];
+        const int r = row_list ? row_list[j] : row_lo + j;
+        const int64_t a = ptr[r], n = ptr[r + 1] - a;
+        if (q < nh) {
+            const int s0 = hoff[j];
+            const int nch = hoff[j + 1] - s0;
+            for (int c = 0; c < nch; ++c) {
+                const int t = s0 + c;
+                task_row[t] = r;
+                task_k0[t] = a + (int64_t)c * chunk;
+                task_n[t] = (int32_t)min((int64_t)chunk, n - (int64_t)c * chunk);
+                task_slot[t] = t;
+            }
+        } else {
+            const int64_t t = H + (q - nh);
+            task_row[t] = r;
+            task_k0[t] = a;
+            task_n[t] = (int32_t)n;
+            task_slot[t] = -1;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // dispatch
 
@@ -639,24 +983,88 @@ size_t pstride_of(int D) {
 }
 
 struct PlanLayout {
+    // warp / CTA paths (D > 20)
     int32_t *items, *slots, *item_row;
     void *scan_tmp;
     size_t scan_bytes;
+    // pair path (D <= 20)
+    int32_t *keys, *jcols, *sorted_j, *hch;
+    float *dvals, *dvals_out;
+    int64_t *kptr;
+    void *csr_ws;
+    size_t csr_bytes;
+    int32_t *task_row, *task_n, *task_slot;
+    int64_t *task_k0;
 };
 
 PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_t chunk,
                       size_t *need) {
     Carve c(buf, cap);
     PlanLayout L;
-    L.items = c.take<int32_t>((size_t)n_list + 1);
-    L.slots = c.take<int32_t>((size_t)n_list + 1);
-    const int64_t max_items = (int64_t)n_list + ceil_div(nnz, chunk) + 1;
-    L.item_row = c.take<int32_t>((size_t)max_items);
+    const size_t nl = (size_t)n_list;
+    L.items = c.take<int32_t>(nl + 1);
+    L.slots = c.take<int32_t>(nl + 1);
+    L.hch = c.take<int32_t>(nl + 1);
     L.scan_bytes = scan_exclusive<int32_t>(nullptr, nullptr, (int64_t)n_list + 1, nullptr, 0,
                                            nullptr, nullptr);
     L.scan_tmp = c.take<char>(L.scan_bytes + 256);
+    L.keys = c.take<int32_t>(nl);
+    L.jcols = c.take<int32_t>(nl);
+    L.sorted_j = c.take<int32_t>(nl);
+    L.dvals = c.take<float>(nl);
+    L.dvals_out = c.take<float>(nl);
+    L.kptr = c.take<int64_t>((size_t)chunk + 3);
+    L.csr_bytes = mcf_csr_workspace_bytes(n_list, chunk + 2);
+    L.csr_ws = c.take<char>(L.csr_bytes);
+    const int64_t max_items = (int64_t)n_list + ceil_div(nnz, chunk) + 1;
+    L.task_row = c.take<int32_t>((size_t)max_items);
+    L.task_n = c.take<int32_t>((size_t)max_items);
+    L.task_slot = c.take<int32_t>((size_t)max_items);
+    L.task_k0 = c.take<int64_t>((size_t)max_items);
+    L.item_row = c.take<int32_t>((size_t)max_items);
     *need = c.used;
     return L;
+}
+
+bool use_pair(int D) { return D <= 20; }
+
+template <int NBK, bool W>
+int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
+    using C = PairCfg<NBK>;
+    const size_t smem = sizeof(float) * C::WARP_FLOATS * C::WARPS;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_als_pair<NBK, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, W>, C::WARPS * 32,
+                                                  smem);
+    const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
+    const int64_t want = ceil_div(groups, C::WARPS);
+    const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
+    if (grid > 0) k_als_pair<NBK, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
+    if (q.n_heavy > 0)
+        k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
+    return check_launch("mcf_als_half_step(pair)");
+}
+
+template <bool W>
+int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
+    const int nb = (p.D + 3) / 4;
+    if (nb <= 1) return launch_pair<1, W>(p, q, s);
+    if (nb <= 3) return launch_pair<3, W>(p, q, s);
+    return launch_pair<5, W>(p, q, s);
+}
+
+size_t pair_gram(int D) {
+    const int nb = (D + 3) / 4;
+    const int nbk = nb <= 1 ? 1 : nb <= 3 ? 3 : 5;
+    const int ldk = 4 * nbk;
+    return (size_t)(ldk * (ldk + 1) / 2 + ldk);
 }
 
 }  // namespace
@@ -697,24 +1105,51 @@ extern "C" int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t
         return MCF_E_WORKSPACE;
     }
     if (n_list > 0) k_plan_fill<<<grid, 256, 0, s>>>(L.items, n_list, L.item_row);
-    int32_t tot[2];
+    // pair path: tasks sorted by length (hot-row chunks first), LPT order
+    k_pair_keys<<<grid, 256, 0, s>>>(ptr, row_list, n_list, row_lo, chunk, L.keys, L.jcols,
+                                     L.dvals, L.hch);
+    scan_exclusive<int32_t>(L.hch, L.hch, (int64_t)n_list + 1, L.scan_tmp, L.scan_bytes, s, &err);
     int rc;
+    if (n_list > 0) {
+        if ((rc = mcf_csr_build(L.keys, L.jcols, L.dvals, n_list, chunk + 2, L.kptr, L.sorted_j,
+                                L.dvals_out, nullptr, L.csr_ws, L.csr_bytes, stream)))
+            return rc;
+        k_pair_fill<<<grid, 256, 0, s>>>(ptr, row_list, n_list, row_lo, chunk, L.sorted_j, L.kptr,
+                                         L.hch, L.task_row, L.task_k0, L.task_n, L.task_slot);
+    } else {
+        if ((rc = cuda_status(cudaMemsetAsync(L.kptr, 0, sizeof(int64_t) * 2, s), "memset")))
+            return rc;
+    }
+    int32_t tot[2];
+    int64_t nh = 0;
+    int32_t H = 0;
     if ((rc = cuda_status(cudaMemcpyAsync(&tot[0], L.items + n_list, sizeof(int32_t),
                                           cudaMemcpyDeviceToHost, s), "memcpy")))
         return rc;
     if ((rc = cuda_status(cudaMemcpyAsync(&tot[1], L.slots + n_list, sizeof(int32_t),
                                           cudaMemcpyDeviceToHost, s), "memcpy")))
         return rc;
+    if ((rc = cuda_status(cudaMemcpyAsync(&nh, L.kptr + 1, sizeof(int64_t),
+                                          cudaMemcpyDeviceToHost, s), "memcpy")))
+        return rc;
+    if ((rc = cuda_status(cudaMemcpyAsync(&H, L.hch + n_list, sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, s), "memcpy")))
+        return rc;
     if ((rc = cuda_status(cudaStreamSynchronize(s), "sync"))) return rc;
-    totals[0] = tot[0];
-    totals[1] = tot[1];
+    if (n_list == 0) nh = 0;
+    totals[0] = tot[0];               // warp/CTA path work items
+    totals[1] = tot[1];               // warp/CTA path partial slots
+    totals[2] = H + (n_list - nh);    // pair path tasks
+    totals[3] = H;                    // pair path partial slots (hot-row chunks)
+    totals[4] = nh;                   // hot rows
+    totals[5] = nnz;                  // plan geometry
     return check_launch("mcf_als_plan");
 }
 
 extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D) {
     if (D < 1 || n_list < 0 || slots < 0) return 0;
-    return align_up(sizeof(int32_t) * (size_t)n_list, 256) +
-           sizeof(float) * (size_t)slots * pstride_of(D);
+    const size_t per = use_pair(D) ? pair_gram(D) : pstride_of(D);
+    return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + sizeof(float) * (size_t)slots * per;
 }
 
 extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
@@ -722,13 +1157,13 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
                                  float lam_c, float lam_n, float y_shift, const float *tax_S,
                                  const float *tax_T, float tau, const int32_t *row_list,
                                  int32_t n_list, int32_t row_lo, int32_t chunk, const void *plan,
-                                 int64_t total_items, int64_t *fail_row, void *ws,
+                                 const int64_t *plan_info, int64_t *fail_row, void *ws,
                                  size_t ws_bytes, void *stream) {
     if (D < 1 || D > 128) {
         set_error("mcf_als_half_step: D must be in [1, 128]");
         return MCF_E_UNSUPPORTED;
     }
-    if (!ptr || !fixed || !out || !plan || !fail_row || n_list < 0 || total_items < 0 ||
+    if (!ptr || !fixed || !out || !plan || !plan_info || !fail_row || n_list < 0 ||
         chunk < BATCH || chunk % BATCH) {
         set_error("mcf_als_half_step: invalid arguments");
         return MCF_E_ARG;
@@ -737,9 +1172,11 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
     int rc;
     if ((rc = cuda_status(cudaMemsetAsync(fail_row, 0xff, sizeof(int64_t), s), "memset")))
         return rc;
-    if (n_list == 0 || total_items == 0) return MCF_OK;
+    const int64_t total_items = plan_info[0];
+    if (n_list == 0) return MCF_OK;
     size_t need_plan = 0;
-    PlanLayout L = carve_plan(const_cast<void *>(plan), SIZE_MAX, n_list, 0, chunk, &need_plan);
+    PlanLayout L = carve_plan(const_cast<void *>(plan), SIZE_MAX, n_list, plan_info[5], chunk,
+                              &need_plan);
     AlsParams p{};
     p.ptr = ptr; p.idx = idx; p.val = val; p.wts = wts; p.fixed = fixed; p.out = out;
     p.D = D; p.ld = mcf_factor_ld(D);
@@ -753,7 +1190,7 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
     p.fail = reinterpret_cast<unsigned long long *>(fail_row);
     // workspace: counters [n_list] + partial slots
     Carve c(ws, ws_bytes);
-    p.counters = c.take<int32_t>((size_t)n_list);
+    p.counters = c.take<int32_t>((size_t)n_list + 64);
     p.partials = c.take<float>(0);
     const size_t fixed_part = c.used;
     if (!ws || ws_bytes < fixed_part) {
@@ -761,8 +1198,23 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
         return MCF_E_WORKSPACE;
     }
     p.partials = reinterpret_cast<float *>(static_cast<char *>(ws) + fixed_part);
-    if ((rc = cuda_status(cudaMemsetAsync(p.counters, 0, sizeof(int32_t) * (size_t)n_list, s),
+    if ((rc = cuda_status(cudaMemsetAsync(p.counters, 0, sizeof(int32_t) * ((size_t)n_list + 64), s),
                           "memset")))
         return rc;
+    if (use_pair(D)) {
+        PairPlan q;
+        q.task_row = L.task_row;
+        q.task_k0 = L.task_k0;
+        q.task_n = L.task_n;
+        q.task_slot = L.task_slot;
+        q.n_tasks = plan_info[2];
+        q.sorted_j = L.sorted_j;
+        q.hoff = L.hch;
+        q.n_heavy = plan_info[4];
+        q.group_counter = p.counters + n_list;
+        if (q.n_tasks == 0) return MCF_OK;
+        return wts ? dispatch_pair<true>(p, q, s) : dispatch_pair<false>(p, q, s);
+    }
+    if (total_items == 0) return MCF_OK;
     return wts ? dispatch<true>(p, s) : dispatch<false>(p, s);
 }

@@ -101,8 +101,8 @@ __global__ void k_user_means(const int64_t *uptr, const float *uval, int32_t n_u
     if (u >= n_users) return;
     double s = 0.0;
     const int64_t a = uptr[u], b = uptr[u + 1];
-    for (int64_t k = a; k < b; ++k) s += (double)uval[k];
-    mean[u] = b > a ? s / (double)(b - a) : 0.0;
+    for (int64_t k = a; k < b; ++k) s = __dadd_rn(s, (double)uval[k]);
+    mean[u] = b > a ? __ddiv_rn(s, (double)(b - a)) : 0.0;
 }
 
 __global__ void k_rows_of(const int64_t *ptr, int32_t n_rows, int32_t *row_of) {
@@ -115,7 +115,7 @@ __global__ void k_centered(const int32_t *perm, const float *uval, const int32_t
                            const double *mean, int64_t nnz, double *cv) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
          k += (int64_t)gridDim.x * blockDim.x)
-        cv[k] = (double)uval[perm[k]] - mean[users_sorted[k]];
+        cv[k] = __dsub_rn((double)uval[perm[k]], mean[users_sorted[k]]);
 }
 
 __device__ __forceinline__ int64_t gallop(const int32_t *a, int64_t lo, int64_t hi, int32_t x) {
@@ -153,15 +153,17 @@ __global__ void k_edge_ac(const int32_t *ec, const int32_t *ep, int64_t E, const
             if (l0 < l1 && iuser[l0] == uk) {
                 const double x = swap ? cv[l0] : cv[k];   // child's value
                 const double y = swap ? cv[k] : cv[l0];   // parent's value
-                num += x * y;
-                di += x * x;
-                dj += y * y;
+                // explicit roundings: no FMA contraction, the reference
+                // (numba, no fastmath) rounds every product and sum
+                num = __dadd_rn(num, __dmul_rn(x, y));
+                di = __dadd_rn(di, __dmul_rn(x, x));
+                dj = __dadd_rn(dj, __dmul_rn(y, y));
                 ++n;
                 ++l0;
             }
         }
         if (n > 0 && di != 0.0 && dj != 0.0) {
-            const double s = num / sqrt(di * dj);
+            const double s = __ddiv_rn(num, __dsqrt_rn(__dmul_rn(di, dj)));
             out = s > 0.0 ? s : 0.0;
         }
     }

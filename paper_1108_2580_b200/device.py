@@ -22,6 +22,7 @@ from ._lib import check, ptr
 from .errors import ConfigError, DeviceError, SingularSystemError
 
 DEFAULT_CHUNK = 2048
+PLAN_INFO_LEN = 6   # MCF_PLAN_INFO_LEN
 
 
 def cuda_device(device=None) -> torch.device:
@@ -62,18 +63,18 @@ class SideLayout:
         return self.ptr[1:] - self.ptr[:-1]
 
     def plan(self, rows: torch.Tensor | None = None, key=None, chunk: int = DEFAULT_CHUNK):
-        """(plan buffer, total work items, partial slots) for all rows, or for
-        the int32 row list `rows` (cached under `key`)."""
+        """(plan buffer, plan_info, row list, n_list) for all rows, or for the
+        int32 row list `rows` (cached under `key`)."""
         k = (key, chunk) if rows is not None else ("all", chunk)
         if k not in self._plans:
             L = _lib.lib()
             n_list = self.n_rows if rows is None else int(rows.numel())
             buf = torch.empty(int(L.mcf_als_plan_bytes(n_list, self.nnz, chunk)), dtype=torch.uint8,
                               device=self.device)
-            totals = (_lib.c_i64 * 2)()
+            info = (_lib.c_i64 * PLAN_INFO_LEN)()
             check(L.mcf_als_plan(ptr(self.ptr), ptr(rows), n_list, 0, chunk, self.nnz, ptr(buf),
-                                 buf.numel(), totals, stream_ptr(self.device)), "mcf_als_plan")
-            self._plans[k] = (buf, int(totals[0]), int(totals[1]), rows, n_list)
+                                 buf.numel(), info, stream_ptr(self.device)), "mcf_als_plan")
+            self._plans[k] = (buf, info, rows, n_list)
         return self._plans[k]
 
 
@@ -177,13 +178,14 @@ class AlsEngine:
         out = self.P if side == "users" else self.Q
         if fixed is None:
             fixed = self.Q if side == "users" else self.P
-        buf, total, slots, rl, n_list = lay.plan(rows, rows_key, self.chunk)
+        buf, info, rl, n_list = lay.plan(rows, rows_key, self.chunk)
+        slots = info[3] if self.D <= 20 else info[1]
         ws = self._workspace(side, n_list, slots, rows_key)
         w = self._wts.get(side)
         check(_lib.lib().mcf_als_half_step(
             ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(w), ptr(fixed), ptr(out), self.D,
             float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
-            ptr(rl), n_list, 0, self.chunk, ptr(buf), total, ptr(self.fail), ptr(ws), ws.numel(),
+            ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(self.fail), ptr(ws), ws.numel(),
             stream_ptr(self.device)), "mcf_als_half_step")
         acc = self._fail_acc[0:1] if side == "items" else self._fail_acc[1:2]
         torch.where(acc < 0, self.fail, acc, out=acc)
