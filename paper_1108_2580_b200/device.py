@@ -115,6 +115,38 @@ class DeviceRatings:
         raise ConfigError(f"side must be 'users' or 'items', got {side!r}")
 
 
+class LayoutSolver:
+    """mcf_als_half_step over one SideLayout with caller-chosen fixed / out
+    tables (used by AlsEngine and by the row-sharded multi-GPU runner)."""
+
+    def __init__(self, D: int, chunk: int = DEFAULT_CHUNK):
+        self.D, self.chunk = int(D), int(chunk)
+        self._ws = {}
+        self.fail = None
+
+    def solve(self, lay: SideLayout, fixed: torch.Tensor, out: torch.Tensor, lam_c=0.0, lam_n=0.0,
+              y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
+              fail: torch.Tensor | None = None):
+        dev = lay.device
+        if fail is None:
+            if self.fail is None:
+                self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
+            fail = self.fail
+        buf, info, rl, n_list = lay.plan(rows, rows_key, self.chunk)
+        slots = info[3] if self.D <= 20 else info[1]
+        k = (id(lay), rows_key)
+        need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
+        if k not in self._ws or self._ws[k].numel() < need:
+            self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        ws = self._ws[k]
+        check(_lib.lib().mcf_als_half_step(
+            ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(wts), ptr(fixed), ptr(out), self.D,
+            float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
+            ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail), ptr(ws), ws.numel(),
+            stream_ptr(dev)), "mcf_als_half_step")
+        return fail
+
+
 class AlsEngine:
     """Factor tables + plans + workspaces for repeated half-steps of one
     ratings split.  All calls are asynchronous on the current stream; row
@@ -131,7 +163,7 @@ class AlsEngine:
         self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
         # first failing row per side since the last check()
         self._fail_acc = torch.full((2,), -1, dtype=torch.int64, device=dev)
-        self._ws = {}
+        self._solver = LayoutSolver(D, chunk)
         self._wts = {}
         self._red = None
 
@@ -164,13 +196,6 @@ class AlsEngine:
             self._wts[side] = w[lay.perm.long()]
 
     # -- half-step -----------------------------------------------------------
-    def _workspace(self, side, n_list, slots, key):
-        k = (side, key)
-        need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
-        if k not in self._ws or self._ws[k].numel() < need:
-            self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
-        return self._ws[k]
-
     def half_step(self, side: str, lam_c: float = 0.0, lam_n: float = 0.0, y_shift: float = 0.0,
                   tax_S=None, tax_T=None, tau: float = 0.0, rows: torch.Tensor | None = None,
                   rows_key=None, fixed: torch.Tensor | None = None):
@@ -178,15 +203,8 @@ class AlsEngine:
         out = self.P if side == "users" else self.Q
         if fixed is None:
             fixed = self.Q if side == "users" else self.P
-        buf, info, rl, n_list = lay.plan(rows, rows_key, self.chunk)
-        slots = info[3] if self.D <= 20 else info[1]
-        ws = self._workspace(side, n_list, slots, rows_key)
-        w = self._wts.get(side)
-        check(_lib.lib().mcf_als_half_step(
-            ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(w), ptr(fixed), ptr(out), self.D,
-            float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
-            ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(self.fail), ptr(ws), ws.numel(),
-            stream_ptr(self.device)), "mcf_als_half_step")
+        self._solver.solve(lay, fixed, out, lam_c, lam_n, y_shift, tax_S, tax_T, tau, rows,
+                           rows_key, self._wts.get(side), self.fail)
         acc = self._fail_acc[0:1] if side == "items" else self._fail_acc[1:2]
         torch.where(acc < 0, self.fail, acc, out=acc)
         return out
