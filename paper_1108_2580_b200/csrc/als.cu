@@ -608,49 +608,76 @@ struct PairCfg {
     static_assert(NBK % 2 == 1, "odd block count");
     static constexpr int LDK = 4 * NBK;
     static constexpr int SLOT = LDK + 4;          // x | y, w, pad, pad
-    static constexpr int NS = 4;                  // pipeline stages
+    static constexpr int NS = 8;                  // pipeline stages (7 steps of lead)
     static constexpr int PAIRS = 16;
     static constexpr int STAGE = PAIRS * SLOT;
     static constexpr int HALF = (NBK + 1) / 2;    // even block starts per orbit
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
     static constexpr int RHS0 = LDK * (LDK + 1) / 2;
     static constexpr int GRAM = RHS0 + LDK;        // packed lower + rhs
-    static constexpr int GSTRIDE = (GRAM + LDK) | 1;  // + 1/L_ii scratch, odd stride
-    static constexpr int WARP_FLOATS = NS * STAGE + PAIRS * GSTRIDE;
+    static constexpr int GSTRIDE = GRAM | 1;       // odd stride: conflict-free per-lane rows
+    static constexpr int RING = NS * STAGE;
+    static constexpr int SOLVE = PAIRS * GSTRIDE;
+    // the gather ring and the solve buffer are never live at the same time
+    static constexpr int WARP_FLOATS = RING > SOLVE ? RING : SOLVE;
     static constexpr int WARPS = 4;
+    static constexpr int PF = 64;                  // L2 prefetch distance (ratings)
 };
 
-__device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
+__device__ __forceinline__ constexpr int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
 
-// Packed in-place Cholesky + both substitutions by ONE thread.  g holds the
-// packed lower triangle (row-major, pidx) and the rhs at rhs0; inv has room
-// for D floats.  Returns false on a non-positive / non-finite pivot.
-__device__ bool thread_solve(float *g, float *inv, int D, int rhs0, float diag_add) {
-    for (int i = 0; i < D; ++i) {
-        const int ii = pidx(i, 0);
-        for (int j = 0; j < i; ++j) {
-            const int jj = pidx(j, 0);
-            float s = g[ii + j];
-            for (int k = 0; k < j; ++k) s = fmaf(-g[ii + k], g[jj + k], s);
-            g[ii + j] = s * inv[j];
+// Packed Cholesky + both substitutions by ONE thread, unrolled to LDK with
+// row i held in registers (one shared-memory load per FMA).  g: packed
+// lower triangle (pidx) and rhs at RHS0 (overwritten with the solution).
+template <int LDK>
+__device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add) {
+    constexpr int RHS0 = LDK * (LDK + 1) / 2;
+    float inv[LDK];
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < LDK; ++i) {
+        if (i < D) {
+            float r[LDK];
+#pragma unroll
+            for (int j = 0; j <= i; ++j) r[j] = g[pidx(i, j)];
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                float t = r[j];
+#pragma unroll
+                for (int k = 0; k < j; ++k) t = fmaf(-r[k], g[pidx(j, k)], t);
+                r[j] = t * inv[j];
+                g[pidx(i, j)] = r[j];
+            }
+            float d = r[i] + diag_add;
+#pragma unroll
+            for (int k = 0; k < i; ++k) d = fmaf(-r[k], r[k], d);
+            ok = ok && (d > 0.f) && isfinite(d);
+            const float l = sqrtf(d);
+            g[pidx(i, i)] = l;
+            inv[i] = 1.f / l;
         }
-        float s = g[ii + i] + diag_add;
-        for (int k = 0; k < i; ++k) s = fmaf(-g[ii + k], g[ii + k], s);
-        if (!(s > 0.f) || !isfinite(s)) return false;
-        const float l = sqrtf(s);
-        g[ii + i] = l;
-        inv[i] = 1.f / l;
     }
-    for (int i = 0; i < D; ++i) {
-        const int ii = pidx(i, 0);
-        float b = g[rhs0 + i];
-        for (int k = 0; k < i; ++k) b = fmaf(-g[ii + k], g[rhs0 + k], b);
-        g[rhs0 + i] = b * inv[i];
+    if (!ok) return false;
+    float y[LDK];
+#pragma unroll
+    for (int i = 0; i < LDK; ++i) {
+        if (i < D) {
+            float t = g[RHS0 + i];
+#pragma unroll
+            for (int k = 0; k < i; ++k) t = fmaf(-g[pidx(i, k)], y[k], t);
+            y[i] = t * inv[i];
+        }
     }
-    for (int i = D - 1; i >= 0; --i) {
-        float b = g[rhs0 + i];
-        for (int k = i + 1; k < D; ++k) b = fmaf(-g[pidx(k, i)], g[rhs0 + k], b);
-        g[rhs0 + i] = b * inv[i];
+#pragma unroll
+    for (int i = LDK - 1; i >= 0; --i) {
+        if (i < D) {
+            float t = y[i];
+#pragma unroll
+            for (int k = i + 1; k < LDK; ++k)
+                if (k < D) t = fmaf(-g[pidx(k, i)], y[k], t);
+            y[i] = t * inv[i];
+            g[RHS0 + i] = y[i];
+        }
     }
     return true;
 }
@@ -667,9 +694,10 @@ struct PairPlan {
     int32_t *group_counter;
 };
 
-// regularise + solve one packed system and write the output row; returns
-// false (and reports) on failure.  Called by one thread.
-__device__ void finish_row(const AlsParams &p, float *g, float *inv, int rhs0, int r, int64_t n) {
+// regularise + solve one packed system (one thread) and write the row.
+template <int LDK>
+__device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n) {
+    constexpr int RHS0 = LDK * (LDK + 1) / 2;
     const int D = p.D;
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     float *orow = p.out + (size_t)r * p.ld;
@@ -683,12 +711,17 @@ __device__ void finish_row(const AlsParams &p, float *g, float *inv, int rhs0, i
     }
     const float diag = p.lam_c + p.lam_n * (float)n + p.tau * S;
     if (p.tax_T)
-        for (int i = 0; i < D; ++i) g[rhs0 + i] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], g[rhs0 + i]);
-    if (!thread_solve(g, inv, D, rhs0, diag)) {
+        for (int i = 0; i < D; ++i)
+            g[RHS0 + i] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], g[RHS0 + i]);
+    if (!thread_solve<LDK>(g, D, diag)) {
         report_fail(p.fail, r);
         return;
     }
-    for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? g[rhs0 + i] : 0.f;
+    for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? g[RHS0 + i] : 0.f;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *a) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 
 template <int NBK, bool HAS_W>
@@ -699,13 +732,14 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = lane >> 1, h = lane & 1;
     float *ring = smem + warp * C::WARP_FLOATS;
-    float *gbuf = ring + C::NS * C::STAGE;
-    float *my_g = gbuf + pair * C::GSTRIDE;
-    const int nb_real = (p.D + 3) / 4;   // memory blocks that exist in `fixed`
-    int boff[NBK];                        // smem offset of register block p
+    float *my_slot0 = ring + pair * C::SLOT;          // + stage * STAGE
+    float *my_g = ring + pair * C::GSTRIDE;            // aliases the ring after the Gram
+    const int nb_real = (p.D + 3) / 4;
+    int boff[NBK];
 #pragma unroll
     for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
     const int64_t n_groups = (q.n_tasks + C::PAIRS - 1) / C::PAIRS;
+    const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(my_slot0));
 
     for (;;) {
         int64_t grp = 0;
@@ -724,91 +758,114 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
         int nmax = n;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, o));
+        const int32_t *idxp = p.idx + k0;
+        const float *valp = p.val + k0;
+        const float *wtsp = HAS_W ? p.wts + k0 : nullptr;
+        // warm L2 with the head of this task's idx / val streams
+        if (n > 0) {
+            for (int o = 0; o < min(n, C::PF); o += 32) prefetch_l2(h ? (const void *)(valp + o)
+                                                                        : (const void *)(idxp + o));
+        }
 
         float acc[C::NACC];
 #pragma unroll
         for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
 
-        // issue the gathers of step s (idx already known)
+        // gathers of step s into stage (s % NS); col = partner id or -1
         auto issue = [&](int s, int col) {
-            float *sl = ring + (s % C::NS) * C::STAGE + pair * C::SLOT;
+            const unsigned st = ring_s + (unsigned)((s % C::NS) * C::STAGE * 4);
             const bool ok = col >= 0;
             const float *src = p.fixed + (size_t)(ok ? col : 0) * p.ld;
 #pragma unroll
-            for (int b = h; b < NBK; b += 2)
-                cp_async16(sl + 4 * b, src + 4 * b, (ok && b < nb_real) ? 16 : 0);
+            for (int b = h; b < NBK; b += 2) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(st + 16 * b),
+                             "l"(src + 4 * b), "r"((ok && b < nb_real) ? 16 : 0));
+            }
             if (h == 0) {
-                const float *vs = p.val + (ok ? k0 + s : 0);
-                unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sl + C::LDK));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(vs),
-                             "r"(ok ? 4 : 0));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(st + 4 * C::LDK),
+                             "l"(valp + (ok ? s : 0)), "r"(ok ? 4 : 0));
             } else if (HAS_W) {
-                const float *ws = p.wts + (ok ? k0 + s : 0);
-                unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sl + C::LDK + 1));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(ws),
-                             "r"(ok ? 4 : 0));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
+                             ::"r"(st + 4 * (C::LDK + 1)), "l"(wtsp + (ok ? s : 0)), "r"(ok ? 4 : 0));
             }
             cp_async_commit();
         };
-        int nidx = n > 0 ? p.idx[k0] : -1;
+        // partner ids two steps ahead in registers
+        int nid0 = n > 0 ? idxp[0] : -1;
+        int nid1 = n > 1 ? idxp[1] : -1;
 #pragma unroll
         for (int s = 0; s < C::NS - 1; ++s) {
-            if (s < nmax) issue(s, nidx);
+            if (s < nmax) issue(s, nid0);
             else cp_async_commit();
-            nidx = (s + 1 < n) ? p.idx[k0 + s + 1] : -1;
+            nid0 = nid1;
+            nid1 = (s + 2 < n) ? idxp[s + 2] : -1;
         }
-        for (int t = 0; t < nmax; ++t) {
-            const int sn = t + C::NS - 1;
-            if (sn < nmax) issue(sn, nidx);
-            else cp_async_commit();
-            nidx = (sn + 1 < n) ? p.idx[k0 + sn + 1] : -1;
-            cp_async_wait<C::NS - 1>();
-            __syncwarp();
-            const float *sl = ring + (t % C::NS) * C::STAGE + pair * C::SLOT;
-            float4 xr[NBK];
+        for (int t0 = 0; t0 < nmax; t0 += C::NS) {
 #pragma unroll
-            for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(sl + boff[b]);
-            float y = sl[C::LDK] - p.y_shift;
-            float4 xa[NBK];
+            for (int u = 0; u < C::NS; ++u) {
+                const int t = t0 + u;
+                if (t < nmax) {
+                    const int sn = t + C::NS - 1;
+                    if (sn < nmax) issue(sn, nid0);
+                    else cp_async_commit();
+                    nid0 = nid1;
+                    nid1 = (sn + 2 < n) ? idxp[sn + 2] : -1;
+                    if (sn + C::PF < n && ((k0 + sn + C::PF) & 31) == 0)
+                        prefetch_l2(h ? (const void *)(valp + sn + C::PF)
+                                      : (const void *)(idxp + sn + C::PF));
+                    cp_async_wait<C::NS - 1>();
+                    __syncwarp();
+                    const float *sl = my_slot0 + u * C::STAGE;   // t % NS == u
+                    float4 xr[NBK];
 #pragma unroll
-            for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
-            if (HAS_W) {
-                const float w = sl[C::LDK + 1];
+                    for (int b = 0; b < NBK; ++b)
+                        xr[b] = *reinterpret_cast<const float4 *>(sl + boff[b]);
+                    const float y = sl[C::LDK] - p.y_shift;
+                    float4 xa[NBK];
 #pragma unroll
-                for (int b = 0; b < NBK; ++b) {
-                    xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
-                }
-            }
-            int e = 0;
+                    for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
+                    if (HAS_W) {
+                        const float w = sl[C::LDK + 1];
 #pragma unroll
-            for (int d = 0; d <= (NBK - 1) / 2; ++d) {
-#pragma unroll
-                for (int b = 0; b < NBK; b += 2) {
-                    const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-                    const float4 bq = xr[(b + d) % NBK];
-                    const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
-                    if (d == 0) {
-#pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int nn = 0; nn <= m; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                    } else {
-#pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int nn = 0; nn < 4; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                        for (int b = 0; b < NBK; ++b) {
+                            xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
+                        }
                     }
+                    int e = 0;
+#pragma unroll
+                    for (int d = 0; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+                        for (int b = 0; b < NBK; b += 2) {
+                            const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+                            const float4 bq = xr[(b + d) % NBK];
+                            const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
+                            if (d == 0) {
+#pragma unroll
+                                for (int m = 0; m < 4; ++m)
+#pragma unroll
+                                    for (int nn = 0; nn <= m; ++nn, ++e)
+                                        acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                            } else {
+#pragma unroll
+                                for (int m = 0; m < 4; ++m)
+#pragma unroll
+                                    for (int nn = 0; nn < 4; ++nn, ++e)
+                                        acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < NBK; b += 2) {
+                        const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+#pragma unroll
+                        for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
+                    }
+                    __syncwarp();
                 }
             }
-#pragma unroll
-            for (int b = 0; b < NBK; b += 2) {
-                const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-#pragma unroll
-                for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
-            }
-            __syncwarp();
         }
         cp_async_wait<0>();
+        __syncwarp();
 
         // scatter the lane's accumulators into the pair's packed [A | b]
         {
@@ -822,7 +879,8 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
 #pragma unroll
                         for (int m = 0; m < 4; ++m)
 #pragma unroll
-                            for (int nn = 0; nn <= m; ++nn, ++e) my_g[pidx(4 * A + m, 4 * A + nn)] = acc[e];
+                            for (int nn = 0; nn <= m; ++nn, ++e)
+                                my_g[pidx(4 * A + m, 4 * A + nn)] = acc[e];
                     } else {
 #pragma unroll
                         for (int m = 0; m < 4; ++m)
@@ -847,7 +905,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
                 float *dst = p.partials + (size_t)slot * C::GRAM;
                 for (int i = h; i < C::GRAM; i += 2) dst[i] = my_g[i];
             } else if (h == 0) {
-                finish_row(p, my_g, my_g + C::GRAM, C::RHS0, row, n);
+                finish_row<C::LDK>(p, my_g, row, n);
             }
         }
         __syncwarp();
@@ -855,10 +913,12 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
 }
 
 // Hot rows: one warp per row sums its chunk partials in chunk order, then
-// lane 0 solves.
+// the warp solves cooperatively (lane i owns row i of A, right-looking
+// Cholesky with shuffles).
 template <int NBK>
 __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK>;
+    constexpr int LDK = C::LDK;
     __shared__ float g[4][C::GSTRIDE];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t hr = (int64_t)blockIdx.x * 4 + warp;
@@ -866,13 +926,69 @@ __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
     const int j = q.sorted_j[hr];
     const int r = p.row_list ? p.row_list[j] : p.row_lo + j;
     const int s0 = q.hoff[j], s1 = q.hoff[j + 1];
+    float *G = g[warp];
     for (int i = lane; i < C::GRAM; i += 32) {
         float a = 0.f;
         for (int s = s0; s < s1; ++s) a += __ldcg(p.partials + (size_t)s * C::GRAM + i);
-        g[warp][i] = a;
+        G[i] = a;
     }
     __syncwarp();
-    if (lane == 0) finish_row(p, g[warp], g[warp] + C::GRAM, C::RHS0, r, p.ptr[r + 1] - p.ptr[r]);
+    const int D = p.D;
+    const int64_t n = p.ptr[r + 1] - p.ptr[r];
+    const float S = p.tax_S ? p.tax_S[r] : 0.f;
+    float *orow = p.out + (size_t)r * p.ld;
+    const float diag = p.lam_c + p.lam_n * (float)n + p.tau * S;
+    float a[LDK];
+#pragma unroll
+    for (int c = 0; c < LDK; ++c) a[c] = (lane < D && c <= lane) ? G[pidx(lane, c)] : 0.f;
+    float b = lane < D ? G[C::RHS0 + lane] : 0.f;
+    if (p.tax_T && lane < D) b = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + lane], b);
+#pragma unroll
+    for (int c = 0; c < LDK; ++c)
+        if (c == lane) a[c] += diag;
+    bool bad = false;
+#pragma unroll
+    for (int j2 = 0; j2 < LDK; ++j2) {
+        if (j2 < D) {
+            const float piv = __shfl_sync(FULL, a[j2], j2);
+            bad |= !(piv > 0.f) || !isfinite(piv);
+            const float l = sqrtf(piv), inv = 1.f / l;
+            if (lane == j2) a[j2] = l;
+            else if (lane > j2) a[j2] *= inv;
+#pragma unroll
+            for (int k2 = j2 + 1; k2 < LDK; ++k2) {
+                if (k2 < D) {
+                    const float lk = __shfl_sync(FULL, a[j2], k2);
+                    if (lane >= k2) a[k2] = fmaf(-a[j2], lk, a[k2]);
+                }
+            }
+        }
+    }
+    if (bad) {
+        if (lane == 0) report_fail(p.fail, r);
+        return;
+    }
+#pragma unroll
+    for (int j2 = 0; j2 < LDK; ++j2) {
+        if (j2 < D) {
+            if (lane == j2) b = b / a[j2];
+            const float yj = __shfl_sync(FULL, b, j2);
+            if (lane > j2) b = fmaf(-a[j2], yj, b);
+        }
+    }
+    __syncwarp();
+    if (lane < D) {
+#pragma unroll
+        for (int c = 0; c < LDK; ++c)
+            if (c <= lane) G[pidx(lane, c)] = a[c];
+    }
+    __syncwarp();
+    for (int j2 = D - 1; j2 >= 0; --j2) {
+        if (lane == j2) b = b / G[pidx(j2, j2)];
+        const float xj = __shfl_sync(FULL, b, j2);
+        if (lane < j2) b = fmaf(-G[pidx(j2, lane)], xj, b);
+    }
+    if (lane < p.ld) orow[lane] = lane < D ? b : 0.f;
 }
 
 // --- plan kernels for the pair path
