@@ -86,7 +86,8 @@ size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
  *   A_r = sum_k w_k x_k x_k^T + (lam_c + lam_n * n_r + tau * S_r) I
  *   b_r = sum_k w_k (val_k - y_shift) x_k + tau * T_r
  *   out[r] = A_r^{-1} b_r
- * with x_k = fixed[idx[k]], w_k = wts[k] (wts NULL -> 1), n_r = ptr[r+1]-ptr[r],
+ * with x_k = fixed[idx[k]] (fixed: n_fixed rows), w_k = wts[k] (wts NULL -> 1),
+ * n_r = ptr[r+1]-ptr[r],
  * S/T (nullable) the taxonomy terms of mcf_taxonomy_terms (T row-major, ld).
  * Plain ALS: lam_c = lam, lam_n = 0.  Weighted-lambda: lam_c = 0, lam_n = lam.
  * A row with no ratings and no taxonomy mass becomes 0 when lam_c > 0 or
@@ -95,7 +96,7 @@ size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
  * other rows still complete (the reference's failing block stops early,
  * _kernels.py:197-203). */
 int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
-                      const float *wts, const float *fixed, float *out, int32_t D,
+                      const float *wts, const float *fixed, int64_t n_fixed, float *out, int32_t D,
                       float lam_c, float lam_n, float y_shift, const float *tax_S,
                       const float *tax_T, float tau, const int32_t *row_list, int32_t n_list,
                       int32_t row_lo, int32_t chunk, const void *plan, const int64_t *plan_info,

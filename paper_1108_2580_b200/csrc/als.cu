@@ -35,6 +35,10 @@
 // threads, CTA-cooperative Cholesky (correctness path for configs 3/4; the
 // tensor-core path for D >= 64 replaces it).
 #include <algorithm>
+#include <string>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "../../include/mcf.h"
@@ -50,6 +54,7 @@ struct AlsParams {
     const float *val;
     const float *wts;
     const float *fixed;
+    int64_t n_fixed;   // rows of `fixed` (TMA bounds)
     float *out;
     int D, ld;
     float lam_c, lam_n, y_shift, tau;
@@ -607,21 +612,26 @@ template <int NBK>
 struct PairCfg {
     static_assert(NBK % 2 == 1, "odd block count");
     static constexpr int LDK = 4 * NBK;
-    static constexpr int SLOT = LDK + 4;          // x | y, w, pad, pad
-    static constexpr int NS = 8;                  // pipeline stages (7 steps of lead)
+    static constexpr int ROWF = LDK + 4;           // TMA box row (floats): +16 B keeps the
+                                                   // 4 rows of a gather bank-conflict free
+    static constexpr int GBYTES = ((4 * ROWF * 4 + 127) / 128) * 128;  // one gather4, 128B aligned
     static constexpr int PAIRS = 16;
-    static constexpr int STAGE = PAIRS * SLOT;
-    static constexpr int HALF = (NBK + 1) / 2;    // even block starts per orbit
+    static constexpr int XBYTES = 4 * GBYTES;      // 16 partner rows
+    static constexpr int STAGE_BYTES = XBYTES + 2 * PAIRS * 4;  // + y[16] + w[16]
+    static constexpr int NS = 8;                   // pipeline stages (7 steps of lead)
+    static constexpr int HALF = (NBK + 1) / 2;
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
     static constexpr int RHS0 = LDK * (LDK + 1) / 2;
     static constexpr int GRAM = RHS0 + LDK;        // packed lower + rhs
     static constexpr int GSTRIDE = GRAM | 1;       // odd stride: conflict-free per-lane rows
-    static constexpr int RING = NS * STAGE;
-    static constexpr int SOLVE = PAIRS * GSTRIDE;
+    static constexpr int RING_BYTES = NS * STAGE_BYTES;
+    static constexpr int SOLVE_BYTES = PAIRS * GSTRIDE * 4;
     // the gather ring and the solve buffer are never live at the same time
-    static constexpr int WARP_FLOATS = RING > SOLVE ? RING : SOLVE;
+    static constexpr int WARP_BYTES =
+        ((RING_BYTES > SOLVE_BYTES ? RING_BYTES : SOLVE_BYTES) + 127) / 128 * 128;
     static constexpr int WARPS = 4;
     static constexpr int PF = 64;                  // L2 prefetch distance (ratings)
+    static constexpr int TX = 4 * 4 * ROWF * 4;    // bytes landed per step (4 gathers)
 };
 
 __device__ __forceinline__ constexpr int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
@@ -724,22 +734,67 @@ __device__ __forceinline__ void prefetch_l2(const void *a) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    while (!mbar_try(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap *map, int col, int r0,
+                                            int r1, int r2, int r3, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+
+// Each warp gathers its own partner rows: per step the lanes 0, 8, 16, 24
+// issue one TMA tile::gather4 each (4 pairs' rows, ROWF floats per row; a
+// row id of -1 is out of bounds and lands as zeros), completion counted on
+// the stage's mbarrier.  The rating (and weight) of each pair rides along as
+// a plain shared store.  Stages are consumed NS-1 steps after issue.
 template <int NBK, bool HAS_W>
-__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams p, PairPlan q) {
+__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32)
+    k_als_pair(AlsParams p, PairPlan q, const __grid_constant__ CUtensorMap fixed_map) {
     using C = PairCfg<NBK>;
-    extern __shared__ float4 smem4[];
-    float *smem = reinterpret_cast<float *>(smem4);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) unsigned long long bars[C::WARPS][C::NS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = lane >> 1, h = lane & 1;
-    float *ring = smem + warp * C::WARP_FLOATS;
-    float *my_slot0 = ring + pair * C::SLOT;          // + stage * STAGE
-    float *my_g = ring + pair * C::GSTRIDE;            // aliases the ring after the Gram
-    const int nb_real = (p.D + 3) / 4;
+    unsigned char *wbase = smem_raw + warp * C::WARP_BYTES;
+    const unsigned wbase_s = static_cast<unsigned>(__cvta_generic_to_shared(wbase));
+    const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[warp][0]));
+    float *my_g = reinterpret_cast<float *>(wbase) + pair * C::GSTRIDE;  // aliases the ring
+    // my row inside a stage: gather (pair / 4), row (pair % 4)
+    const int row_off = (pair >> 2) * C::GBYTES + (pair & 3) * C::ROWF * 4;
     int boff[NBK];
 #pragma unroll
-    for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
+    for (int b = 0; b < NBK; ++b) boff[b] = row_off + 16 * ((b + h) % NBK);
+    const bool issuer = (lane & 7) == 0;   // lanes 0, 8, 16, 24: one gather4 each
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < C::NS; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     const int64_t n_groups = (q.n_tasks + C::PAIRS - 1) / C::PAIRS;
-    const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(my_slot0));
+    unsigned gstep = 0;   // steps issued by this warp so far (stage = gstep % NS)
 
     for (;;) {
         int64_t grp = 0;
@@ -761,111 +816,108 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
         const int32_t *idxp = p.idx + k0;
         const float *valp = p.val + k0;
         const float *wtsp = HAS_W ? p.wts + k0 : nullptr;
-        // warm L2 with the head of this task's idx / val streams
-        if (n > 0) {
-            for (int o = 0; o < min(n, C::PF); o += 32) prefetch_l2(h ? (const void *)(valp + o)
-                                                                        : (const void *)(idxp + o));
-        }
+        if (n > 0)
+            for (int o = 0; o < min(n, C::PF); o += 32)
+                prefetch_l2(h ? (const void *)(valp + o) : (const void *)(idxp + o));
+        // the solve of the previous group wrote this area through the generic
+        // proxy; order it before the TMA (async proxy) overwrites it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
 
         float acc[C::NACC];
 #pragma unroll
         for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
 
-        // gathers of step s into stage (s % NS); col = partner id or -1
-        auto issue = [&](int s, int col) {
-            const unsigned st = ring_s + (unsigned)((s % C::NS) * C::STAGE * 4);
-            const bool ok = col >= 0;
-            const float *src = p.fixed + (size_t)(ok ? col : 0) * p.ld;
-#pragma unroll
-            for (int b = h; b < NBK; b += 2) {
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(st + 16 * b),
-                             "l"(src + 4 * b), "r"((ok && b < nb_real) ? 16 : 0));
-            }
-            if (h == 0) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(st + 4 * C::LDK),
-                             "l"(valp + (ok ? s : 0)), "r"(ok ? 4 : 0));
-            } else if (HAS_W) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
-                             ::"r"(st + 4 * (C::LDK + 1)), "l"(wtsp + (ok ? s : 0)), "r"(ok ? 4 : 0));
-            }
-            cp_async_commit();
-        };
-        // partner ids two steps ahead in registers
-        int nid0 = n > 0 ? idxp[0] : -1;
-        int nid1 = n > 1 ? idxp[1] : -1;
-#pragma unroll
-        for (int s = 0; s < C::NS - 1; ++s) {
-            if (s < nmax) issue(s, nid0);
-            else cp_async_commit();
-            nid0 = nid1;
-            nid1 = (s + 2 < n) ? idxp[s + 2] : -1;
+        // operands of the next issue, 3 steps ahead in registers
+        int c0 = n > 0 ? idxp[0] : -1, c1 = n > 1 ? idxp[1] : -1, c2 = n > 2 ? idxp[2] : -1;
+        float v0 = n > 0 ? valp[0] : 0.f, v1 = n > 1 ? valp[1] : 0.f, v2 = n > 2 ? valp[2] : 0.f;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f;
+        if (HAS_W) {
+            w0 = n > 0 ? wtsp[0] : 0.f;
+            w1 = n > 1 ? wtsp[1] : 0.f;
+            w2 = n > 2 ? wtsp[2] : 0.f;
         }
-        for (int t0 = 0; t0 < nmax; t0 += C::NS) {
+        const unsigned gbase = gstep;
+        auto issue = [&](int s) {   // step s of this group, operands in c0/v0/w0
+            const unsigned gs = gbase + (unsigned)s;
+            const unsigned st = wbase_s + (gs % C::NS) * C::STAGE_BYTES;
+            const unsigned bar = bar0 + 8 * (gs % C::NS);
+            float *ys = reinterpret_cast<float *>(wbase + (gs % C::NS) * C::STAGE_BYTES + C::XBYTES);
+            if (h == 0) {
+                ys[pair] = v0;
+                if (HAS_W) ys[C::PAIRS + pair] = w0;
+            }
+            const int q0 = __shfl_sync(FULL, c0, (lane & 24) + 0);
+            const int q1 = __shfl_sync(FULL, c0, (lane & 24) + 2);
+            const int q2 = __shfl_sync(FULL, c0, (lane & 24) + 4);
+            const int q3 = __shfl_sync(FULL, c0, (lane & 24) + 6);
+            if (lane == 0) mbar_expect_tx(bar, C::TX);
+            __syncwarp();
+            if (issuer) tma_gather4(st + (lane >> 3) * C::GBYTES, &fixed_map, 0, q0, q1, q2, q3, bar);
+            // rotate the operand registers and fetch 3 steps ahead
+            c0 = c1; c1 = c2;
+            v0 = v1; v1 = v2;
+            if (HAS_W) { w0 = w1; w1 = w2; }
+            const int nx = s + 3;
+            c2 = nx < n ? idxp[nx] : -1;
+            v2 = nx < n ? valp[nx] : 0.f;
+            if (HAS_W) w2 = nx < n ? wtsp[nx] : 0.f;
+            if (nx + C::PF < n && ((k0 + nx + C::PF) & 31) == 0)
+                prefetch_l2(h ? (const void *)(valp + nx + C::PF) : (const void *)(idxp + nx + C::PF));
+        };
+#pragma unroll 1
+        for (int s = 0; s < C::NS - 1 && s < nmax; ++s) issue(s);
+#pragma unroll 1
+        for (int t = 0; t < nmax; ++t) {
+            if (t + C::NS - 1 < nmax) issue(t + C::NS - 1);
+            const unsigned gs = gbase + (unsigned)t;
+            mbar_wait(bar0 + 8 * (gs % C::NS), (gs / C::NS) & 1);
+            const unsigned char *sb = wbase + (gs % C::NS) * C::STAGE_BYTES;
+            float4 xr[NBK];
 #pragma unroll
-            for (int u = 0; u < C::NS; ++u) {
-                const int t = t0 + u;
-                if (t < nmax) {
-                    const int sn = t + C::NS - 1;
-                    if (sn < nmax) issue(sn, nid0);
-                    else cp_async_commit();
-                    nid0 = nid1;
-                    nid1 = (sn + 2 < n) ? idxp[sn + 2] : -1;
-                    if (sn + C::PF < n && ((k0 + sn + C::PF) & 31) == 0)
-                        prefetch_l2(h ? (const void *)(valp + sn + C::PF)
-                                      : (const void *)(idxp + sn + C::PF));
-                    cp_async_wait<C::NS - 1>();
-                    __syncwarp();
-                    const float *sl = my_slot0 + u * C::STAGE;   // t % NS == u
-                    float4 xr[NBK];
+            for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(sb + boff[b]);
+            const float *ys = reinterpret_cast<const float *>(sb + C::XBYTES);
+            const float y = ys[pair] - p.y_shift;
+            float4 xa[NBK];
 #pragma unroll
-                    for (int b = 0; b < NBK; ++b)
-                        xr[b] = *reinterpret_cast<const float4 *>(sl + boff[b]);
-                    const float y = sl[C::LDK] - p.y_shift;
-                    float4 xa[NBK];
+            for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
+            if (HAS_W) {
+                const float w = ys[C::PAIRS + pair];
 #pragma unroll
-                    for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
-                    if (HAS_W) {
-                        const float w = sl[C::LDK + 1];
-#pragma unroll
-                        for (int b = 0; b < NBK; ++b) {
-                            xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
-                        }
-                    }
-                    int e = 0;
-#pragma unroll
-                    for (int d = 0; d <= (NBK - 1) / 2; ++d) {
-#pragma unroll
-                        for (int b = 0; b < NBK; b += 2) {
-                            const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-                            const float4 bq = xr[(b + d) % NBK];
-                            const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
-                            if (d == 0) {
-#pragma unroll
-                                for (int m = 0; m < 4; ++m)
-#pragma unroll
-                                    for (int nn = 0; nn <= m; ++nn, ++e)
-                                        acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                            } else {
-#pragma unroll
-                                for (int m = 0; m < 4; ++m)
-#pragma unroll
-                                    for (int nn = 0; nn < 4; ++nn, ++e)
-                                        acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int b = 0; b < NBK; b += 2) {
-                        const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-#pragma unroll
-                        for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
-                    }
-                    __syncwarp();
+                for (int b = 0; b < NBK; ++b) {
+                    xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
                 }
             }
+            int e = 0;
+#pragma unroll
+            for (int d = 0; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+                for (int b = 0; b < NBK; b += 2) {
+                    const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+                    const float4 bq = xr[(b + d) % NBK];
+                    const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
+                    if (d == 0) {
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+#pragma unroll
+                            for (int nn = 0; nn <= m; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+#pragma unroll
+                            for (int nn = 0; nn < 4; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < NBK; b += 2) {
+                const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+#pragma unroll
+                for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
+            }
+            __syncwarp();   // all lanes done with this stage before it is refilled
         }
-        cp_async_wait<0>();
-        __syncwarp();
+        gstep = gbase + (unsigned)nmax;
 
         // scatter the lane's accumulators into the pair's packed [A | b]
         {
@@ -1144,10 +1196,50 @@ PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_
 
 bool use_pair(int D) { return D <= 20; }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) ==
+                cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+// 2-D fp32 map over the fixed factor table [n_rows][ld], box {row_floats, 1}
+// (the tile::gather4 form: one box row per gathered index; rows past the
+// table and columns past ld land as zeros).
+int fixed_tensor_map(CUtensorMap *map, const float *fixed, int64_t n_rows, int ld, int row_floats) {
+    auto fn = encode_fn();
+    if (!fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return MCF_E_CUDA;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)std::max<int64_t>(n_rows, 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)row_floats, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(fixed), dims,
+                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        return MCF_E_CUDA;
+    }
+    return MCF_OK;
+}
+
 template <int NBK, bool W>
 int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     using C = PairCfg<NBK>;
-    const size_t smem = sizeof(float) * C::WARP_FLOATS * C::WARPS;
+    const size_t smem = (size_t)C::WARP_BYTES * C::WARPS;
+    CUtensorMap map;
+    int rc = fixed_tensor_map(&map, p.fixed, p.n_fixed, p.ld, C::ROWF);
+    if (rc) return rc;
+
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_als_pair<NBK, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1162,7 +1254,7 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
     const int64_t want = ceil_div(groups, C::WARPS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_pair<NBK, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
+    if (grid > 0) k_als_pair<NBK, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q, map);
     if (q.n_heavy > 0)
         k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
     return check_launch("mcf_als_half_step(pair)");
@@ -1269,7 +1361,8 @@ extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t
 }
 
 extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
-                                 const float *wts, const float *fixed, float *out, int32_t D,
+                                 const float *wts, const float *fixed, int64_t n_fixed, float *out,
+                                 int32_t D,
                                  float lam_c, float lam_n, float y_shift, const float *tax_S,
                                  const float *tax_T, float tau, const int32_t *row_list,
                                  int32_t n_list, int32_t row_lo, int32_t chunk, const void *plan,
@@ -1294,7 +1387,8 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
     PlanLayout L = carve_plan(const_cast<void *>(plan), SIZE_MAX, n_list, plan_info[5], chunk,
                               &need_plan);
     AlsParams p{};
-    p.ptr = ptr; p.idx = idx; p.val = val; p.wts = wts; p.fixed = fixed; p.out = out;
+    p.ptr = ptr; p.idx = idx; p.val = val; p.wts = wts; p.fixed = fixed; p.n_fixed = n_fixed;
+    p.out = out;
     p.D = D; p.ld = mcf_factor_ld(D);
     p.lam_c = lam_c; p.lam_n = lam_n; p.y_shift = y_shift; p.tau = tau;
     p.tax_S = tax_S; p.tax_T = tax_T;

@@ -140,7 +140,8 @@ class LayoutSolver:
             self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = self._ws[k]
         check(_lib.lib().mcf_als_half_step(
-            ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(wts), ptr(fixed), ptr(out), self.D,
+            ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(wts), ptr(fixed), fixed.shape[0],
+            ptr(out), self.D,
             float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
             ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail), ptr(ws), ws.numel(),
             stream_ptr(dev)), "mcf_als_half_step")
