@@ -288,7 +288,7 @@ def run_ours(args, rank, world):
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "k_als_warp<NB=5> (fused Gram + lam*n + Cholesky + solve)",
+                "kernel": "k_als_pair<5> (fused Gram + lam*n + Cholesky + solve; + k_als_heavy for hot rows)",
                 "launch_ms": {"items": statistics.mean(half_ms[0::2]),
                               "users": statistics.mean(half_ms[1::2])},
                 "achieved_tflops": alg["flops_launch_mean"] / mean_launch_s / 1e12,

@@ -618,7 +618,7 @@ struct PairCfg {
     static constexpr int PAIRS = 16;
     static constexpr int XBYTES = 4 * GBYTES;      // 16 partner rows
     static constexpr int STAGE_BYTES = XBYTES + 2 * PAIRS * 4;  // + y[16] + w[16]
-    static constexpr int NS = 8;                   // pipeline stages (7 steps of lead)
+    static constexpr int NS = 16;                  // pipeline stages (15 steps of lead)
     static constexpr int HALF = (NBK + 1) / 2;
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
     static constexpr int RHS0 = LDK * (LDK + 1) / 2;
