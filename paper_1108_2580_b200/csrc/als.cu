@@ -37,9 +37,6 @@
 #include <algorithm>
 #include <string>
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "common.cuh"
 #include "../../include/mcf.h"
 
@@ -612,12 +609,10 @@ template <int NBK>
 struct PairCfg {
     static_assert(NBK % 2 == 1, "odd block count");
     static constexpr int LDK = 4 * NBK;
-    static constexpr int ROWF = LDK + 4;           // TMA box row (floats): +16 B keeps the
-                                                   // 4 rows of a gather bank-conflict free
-    static constexpr int GBYTES = ((4 * ROWF * 4 + 127) / 128) * 128;  // one gather4, 128B aligned
+    static constexpr int SLOT = LDK + 4;           // x | y, w, pad, pad  (96 B for D = 20:
+                                                   // 4 consecutive pairs hit distinct banks)
     static constexpr int PAIRS = 16;
-    static constexpr int XBYTES = 4 * GBYTES;      // 16 partner rows
-    static constexpr int STAGE_BYTES = XBYTES + 2 * PAIRS * 4;  // + y[16] + w[16]
+    static constexpr int STAGE_BYTES = PAIRS * SLOT * 4;
     static constexpr int NS = 16;                  // pipeline stages (15 steps of lead)
     static constexpr int HALF = (NBK + 1) / 2;
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
@@ -631,7 +626,6 @@ struct PairCfg {
         ((RING_BYTES > SOLVE_BYTES ? RING_BYTES : SOLVE_BYTES) + 127) / 128 * 128;
     static constexpr int WARPS = 4;
     static constexpr int PF = 64;                  // L2 prefetch distance (ratings)
-    static constexpr int TX = 4 * 4 * ROWF * 4;    // bytes landed per step (4 gathers)
 };
 
 __device__ __forceinline__ constexpr int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
@@ -755,23 +749,13 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     while (!mbar_try(bar, parity)) {
     }
 }
-__device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap *map, int col, int r0,
-                                            int r1, int r2, int r3, unsigned bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-        : "memory");
-}
-
-// Each warp gathers its own partner rows: per step the lanes 0, 8, 16, 24
-// issue one TMA tile::gather4 each (4 pairs' rows, ROWF floats per row; a
-// row id of -1 is out of bounds and lands as zeros), completion counted on
-// the stage's mbarrier.  The rating (and weight) of each pair rides along as
-// a plain shared store.  Stages are consumed NS-1 steps after issue.
+// Each lane pair gathers its own partner row per step with cp.async (16 B
+// blocks split between the two lanes, zero-fill past the task end) and the
+// rating with a 4 B cp.async; every lane's copies are tracked by the
+// stage's mbarrier (cp.async.mbarrier.arrive.noinc, 32 arrivals), so a
+// stage is waited on individually, NS-1 steps after its issue.
 template <int NBK, bool HAS_W>
-__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32)
-    k_als_pair(AlsParams p, PairPlan q, const __grid_constant__ CUtensorMap fixed_map) {
+__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[C::WARPS][C::NS];
@@ -781,15 +765,14 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32)
     const unsigned wbase_s = static_cast<unsigned>(__cvta_generic_to_shared(wbase));
     const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[warp][0]));
     float *my_g = reinterpret_cast<float *>(wbase) + pair * C::GSTRIDE;  // aliases the ring
-    // my row inside a stage: gather (pair / 4), row (pair % 4)
-    const int row_off = (pair >> 2) * C::GBYTES + (pair & 3) * C::ROWF * 4;
-    int boff[NBK];
+    const unsigned my_slot_s = wbase_s + pair * C::SLOT * 4;
+    const int nb_real = (p.D + 3) / 4;
+    int boff[NBK];   // float offset of register block b inside the pair's slot
 #pragma unroll
-    for (int b = 0; b < NBK; ++b) boff[b] = row_off + 16 * ((b + h) % NBK);
-    const bool issuer = (lane & 7) == 0;   // lanes 0, 8, 16, 24: one gather4 each
+    for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
     if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < C::NS; ++s) mbar_init(bar0 + 8 * s, 1);
+        for (int s = 0; s < C::NS; ++s) mbar_init(bar0 + 8 * s, 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -819,49 +802,40 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32)
         if (n > 0)
             for (int o = 0; o < min(n, C::PF); o += 32)
                 prefetch_l2(h ? (const void *)(valp + o) : (const void *)(idxp + o));
-        // the solve of the previous group wrote this area through the generic
-        // proxy; order it before the TMA (async proxy) overwrites it
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
+        __syncwarp();   // the previous group's solve is done with the (aliased) ring
 
         float acc[C::NACC];
 #pragma unroll
         for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
 
-        // operands of the next issue, 3 steps ahead in registers
+        // partner ids of the next issues, 3 steps ahead in registers
         int c0 = n > 0 ? idxp[0] : -1, c1 = n > 1 ? idxp[1] : -1, c2 = n > 2 ? idxp[2] : -1;
-        float v0 = n > 0 ? valp[0] : 0.f, v1 = n > 1 ? valp[1] : 0.f, v2 = n > 2 ? valp[2] : 0.f;
-        float w0 = 0.f, w1 = 0.f, w2 = 0.f;
-        if (HAS_W) {
-            w0 = n > 0 ? wtsp[0] : 0.f;
-            w1 = n > 1 ? wtsp[1] : 0.f;
-            w2 = n > 2 ? wtsp[2] : 0.f;
-        }
         const unsigned gbase = gstep;
-        auto issue = [&](int s) {   // step s of this group, operands in c0/v0/w0
+        // step s of this group: this lane's half of the partner row (+ the
+        // rating on lane 0 / the weight on lane 1) by 16 B / 4 B cp.async,
+        // completion signalled on the stage's mbarrier (count 32, .noinc)
+        auto issue = [&](int s) {
             const unsigned gs = gbase + (unsigned)s;
-            const unsigned st = wbase_s + (gs % C::NS) * C::STAGE_BYTES;
-            const unsigned bar = bar0 + 8 * (gs % C::NS);
-            float *ys = reinterpret_cast<float *>(wbase + (gs % C::NS) * C::STAGE_BYTES + C::XBYTES);
+            const unsigned slot_s = my_slot_s + (gs % C::NS) * C::STAGE_BYTES;
+            const bool ok = c0 >= 0;
+            const float *src = p.fixed + (size_t)(ok ? c0 : 0) * p.ld;
+#pragma unroll
+            for (int b = h; b < NBK; b += 2)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(slot_s + 16 * b),
+                             "l"(src + 4 * b), "r"((ok && b < nb_real) ? 16 : 0));
             if (h == 0) {
-                ys[pair] = v0;
-                if (HAS_W) ys[C::PAIRS + pair] = w0;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(slot_s + 4 * C::LDK),
+                             "l"(valp + (ok ? s : 0)), "r"(ok ? 4 : 0));
+            } else if (HAS_W) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
+                             ::"r"(slot_s + 4 * (C::LDK + 1)), "l"(wtsp + (ok ? s : 0)), "r"(ok ? 4 : 0));
             }
-            const int q0 = __shfl_sync(FULL, c0, (lane & 24) + 0);
-            const int q1 = __shfl_sync(FULL, c0, (lane & 24) + 2);
-            const int q2 = __shfl_sync(FULL, c0, (lane & 24) + 4);
-            const int q3 = __shfl_sync(FULL, c0, (lane & 24) + 6);
-            if (lane == 0) mbar_expect_tx(bar, C::TX);
-            __syncwarp();
-            if (issuer) tma_gather4(st + (lane >> 3) * C::GBYTES, &fixed_map, 0, q0, q1, q2, q3, bar);
-            // rotate the operand registers and fetch 3 steps ahead
-            c0 = c1; c1 = c2;
-            v0 = v1; v1 = v2;
-            if (HAS_W) { w0 = w1; w1 = w2; }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar0 + 8 * (gs % C::NS))
+                         : "memory");
+            c0 = c1;
+            c1 = c2;
             const int nx = s + 3;
             c2 = nx < n ? idxp[nx] : -1;
-            v2 = nx < n ? valp[nx] : 0.f;
-            if (HAS_W) w2 = nx < n ? wtsp[nx] : 0.f;
             if (nx + C::PF < n && ((k0 + nx + C::PF) & 31) == 0)
                 prefetch_l2(h ? (const void *)(valp + nx + C::PF) : (const void *)(idxp + nx + C::PF));
         };
@@ -872,17 +846,17 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32)
             if (t + C::NS - 1 < nmax) issue(t + C::NS - 1);
             const unsigned gs = gbase + (unsigned)t;
             mbar_wait(bar0 + 8 * (gs % C::NS), (gs / C::NS) & 1);
-            const unsigned char *sb = wbase + (gs % C::NS) * C::STAGE_BYTES;
+            const float *sl = reinterpret_cast<const float *>(wbase + (gs % C::NS) * C::STAGE_BYTES) +
+                              pair * C::SLOT;
             float4 xr[NBK];
 #pragma unroll
-            for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(sb + boff[b]);
-            const float *ys = reinterpret_cast<const float *>(sb + C::XBYTES);
-            const float y = ys[pair] - p.y_shift;
+            for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(sl + boff[b]);
+            const float y = sl[C::LDK] - p.y_shift;
             float4 xa[NBK];
 #pragma unroll
             for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
             if (HAS_W) {
-                const float w = ys[C::PAIRS + pair];
+                const float w = sl[C::LDK + 1];
 #pragma unroll
                 for (int b = 0; b < NBK; ++b) {
                     xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
@@ -1196,49 +1170,10 @@ PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_
 
 bool use_pair(int D) { return D <= 20; }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void *f = nullptr;
-        cudaDriverEntryPointQueryResult qr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) ==
-                cudaSuccess &&
-            qr == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    }
-    return fn;
-}
-
-// 2-D fp32 map over the fixed factor table [n_rows][ld], box {row_floats, 1}
-// (the tile::gather4 form: one box row per gathered index; rows past the
-// table and columns past ld land as zeros).
-int fixed_tensor_map(CUtensorMap *map, const float *fixed, int64_t n_rows, int ld, int row_floats) {
-    auto fn = encode_fn();
-    if (!fn) {
-        set_error("cuTensorMapEncodeTiled unavailable");
-        return MCF_E_CUDA;
-    }
-    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)std::max<int64_t>(n_rows, 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {(cuuint32_t)row_floats, 1};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(fixed), dims,
-                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-        return MCF_E_CUDA;
-    }
-    return MCF_OK;
-}
-
 template <int NBK, bool W>
 int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     using C = PairCfg<NBK>;
     const size_t smem = (size_t)C::WARP_BYTES * C::WARPS;
-    CUtensorMap map;
-    int rc = fixed_tensor_map(&map, p.fixed, p.n_fixed, p.ld, C::ROWF);
-    if (rc) return rc;
 
     static bool attr = false;
     if (!attr) {
@@ -1254,7 +1189,7 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
     const int64_t want = ceil_div(groups, C::WARPS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_pair<NBK, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q, map);
+    if (grid > 0) k_als_pair<NBK, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
         k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
     return check_launch("mcf_als_half_step(pair)");
