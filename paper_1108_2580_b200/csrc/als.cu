@@ -609,11 +609,14 @@ template <int NBK>
 struct PairCfg {
     static_assert(NBK % 2 == 1, "odd block count");
     static constexpr int LDK = 4 * NBK;
-    static constexpr int SLOT = LDK + 4;           // x | y, w, pad, pad  (96 B for D = 20:
-                                                   // 4 consecutive pairs hit distinct banks)
+    static constexpr int R = 2;                    // ratings per pipeline stage per pair
+    static constexpr int ROW = LDK + 4;            // x | y, w, pad, pad
+    // pair slot stride: (SLOT / 4) % 8 == 6 puts the 4 pairs of a quarter-warp
+    // on disjoint bank groups for the two consecutive blocks they read
+    static constexpr int SLOT = ((R * ROW / 4 + 7 - 6) / 8 * 8 + 6) * 4;
     static constexpr int PAIRS = 16;
     static constexpr int STAGE_BYTES = PAIRS * SLOT * 4;
-    static constexpr int NS = 16;                  // pipeline stages (15 steps of lead)
+    static constexpr int NS = 7;                   // pipeline stages (6 stages = 12 ratings of lead)
     static constexpr int HALF = (NBK + 1) / 2;
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
     static constexpr int RHS0 = LDK * (LDK + 1) / 2;
@@ -749,14 +752,18 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     while (!mbar_try(bar, parity)) {
     }
 }
-// Each lane pair gathers its own partner row per step with cp.async (16 B
-// blocks split between the two lanes, zero-fill past the task end) and the
-// rating with a 4 B cp.async; every lane's copies are tracked by the
-// stage's mbarrier (cp.async.mbarrier.arrive.noinc, 32 arrivals), so a
-// stage is waited on individually, NS-1 steps after its issue.
-template <int NBK, bool HAS_W>
+// Each lane pair gathers its own partner rows with cp.async (16 B blocks
+// split between the two lanes, zero-fill past the task end) and the ratings
+// with 4 B cp.async, R = 2 ratings per pipeline stage; every lane's copies
+// are tracked by the stage's mbarrier (cp.async.mbarrier.arrive.noinc, 32
+// arrivals), so a stage is waited on individually, NS-1 stages after its
+// issue.  Partner ids are register-prefetched two stages ahead with a
+// statically indexed ring (the loop is unrolled by 2 stages, so no register
+// moves ever wait on an in-flight load).
+template <int NBK, bool HAS_W, bool FULLBLK>
 __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK>;
+    constexpr int R = C::R;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[C::WARPS][C::NS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -766,8 +773,9 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
     const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[warp][0]));
     float *my_g = reinterpret_cast<float *>(wbase) + pair * C::GSTRIDE;  // aliases the ring
     const unsigned my_slot_s = wbase_s + pair * C::SLOT * 4;
-    const int nb_real = (p.D + 3) / 4;
-    int boff[NBK];   // float offset of register block b inside the pair's slot
+    const float *my_slot = reinterpret_cast<const float *>(wbase) + pair * C::SLOT;
+    const int nb_real = FULLBLK ? NBK : (p.D + 3) / 4;
+    int boff[NBK];   // float offset of register block b inside a row
 #pragma unroll
     for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
     if (lane == 0) {
@@ -777,7 +785,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
     }
     __syncwarp();
     const int64_t n_groups = (q.n_tasks + C::PAIRS - 1) / C::PAIRS;
-    unsigned gstep = 0;   // steps issued by this warp so far (stage = gstep % NS)
+    unsigned gst = 0;   // stages issued by this warp so far (slot = gst % NS)
 
     for (;;) {
         int64_t grp = 0;
@@ -796,6 +804,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
         int nmax = n;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, o));
+        const int nst = (nmax + R - 1) / R;   // stages of this group
         const int32_t *idxp = p.idx + k0;
         const float *valp = p.val + k0;
         const float *wtsp = HAS_W ? p.wts + k0 : nullptr;
@@ -808,90 +817,113 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
 #pragma unroll
         for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
 
-        // partner ids of the next issues, 3 steps ahead in registers
-        int c0 = n > 0 ? idxp[0] : -1, c1 = n > 1 ? idxp[1] : -1, c2 = n > 2 ? idxp[2] : -1;
-        const unsigned gbase = gstep;
-        // step s of this group: this lane's half of the partner row (+ the
-        // rating on lane 0 / the weight on lane 1) by 16 B / 4 B cp.async,
-        // completion signalled on the stage's mbarrier (count 32, .noinc)
-        auto issue = [&](int s) {
+        const unsigned gbase = gst;
+        auto ld_idx = [&](int k) -> int { return k < n ? idxp[k] : -1; };
+        // gathers of stage s (ratings R*s .. R*s+R-1): partner ids in ia/ib
+        auto issue = [&](int s, int ia, int ib) {
             const unsigned gs = gbase + (unsigned)s;
-            const unsigned slot_s = my_slot_s + (gs % C::NS) * C::STAGE_BYTES;
-            const bool ok = c0 >= 0;
-            const float *src = p.fixed + (size_t)(ok ? c0 : 0) * p.ld;
+            const unsigned ss = my_slot_s + (gs % C::NS) * C::STAGE_BYTES;
 #pragma unroll
-            for (int b = h; b < NBK; b += 2)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(slot_s + 16 * b),
-                             "l"(src + 4 * b), "r"((ok && b < nb_real) ? 16 : 0));
-            if (h == 0) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(slot_s + 4 * C::LDK),
-                             "l"(valp + (ok ? s : 0)), "r"(ok ? 4 : 0));
-            } else if (HAS_W) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
-                             ::"r"(slot_s + 4 * (C::LDK + 1)), "l"(wtsp + (ok ? s : 0)), "r"(ok ? 4 : 0));
+            for (int r = 0; r < R; ++r) {
+                const int col = r == 0 ? ia : ib;
+                const bool ok = col >= 0;
+                const float *src = p.fixed + (size_t)(ok ? col : 0) * p.ld;
+                const unsigned rs = ss + r * C::ROW * 4;
+#pragma unroll
+                for (int b = h; b < NBK; b += 2)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(rs + 16 * b),
+                                 "l"(src + 4 * b), "r"((ok && (FULLBLK || b < nb_real)) ? 16 : 0));
             }
+            // lane h brings the rating (and weight) of row h
+            const int k = R * s + h;
+            const bool okv = k < n;
+            const unsigned ys = ss + h * C::ROW * 4 + 4 * C::LDK;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(ys),
+                         "l"(valp + (okv ? k : 0)), "r"(okv ? 4 : 0));
+            if (HAS_W)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(ys + 4),
+                             "l"(wtsp + (okv ? k : 0)), "r"(okv ? 4 : 0));
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar0 + 8 * (gs % C::NS))
                          : "memory");
-            c0 = c1;
-            c1 = c2;
-            const int nx = s + 3;
-            c2 = nx < n ? idxp[nx] : -1;
-            if (nx + C::PF < n && ((k0 + nx + C::PF) & 31) == 0)
-                prefetch_l2(h ? (const void *)(valp + nx + C::PF) : (const void *)(idxp + nx + C::PF));
         };
-#pragma unroll 1
-        for (int s = 0; s < C::NS - 1 && s < nmax; ++s) issue(s);
-#pragma unroll 1
-        for (int t = 0; t < nmax; ++t) {
-            if (t + C::NS - 1 < nmax) issue(t + C::NS - 1);
+        auto consume = [&](int t) {
             const unsigned gs = gbase + (unsigned)t;
             mbar_wait(bar0 + 8 * (gs % C::NS), (gs / C::NS) & 1);
-            const float *sl = reinterpret_cast<const float *>(wbase + (gs % C::NS) * C::STAGE_BYTES) +
-                              pair * C::SLOT;
-            float4 xr[NBK];
+            const float *sl = my_slot + (gs % C::NS) * (C::STAGE_BYTES / 4);
 #pragma unroll
-            for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(sl + boff[b]);
-            const float y = sl[C::LDK] - p.y_shift;
-            float4 xa[NBK];
+            for (int r = 0; r < R; ++r) {
+                const float *rw = sl + r * C::ROW;
+                float4 xr[NBK];
 #pragma unroll
-            for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
-            if (HAS_W) {
-                const float w = sl[C::LDK + 1];
+                for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(rw + boff[b]);
+                const float y = rw[C::LDK] - p.y_shift;
+                float4 xa[NBK];
 #pragma unroll
-                for (int b = 0; b < NBK; ++b) {
-                    xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
+                for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
+                if (HAS_W) {
+                    const float w = rw[C::LDK + 1];
+#pragma unroll
+                    for (int b = 0; b < NBK; ++b) {
+                        xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
+                    }
                 }
-            }
-            int e = 0;
+                int e = 0;
 #pragma unroll
-            for (int d = 0; d <= (NBK - 1) / 2; ++d) {
+                for (int d = 0; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+                    for (int b = 0; b < NBK; b += 2) {
+                        const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+                        const float4 bq = xr[(b + d) % NBK];
+                        const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
+                        if (d == 0) {
+#pragma unroll
+                            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                                for (int nn = 0; nn <= m; ++nn, ++e)
+                                    acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                        } else {
+#pragma unroll
+                            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                                for (int nn = 0; nn < 4; ++nn, ++e)
+                                    acc[e] = fmaf(av[m], bv[nn], acc[e]);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int b = 0; b < NBK; b += 2) {
                     const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-                    const float4 bq = xr[(b + d) % NBK];
-                    const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
-                    if (d == 0) {
 #pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int nn = 0; nn <= m; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                    } else {
-#pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int nn = 0; nn < 4; ++nn, ++e) acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                    }
+                    for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
                 }
             }
-#pragma unroll
-            for (int b = 0; b < NBK; b += 2) {
-                const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-#pragma unroll
-                for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
-            }
             __syncwarp();   // all lanes done with this stage before it is refilled
+        };
+
+        // prologue: stages 0 .. NS-2, then ids of stages NS-1 and NS in the ring
+        for (int s = 0; s < C::NS - 1 && s < nst; ++s) issue(s, ld_idx(R * s), ld_idx(R * s + 1));
+        int ra0 = ld_idx(R * (C::NS - 1)), rb0 = ld_idx(R * (C::NS - 1) + 1);
+        int ra1 = ld_idx(R * C::NS), rb1 = ld_idx(R * C::NS + 1);
+        for (int t = 0; t < nst; t += 2) {
+            {   // even stage of the pair: ring entry 0
+                const int s = t + C::NS - 1;
+                if (s < nst) issue(s, ra0, rb0);
+                ra0 = ld_idx(R * (s + 2));
+                rb0 = ld_idx(R * (s + 2) + 1);
+                const int pf = R * s + C::PF;
+                if (pf < n && ((k0 + pf) & 31) < R)
+                    prefetch_l2(h ? (const void *)(valp + pf) : (const void *)(idxp + pf));
+                consume(t);
+            }
+            if (t + 1 < nst) {   // odd stage: ring entry 1
+                const int s = t + C::NS;
+                if (s < nst) issue(s, ra1, rb1);
+                ra1 = ld_idx(R * (s + 2));
+                rb1 = ld_idx(R * (s + 2) + 1);
+                consume(t + 1);
+            }
         }
-        gstep = gbase + (unsigned)nmax;
+        gst = gbase + (unsigned)nst;
 
         // scatter the lane's accumulators into the pair's packed [A | b]
         {
@@ -1170,26 +1202,26 @@ PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_
 
 bool use_pair(int D) { return D <= 20; }
 
-template <int NBK, bool W>
+template <int NBK, bool W, bool FB>
 int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     using C = PairCfg<NBK>;
     const size_t smem = (size_t)C::WARP_BYTES * C::WARPS;
 
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_pair<NBK, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_pair<NBK, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, W>, C::WARPS * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, W, FB>, C::WARPS * 32,
                                                   smem);
     const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
     const int64_t want = ceil_div(groups, C::WARPS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_pair<NBK, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
+    if (grid > 0) k_als_pair<NBK, W, FB><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
         k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
     return check_launch("mcf_als_half_step(pair)");
@@ -1198,9 +1230,10 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int nb = (p.D + 3) / 4;
-    if (nb <= 1) return launch_pair<1, W>(p, q, s);
-    if (nb <= 3) return launch_pair<3, W>(p, q, s);
-    return launch_pair<5, W>(p, q, s);
+    if (nb <= 1) return launch_pair<1, W, false>(p, q, s);
+    if (nb <= 3) return launch_pair<3, W, false>(p, q, s);
+    if (nb == 5) return launch_pair<5, W, true>(p, q, s);
+    return launch_pair<5, W, false>(p, q, s);
 }
 
 size_t pair_gram(int D) {
