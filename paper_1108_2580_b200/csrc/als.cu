@@ -625,8 +625,10 @@ struct PairCfg {
     static constexpr int RING_BYTES = NS * STAGE_BYTES;
     static constexpr int SOLVE_BYTES = PAIRS * GSTRIDE * 4;
     // the gather ring and the solve buffer are never live at the same time
-    static constexpr int WARP_BYTES =
+    static constexpr int RING_AREA =
         ((RING_BYTES > SOLVE_BYTES ? RING_BYTES : SOLVE_BYTES) + 127) / 128 * 128;
+    static constexpr int NR = 8;                   // id ring entries (>= NS)
+    static constexpr int WARP_BYTES = RING_AREA + PAIRS * NR * R * 4;
     static constexpr int WARPS = 4;
     static constexpr int PF = 64;                  // L2 prefetch distance (ratings)
 };
@@ -756,10 +758,11 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 // split between the two lanes, zero-fill past the task end) and the ratings
 // with 4 B cp.async, R = 2 ratings per pipeline stage; every lane's copies
 // are tracked by the stage's mbarrier (cp.async.mbarrier.arrive.noinc, 32
-// arrivals), so a stage is waited on individually, NS-1 stages after its
-// issue.  Partner ids are register-prefetched two stages ahead with a
-// statically indexed ring (the loop is unrolled by 2 stages, so no register
-// moves ever wait on an in-flight load).
+// arrivals), so a stage is waited on individually, NS-2 stages after its
+// issue.  Partner ids travel the same way: issuing stage s also cp.asyncs
+// the ids of stage s+NS-1 into a small per-pair ring in shared memory, and
+// they are read (after stage s's barrier has been waited on) when stage
+// s+NS-1 is issued -- no register ever waits on an in-flight load.
 template <int NBK, bool HAS_W, bool FULLBLK>
 __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK>;
@@ -774,6 +777,9 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
     float *my_g = reinterpret_cast<float *>(wbase) + pair * C::GSTRIDE;  // aliases the ring
     const unsigned my_slot_s = wbase_s + pair * C::SLOT * 4;
     const float *my_slot = reinterpret_cast<const float *>(wbase) + pair * C::SLOT;
+    // ids ring: [PAIRS][NR][R] int32 after the gather ring / solve area
+    int *ring_ids = reinterpret_cast<int *>(wbase + C::RING_AREA) + pair * C::NR * C::R;
+    const unsigned ring_ids_s = wbase_s + C::RING_AREA + pair * C::NR * C::R * 4;
     const int nb_real = FULLBLK ? NBK : (p.D + 3) / 4;
     int boff[NBK];   // float offset of register block b inside a row
 #pragma unroll
@@ -819,7 +825,8 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
 
         const unsigned gbase = gst;
         auto ld_idx = [&](int k) -> int { return k < n ? idxp[k] : -1; };
-        // gathers of stage s (ratings R*s .. R*s+R-1): partner ids in ia/ib
+        // gathers of stage s (ratings R*s .. R*s+R-1): partner ids in ia/ib;
+        // also brings the ids of stage s+NS-1 into the ring
         auto issue = [&](int s, int ia, int ib) {
             const unsigned gs = gbase + (unsigned)s;
             const unsigned ss = my_slot_s + (gs % C::NS) * C::STAGE_BYTES;
@@ -834,7 +841,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(rs + 16 * b),
                                  "l"(src + 4 * b), "r"((ok && (FULLBLK || b < nb_real)) ? 16 : 0));
             }
-            // lane h brings the rating (and weight) of row h
+            // lane h brings the rating (and weight) of row h ...
             const int k = R * s + h;
             const bool okv = k < n;
             const unsigned ys = ss + h * C::ROW * 4 + 4 * C::LDK;
@@ -843,8 +850,17 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
             if (HAS_W)
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(ys + 4),
                              "l"(wtsp + (okv ? k : 0)), "r"(okv ? 4 : 0));
+            // ... and the partner id of row h of stage s + NS - 1
+            const int ku = R * (s + C::NS - 1) + h;
+            const bool oku = ku < n;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
+                         ::"r"(ring_ids_s + 4 * (R * ((gs + C::NS - 1) % C::NR) + h)),
+                         "l"(idxp + (oku ? ku : 0)), "r"(oku ? 4 : 0));
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar0 + 8 * (gs % C::NS))
                          : "memory");
+            const int pf = R * s + C::PF;
+            if (pf < n && ((k0 + pf) & 31) < R)
+                prefetch_l2(h ? (const void *)(valp + pf) : (const void *)(idxp + pf));
         };
         auto consume = [&](int t) {
             const unsigned gs = gbase + (unsigned)t;
@@ -900,27 +916,15 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams
             __syncwarp();   // all lanes done with this stage before it is refilled
         };
 
-        // prologue: stages 0 .. NS-2, then ids of stages NS-1 and NS in the ring
+        // prologue: stages 0 .. NS-2 with ids loaded directly
         for (int s = 0; s < C::NS - 1 && s < nst; ++s) issue(s, ld_idx(R * s), ld_idx(R * s + 1));
-        int ra0 = ld_idx(R * (C::NS - 1)), rb0 = ld_idx(R * (C::NS - 1) + 1);
-        int ra1 = ld_idx(R * C::NS), rb1 = ld_idx(R * C::NS + 1);
-        for (int t = 0; t < nst; t += 2) {
-            {   // even stage of the pair: ring entry 0
-                const int s = t + C::NS - 1;
-                if (s < nst) issue(s, ra0, rb0);
-                ra0 = ld_idx(R * (s + 2));
-                rb0 = ld_idx(R * (s + 2) + 1);
-                const int pf = R * s + C::PF;
-                if (pf < n && ((k0 + pf) & 31) < R)
-                    prefetch_l2(h ? (const void *)(valp + pf) : (const void *)(idxp + pf));
-                consume(t);
-            }
-            if (t + 1 < nst) {   // odd stage: ring entry 1
-                const int s = t + C::NS;
-                if (s < nst) issue(s, ra1, rb1);
-                ra1 = ld_idx(R * (s + 2));
-                rb1 = ld_idx(R * (s + 2) + 1);
-                consume(t + 1);
+        for (int t = 0; t < nst; ++t) {
+            consume(t);   // waits stage t: the ids of stage t+NS-1 have landed too
+            const int s = t + C::NS - 1;
+            if (s < nst) {
+                const int2 ids = *reinterpret_cast<const int2 *>(ring_ids + R * ((gbase + s) % C::NR));
+                // a zero-filled id (past the task end) reads as 0: mask by the task length
+                issue(s, R * s < n ? ids.x : -1, R * s + 1 < n ? ids.y : -1);
             }
         }
         gst = gbase + (unsigned)nst;
