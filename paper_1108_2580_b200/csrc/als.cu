@@ -630,6 +630,7 @@ struct PairCfg {
     static constexpr int NR = 8;                   // id ring entries (>= NS)
     static constexpr int WARP_BYTES = RING_AREA + PAIRS * NR * R * 4;
     static constexpr int WARPS = 4;
+    static constexpr int MIN_CTAS = 2;             // 8 warps / SM (register bound: 138 accumulators)
     static constexpr int PF = 64;                  // L2 prefetch distance (ratings)
 };
 
@@ -764,7 +765,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 // they are read (after stage s's barrier has been waited on) when stage
 // s+NS-1 is issued -- no register ever waits on an in-flight load.
 template <int NBK, bool HAS_W, bool FULLBLK>
-__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32) k_als_pair(AlsParams p, PairPlan q) {
+__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CTAS) k_als_pair(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK>;
     constexpr int R = C::R;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
