@@ -756,6 +756,116 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     while (!mbar_try(bar, parity)) {
     }
 }
+
+// Paired FP32 FMA (sm_100 FFMA2): acc.{x,y} += a * b.{x,y}; the scalar a is
+// a broadcast operand of the instruction (no register moves).
+__device__ __forceinline__ void ffma2(float2 &acc, float a, float bx, float by) {
+    unsigned long long A, B, C;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(bx), "f"(by));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(acc.x), "f"(acc.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(C));
+}
+
+// Per-lane accumulators of the pair path, FFMA2-shaped: for each of HALF
+// diagonal blocks the lower 4x4 triangle (m=0: 1 scalar; m=1: a pair; m=2: a
+// pair + a scalar; m=3: two pairs), for each of NOFF off-diagonal blocks
+// 4 rows x 2 pairs, for each of HALF rhs blocks 2 pairs.
+template <int NBK>
+struct PairAcc {
+    static constexpr int HALF = (NBK + 1) / 2;
+    static constexpr int NOFF = ((NBK - 1) / 2) * HALF;
+    float dsc[HALF][2];
+    float2 dpr[HALF][4];
+    float2 off[NOFF > 0 ? NOFF : 1][4][2];
+    float2 rhs[HALF][2];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < HALF; ++i) {
+            dsc[i][0] = dsc[i][1] = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dpr[i][k] = make_float2(0.f, 0.f);
+            rhs[i][0] = rhs[i][1] = make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < (NOFF > 0 ? NOFF : 1); ++i)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) off[i][m][0] = off[i][m][1] = make_float2(0.f, 0.f);
+    }
+    // one rating: register blocks xr (unscaled) / xa (weight-scaled), target y
+    __device__ __forceinline__ void add(const float4 (&xa)[NBK], const float4 (&xr)[NBK], float y) {
+#pragma unroll
+        for (int i = 0; i < HALF; ++i) {
+            const int b = 2 * i;
+            const float a[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+            const float4 u = xr[b];
+            dsc[i][0] = fmaf(a[0], u.x, dsc[i][0]);
+            ffma2(dpr[i][0], a[1], u.x, u.y);
+            ffma2(dpr[i][1], a[2], u.x, u.y);
+            dsc[i][1] = fmaf(a[2], u.z, dsc[i][1]);
+            ffma2(dpr[i][2], a[3], u.x, u.y);
+            ffma2(dpr[i][3], a[3], u.z, u.w);
+            ffma2(rhs[i][0], y, a[0], a[1]);
+            ffma2(rhs[i][1], y, a[2], a[3]);
+        }
+        int o = 0;
+#pragma unroll
+        for (int d = 1; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+            for (int i = 0; i < HALF; ++i, ++o) {
+                const int b = 2 * i;
+                const float a[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
+                const float4 u = xr[(b + d) % NBK];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    ffma2(off[o][m][0], a[m], u.x, u.y);
+                    ffma2(off[o][m][1], a[m], u.z, u.w);
+                }
+            }
+        }
+    }
+    // write into the packed [A | b] (pidx layout) of lane h's memory blocks
+    __device__ __forceinline__ void scatter(float *g, int h, int rhs0) const {
+#pragma unroll
+        for (int i = 0; i < HALF; ++i) {
+            const int A = (2 * i + h) % NBK, r = 4 * A;
+            g[pidx(r, r)] = dsc[i][0];
+            g[pidx(r + 1, r)] = dpr[i][0].x;
+            g[pidx(r + 1, r + 1)] = dpr[i][0].y;
+            g[pidx(r + 2, r)] = dpr[i][1].x;
+            g[pidx(r + 2, r + 1)] = dpr[i][1].y;
+            g[pidx(r + 2, r + 2)] = dsc[i][1];
+            g[pidx(r + 3, r)] = dpr[i][2].x;
+            g[pidx(r + 3, r + 1)] = dpr[i][2].y;
+            g[pidx(r + 3, r + 2)] = dpr[i][3].x;
+            g[pidx(r + 3, r + 3)] = dpr[i][3].y;
+            g[rhs0 + r] = rhs[i][0].x;
+            g[rhs0 + r + 1] = rhs[i][0].y;
+            g[rhs0 + r + 2] = rhs[i][1].x;
+            g[rhs0 + r + 3] = rhs[i][1].y;
+        }
+        int o = 0;
+#pragma unroll
+        for (int d = 1; d <= (NBK - 1) / 2; ++d) {
+#pragma unroll
+            for (int i = 0; i < HALF; ++i, ++o) {
+                const int A = (2 * i + h) % NBK, B = (2 * i + d + h) % NBK;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const float v[4] = {off[o][m][0].x, off[o][m][0].y, off[o][m][1].x,
+                                        off[o][m][1].y};
+#pragma unroll
+                    for (int nn = 0; nn < 4; ++nn) {
+                        const int r_ = 4 * A + m, c_ = 4 * B + nn;
+                        g[r_ >= c_ ? pidx(r_, c_) : pidx(c_, r_)] = v[nn];
+                    }
+                }
+            }
+        }
+    }
+};
+
 // Each lane pair gathers its own partner rows with cp.async (16 B blocks
 // split between the two lanes, zero-fill past the task end) and the ratings
 // with 4 B cp.async, R = 2 ratings per pipeline stage; every lane's copies
@@ -821,9 +931,8 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
                 prefetch_l2(h ? (const void *)(valp + o) : (const void *)(idxp + o));
         __syncwarp();   // the previous group's solve is done with the (aliased) ring
 
-        float acc[C::NACC];
-#pragma unroll
-        for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
+        PairAcc<NBK> acc;
+        acc.zero();
 
         const unsigned gbase = gst;
         auto ld_idx = [&](int k) -> int { return k < n ? idxp[k] : -1; };
@@ -885,35 +994,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
                         xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
                     }
                 }
-                int e = 0;
-#pragma unroll
-                for (int d = 0; d <= (NBK - 1) / 2; ++d) {
-#pragma unroll
-                    for (int b = 0; b < NBK; b += 2) {
-                        const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-                        const float4 bq = xr[(b + d) % NBK];
-                        const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
-                        if (d == 0) {
-#pragma unroll
-                            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                                for (int nn = 0; nn <= m; ++nn, ++e)
-                                    acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                        } else {
-#pragma unroll
-                            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                                for (int nn = 0; nn < 4; ++nn, ++e)
-                                    acc[e] = fmaf(av[m], bv[nn], acc[e]);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int b = 0; b < NBK; b += 2) {
-                    const float av[4] = {xa[b].x, xa[b].y, xa[b].z, xa[b].w};
-#pragma unroll
-                    for (int m = 0; m < 4; ++m, ++e) acc[e] = fmaf(y, av[m], acc[e]);
-                }
+                acc.add(xa, xr, y);
             }
             __syncwarp();   // all lanes done with this stage before it is refilled
         };
@@ -932,37 +1013,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
         gst = gbase + (unsigned)nst;
 
         // scatter the lane's accumulators into the pair's packed [A | b]
-        {
-            int e = 0;
-#pragma unroll
-            for (int d = 0; d <= (NBK - 1) / 2; ++d) {
-#pragma unroll
-                for (int b = 0; b < NBK; b += 2) {
-                    const int A = (b + h) % NBK, B = (b + d + h) % NBK;
-                    if (d == 0) {
-#pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int nn = 0; nn <= m; ++nn, ++e)
-                                my_g[pidx(4 * A + m, 4 * A + nn)] = acc[e];
-                    } else {
-#pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int nn = 0; nn < 4; ++nn, ++e) {
-                                const int r_ = 4 * A + m, c_ = 4 * B + nn;
-                                my_g[r_ >= c_ ? pidx(r_, c_) : pidx(c_, r_)] = acc[e];
-                            }
-                    }
-                }
-            }
-#pragma unroll
-            for (int b = 0; b < NBK; b += 2) {
-                const int A = (b + h) % NBK;
-#pragma unroll
-                for (int m = 0; m < 4; ++m, ++e) my_g[C::RHS0 + 4 * A + m] = acc[e];
-            }
-        }
+        acc.scatter(my_g, h, C::RHS0);
         __syncwarp();
         if (task < q.n_tasks) {
             if (slot >= 0) {
@@ -991,7 +1042,6 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
 // registers, so 12 warps / SM hide the L2 latency of the partner-row
 // gathers, which go straight to registers (read-only L1 path) three ratings
 // ahead, without a shared-memory ring.
-__constant__ int QMAP[4][4] = {{0, 2, 4, 3}, {3, 1, 4, 3}, {1, 4, 0, 2}, {2, 0, 3, 4}};
 
 struct QuadCfg {
     static constexpr int LDK = 20;
@@ -1004,30 +1054,24 @@ struct QuadCfg {
     static constexpr int PF = 64;
 };
 
-__device__ __forceinline__ float4 ldg_nc4(const float *p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
-    return v;
+// QMAP packed 3 bits per entry: lane h, register block j -> bits 12h + 3j
+constexpr unsigned long long QMAP_BITS =
+    (0ull << 0) | (2ull << 3) | (4ull << 6) | (3ull << 9) |        // lane 0
+    (3ull << 12) | (1ull << 15) | (4ull << 18) | (3ull << 21) |    // lane 1
+    (1ull << 24) | (4ull << 27) | (0ull << 30) | (2ull << 33) |    // lane 2
+    (2ull << 36) | (0ull << 39) | (3ull << 42) | (4ull << 45);     // lane 3
+__device__ __forceinline__ int qmap(int h, int j) {
+    return (int)((QMAP_BITS >> (12 * h + 3 * j)) & 7ull);
 }
 
-template <bool HAS_W>
+template <bool HAS_W, bool FULLBLK>
 __global__ void __launch_bounds__(QuadCfg::WARPS * 32, 3) k_als_quad(AlsParams p, PairPlan q) {
     using C = QuadCfg;
     __shared__ float gbuf[C::WARPS][C::ROWS * C::GSTRIDE];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rs = lane >> 2, h = lane & 3, qb = lane & 28;
     float *my_g = gbuf[warp] + rs * C::GSTRIDE;
-    const int nb_real = (p.D + 3) / 4;
-    int moff[4];
-    bool mok[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int m = QMAP[h][j];
-        moff[j] = 4 * m;
-        mok[j] = m < nb_real;
-    }
+    const int nb_real = FULLBLK ? 5 : (p.D + 3) / 4;
     const int64_t n_groups = (q.n_tasks + C::ROWS - 1) / C::ROWS;
 
     for (;;) {
@@ -1067,12 +1111,19 @@ __global__ void __launch_bounds__(QuadCfg::WARPS * 32, 3) k_als_quad(AlsParams p
         int ci = ld_i(h), ni = ld_i(4 + h);
         float cv = ld_v(h), nv = ld_v(4 + h);
         float cw = ld_w(h), nw = ld_w(4 + h);
+        // invalid ids (past the task end) load nothing: those ratings are
+        // skipped by the FMA step below, so the stale registers are never read
         auto gather = [&](int id, float4 (&x)[4]) {
             const float *src = p.fixed + (size_t)(id >= 0 ? id : 0) * p.ld;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (id >= 0 && mok[j]) x[j] = ldg_nc4(src + moff[j]);
+                const int m = qmap(h, j);
+                if (FULLBLK) {
+                    if (id >= 0) x[j] = __ldg(reinterpret_cast<const float4 *>(src + 4 * m));
+                } else {
+                    if (id >= 0) x[j] = m < nb_real ? __ldg(reinterpret_cast<const float4 *>(src + 4 * m))
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
         };
         auto fma_rating = [&](const float4 (&x)[4], float y, float w) {
@@ -1119,10 +1170,8 @@ __global__ void __launch_bounds__(QuadCfg::WARPS * 32, 3) k_als_quad(AlsParams p
                 const float y = __shfl_sync(FULL, cv, qb + u) - p.y_shift;
                 const float w = HAS_W ? __shfl_sync(FULL, cw, qb + u) : 1.f;
                 const int idn = __shfl_sync(FULL, ni, qb + u);   // rating t + 4
-                if (t < nmax) {
-                    fma_rating(xb[u], y, w);
-                    gather(t + 4 < nmax ? idn : -1, xb[u]);
-                }
+                if (t < n) fma_rating(xb[u], y, w);
+                if (t < nmax) gather(t + 4 < n ? idn : -1, xb[u]);
             }
             ci = ni; cv = nv; cw = nw;
             ni = ld_i(4 * c + 8 + h);
@@ -1136,7 +1185,7 @@ __global__ void __launch_bounds__(QuadCfg::WARPS * 32, 3) k_als_quad(AlsParams p
 
         // scatter into the task's packed [A | b]
         {
-            const int A = QMAP[h][0], B1 = QMAP[h][1], B2 = QMAP[h][2], B3 = QMAP[h][3];
+            const int A = qmap(h, 0), B1 = qmap(h, 1), B2 = qmap(h, 2), B3 = qmap(h, 3);
             int e = 0;
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -1428,29 +1477,30 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     return check_launch("mcf_als_half_step(pair)");
 }
 
-template <bool W>
+template <bool W, bool FB>
 int launch_quad(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     using C = QuadCfg;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_quad<W>, C::WARPS * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_quad<W, FB>, C::WARPS * 32, 0);
     const int64_t groups = ceil_div(q.n_tasks, C::ROWS);
     const int64_t grid = std::min<int64_t>(ceil_div(groups, C::WARPS), (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_quad<W><<<(unsigned)grid, C::WARPS * 32, 0, s>>>(p, q);
+    if (grid > 0) k_als_quad<W, FB><<<(unsigned)grid, C::WARPS * 32, 0, s>>>(p, q);
     if (q.n_heavy > 0) k_als_heavy<5><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
     return check_launch("mcf_als_half_step(quad)");
 }
 
-int g_kernel_choice = -1;   // -1: default, 0: pair, 1: quad (MCF_ALS_KERNEL)
+int g_kernel_choice = -1;   // -1: unset, 0: pair (default), 1: quad (MCF_ALS_KERNEL=quad)
 
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     if (g_kernel_choice < 0) {
         const char *e = getenv("MCF_ALS_KERNEL");
-        g_kernel_choice = (e && e[0] == 'p') ? 0 : 1;
+        g_kernel_choice = (e && e[0] == 'q') ? 1 : 0;
     }
-    if (g_kernel_choice == 1 && p.D > 12) return launch_quad<W>(p, q, s);
+    if (g_kernel_choice == 1 && p.D > 12)
+        return p.D > 16 && p.ld == 20 ? launch_quad<W, true>(p, q, s) : launch_quad<W, false>(p, q, s);
     const int nb = (p.D + 3) / 4;
     if (nb <= 1) return launch_pair<1, W, false>(p, q, s);
     if (nb <= 3) return launch_pair<3, W, false>(p, q, s);
