@@ -35,7 +35,6 @@
 // threads, CTA-cooperative Cholesky (correctness path for configs 3/4; the
 // tensor-core path for D >= 64 replaces it).
 #include <algorithm>
-#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -1027,199 +1026,6 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
     }
 }
 
-// ---------------------------------------------------------------------------
-// quad path, D <= 20: 4 lanes per task, 8 tasks per warp, 16 warps / SM.
-//
-// The packed [A | b] of a D <= 20 row (5 blocks of 4) is covered by 4 lanes
-// running ONE instruction stream: each lane loads 4 register blocks
-// R0..R3 = memory blocks QMAP[h][0..3] of the partner row and accumulates
-// R0 x R1, R0 x R2, R0 x R3 (3 x 16 FMA), the lower triangle of R1 x R1
-// (10 FMA) and y R0, y R1 (8 FMA): 66 FMA per lane per rating, 264 for the
-// 230 useful (87%).  The lane maps below were found by exhaustive covering
-// search: together the 4 lanes produce every off-diagonal block pair (10),
-// every diagonal block (5; lane 1's R0 x R3 is block (3,3) in full) and
-// every rhs block (5).  With ~66 accumulators a thread needs ~128
-// registers, so 12 warps / SM hide the L2 latency of the partner-row
-// gathers, which go straight to registers (read-only L1 path) three ratings
-// ahead, without a shared-memory ring.
-
-struct QuadCfg {
-    static constexpr int LDK = 20;
-    static constexpr int ROWS = 8;                  // tasks per warp
-    static constexpr int RHS0 = LDK * (LDK + 1) / 2;
-    static constexpr int GRAM = RHS0 + LDK;
-    static constexpr int GSTRIDE = GRAM | 1;
-    static constexpr int WARPS = 4;
-    static constexpr int NACC = 66;
-    static constexpr int PF = 64;
-};
-
-// QMAP packed 3 bits per entry: lane h, register block j -> bits 12h + 3j
-constexpr unsigned long long QMAP_BITS =
-    (0ull << 0) | (2ull << 3) | (4ull << 6) | (3ull << 9) |        // lane 0
-    (3ull << 12) | (1ull << 15) | (4ull << 18) | (3ull << 21) |    // lane 1
-    (1ull << 24) | (4ull << 27) | (0ull << 30) | (2ull << 33) |    // lane 2
-    (2ull << 36) | (0ull << 39) | (3ull << 42) | (4ull << 45);     // lane 3
-__device__ __forceinline__ int qmap(int h, int j) {
-    return (int)((QMAP_BITS >> (12 * h + 3 * j)) & 7ull);
-}
-
-template <bool HAS_W, bool FULLBLK>
-__global__ void __launch_bounds__(QuadCfg::WARPS * 32, 3) k_als_quad(AlsParams p, PairPlan q) {
-    using C = QuadCfg;
-    __shared__ float gbuf[C::WARPS][C::ROWS * C::GSTRIDE];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rs = lane >> 2, h = lane & 3, qb = lane & 28;
-    float *my_g = gbuf[warp] + rs * C::GSTRIDE;
-    const int nb_real = FULLBLK ? 5 : (p.D + 3) / 4;
-    const int64_t n_groups = (q.n_tasks + C::ROWS - 1) / C::ROWS;
-
-    for (;;) {
-        int64_t grp = 0;
-        if (lane == 0) grp = atomicAdd(q.group_counter, 1);
-        grp = __shfl_sync(FULL, grp, 0);
-        if (grp >= n_groups) break;
-        const int64_t task = grp * C::ROWS + rs;
-        int row = 0, slot = -1, n = 0;
-        int64_t k0 = 0;
-        if (task < q.n_tasks) {
-            row = q.task_row[task];
-            k0 = q.task_k0[task];
-            n = q.task_n[task];
-            slot = q.task_slot[task];
-        }
-        int nmax = n;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, o));
-        const int32_t *idxp = p.idx + k0;
-        const float *valp = p.val + k0;
-        const float *wtsp = HAS_W ? p.wts + k0 : nullptr;
-        if (h == 0 && n > 0)
-            for (int o = 0; o < min(n, C::PF); o += 32) {
-                prefetch_l2(idxp + o);
-                prefetch_l2(valp + o);
-            }
-
-        float acc[C::NACC];
-#pragma unroll
-        for (int e = 0; e < C::NACC; ++e) acc[e] = 0.f;
-
-        // lane h of the quad holds element 4c + h of chunk c: ids, ratings, weights
-        auto ld_i = [&](int k) { return k < n ? idxp[k] : -1; };
-        auto ld_v = [&](int k) { return k < n ? valp[k] : 0.f; };
-        auto ld_w = [&](int k) { return (HAS_W && k < n) ? wtsp[k] : 0.f; };
-        int ci = ld_i(h), ni = ld_i(4 + h);
-        float cv = ld_v(h), nv = ld_v(4 + h);
-        float cw = ld_w(h), nw = ld_w(4 + h);
-        // invalid ids (past the task end) load nothing: those ratings are
-        // skipped by the FMA step below, so the stale registers are never read
-        auto gather = [&](int id, float4 (&x)[4]) {
-            const float *src = p.fixed + (size_t)(id >= 0 ? id : 0) * p.ld;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int m = qmap(h, j);
-                if (FULLBLK) {
-                    if (id >= 0) x[j] = __ldg(reinterpret_cast<const float4 *>(src + 4 * m));
-                } else {
-                    if (id >= 0) x[j] = m < nb_real ? __ldg(reinterpret_cast<const float4 *>(src + 4 * m))
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-        };
-        auto fma_rating = [&](const float4 (&x)[4], float y, float w) {
-            float4 a0 = x[0], a1 = x[1];
-            if (HAS_W) {
-                a0.x *= w; a0.y *= w; a0.z *= w; a0.w *= w;
-                a1.x *= w; a1.y *= w; a1.z *= w; a1.w *= w;
-            }
-            const float r0[4] = {a0.x, a0.y, a0.z, a0.w};
-            const float r1[4] = {a1.x, a1.y, a1.z, a1.w};
-            const float u1[4] = {x[1].x, x[1].y, x[1].z, x[1].w};
-            const float u2[4] = {x[2].x, x[2].y, x[2].z, x[2].w};
-            const float u3[4] = {x[3].x, x[3].y, x[3].z, x[3].w};
-            int e = 0;
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-#pragma unroll
-                for (int nn = 0; nn < 4; ++nn) acc[e + nn] = fmaf(r0[m], u1[nn], acc[e + nn]);
-#pragma unroll
-                for (int nn = 0; nn < 4; ++nn) acc[e + 4 + nn] = fmaf(r0[m], u2[nn], acc[e + 4 + nn]);
-#pragma unroll
-                for (int nn = 0; nn < 4; ++nn) acc[e + 8 + nn] = fmaf(r0[m], u3[nn], acc[e + 8 + nn]);
-                e += 12;
-            }
-#pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                for (int nn = 0; nn <= m; ++nn, ++e) acc[e] = fmaf(r1[m], u1[nn], acc[e]);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) acc[58 + m] = fmaf(y, r0[m], acc[58 + m]);
-#pragma unroll
-            for (int m = 0; m < 4; ++m) acc[62 + m] = fmaf(y, r1[m], acc[62 + m]);
-        };
-
-        // x(t) for t = 4c + u lives in buffer u; it is gathered right after
-        // x(t - 4) was consumed, i.e. three ratings of FMAs ahead of its use
-        float4 xb[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) gather(__shfl_sync(FULL, ci, qb + u), xb[u]);
-        for (int c = 0; 4 * c < nmax; ++c) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = 4 * c + u;
-                const float y = __shfl_sync(FULL, cv, qb + u) - p.y_shift;
-                const float w = HAS_W ? __shfl_sync(FULL, cw, qb + u) : 1.f;
-                const int idn = __shfl_sync(FULL, ni, qb + u);   // rating t + 4
-                if (t < n) fma_rating(xb[u], y, w);
-                if (t < nmax) gather(t + 4 < n ? idn : -1, xb[u]);
-            }
-            ci = ni; cv = nv; cw = nw;
-            ni = ld_i(4 * c + 8 + h);
-            nv = ld_v(4 * c + 8 + h);
-            nw = ld_w(4 * c + 8 + h);
-            if (h == 0 && 4 * c + C::PF < n && ((k0 + 4 * c + C::PF) & 31) < 4) {
-                prefetch_l2(idxp + 4 * c + C::PF);
-                prefetch_l2(valp + 4 * c + C::PF);
-            }
-        }
-
-        // scatter into the task's packed [A | b]
-        {
-            const int A = qmap(h, 0), B1 = qmap(h, 1), B2 = qmap(h, 2), B3 = qmap(h, 3);
-            int e = 0;
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int Bs[3] = {B1, B2, B3};
-#pragma unroll
-                for (int s2 = 0; s2 < 3; ++s2)
-#pragma unroll
-                    for (int nn = 0; nn < 4; ++nn, ++e) {
-                        const int r_ = 4 * A + m, c_ = 4 * Bs[s2] + nn;
-                        my_g[r_ >= c_ ? pidx(r_, c_) : pidx(c_, r_)] = acc[e];
-                    }
-            }
-#pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                for (int nn = 0; nn <= m; ++nn, ++e) my_g[pidx(4 * B1 + m, 4 * B1 + nn)] = acc[e];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) my_g[C::RHS0 + 4 * A + m] = acc[58 + m];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) my_g[C::RHS0 + 4 * B1 + m] = acc[62 + m];
-        }
-        __syncwarp();
-        if (task < q.n_tasks) {
-            if (slot >= 0) {
-                float *dst = p.partials + (size_t)slot * C::GRAM;
-                for (int i = h; i < C::GRAM; i += 4) dst[i] = my_g[i];
-            } else if (h == 0) {
-                finish_row<C::LDK>(p, my_g, row, n);
-            }
-        }
-        __syncwarp();
-    }
-}
-
 // Hot rows: one warp per row sums its chunk partials in chunk order, then
 // the warp solves cooperatively (lane i owns row i of A, right-looking
 // Cholesky with shuffles).
@@ -1477,30 +1283,8 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     return check_launch("mcf_als_half_step(pair)");
 }
 
-template <bool W, bool FB>
-int launch_quad(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
-    using C = QuadCfg;
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_quad<W, FB>, C::WARPS * 32, 0);
-    const int64_t groups = ceil_div(q.n_tasks, C::ROWS);
-    const int64_t grid = std::min<int64_t>(ceil_div(groups, C::WARPS), (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_quad<W, FB><<<(unsigned)grid, C::WARPS * 32, 0, s>>>(p, q);
-    if (q.n_heavy > 0) k_als_heavy<5><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
-    return check_launch("mcf_als_half_step(quad)");
-}
-
-int g_kernel_choice = -1;   // -1: unset, 0: pair (default), 1: quad (MCF_ALS_KERNEL=quad)
-
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
-    if (g_kernel_choice < 0) {
-        const char *e = getenv("MCF_ALS_KERNEL");
-        g_kernel_choice = (e && e[0] == 'q') ? 1 : 0;
-    }
-    if (g_kernel_choice == 1 && p.D > 12)
-        return p.D > 16 && p.ld == 20 ? launch_quad<W, true>(p, q, s) : launch_quad<W, false>(p, q, s);
     const int nb = (p.D + 3) / 4;
     if (nb <= 1) return launch_pair<1, W, false>(p, q, s);
     if (nb <= 3) return launch_pair<3, W, false>(p, q, s);

@@ -5,7 +5,7 @@
 // is built once, on device, and stays resident.  In-row order must equal
 // record order (argsort kind="stable"), bit for bit.
 //
-//   1. degrees: histogram of keys (int atomics, exact) -> exclusive scan -> ptr
+//   1. range check of the keys (reported after the build, one sync)
 //   2. stable LSD radix sort of (key, record index) with 7/8-bit digits:
 //      per pass  (a) per-tile digit histograms, (b) one device-wide exclusive
 //      scan over the digit-major [bins][tiles] table, (c) stable scatter.
@@ -14,7 +14,9 @@
 //      digits with __match_any_sync, and keeps a warp-private running
 //      histogram; warps are then offset in order.  Record order is therefore
 //      (tile, warp, slot, lane) = ascending record index.
-//   3. gather: idx[k] = cols[perm[k]], val[k] = vals[perm[k]].
+//   3. ptr from the row boundaries of the sorted keys (no atomics: Zipf-hot
+//      rows would serialise a histogram), gather idx[k] = cols[perm[k]],
+//      val[k] = vals[perm[k]].
 #include "common.cuh"
 #include "../../include/mcf.h"
 
@@ -27,17 +29,28 @@ constexpr int RS_THREADS = RS_WARPS * 32;
 constexpr int RS_TILE = RS_THREADS * RS_SLOTS;  // 2048 records
 constexpr int RS_MAX_BINS = 256;
 
-__global__ void k_degrees(const int32_t *keys, int64_t nnz, int32_t n_rows, int64_t *cnt,
-                          int *bad) {
+__global__ void k_check(const int32_t *keys, int64_t nnz, int32_t n_rows, int *bad) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
          k += (int64_t)gridDim.x * blockDim.x) {
         const int32_t key = keys[k];
-        if (key < 0 || key >= n_rows) {
-            atomicExch(bad, 1);
-            continue;
-        }
-        atomicAdd(reinterpret_cast<unsigned long long *>(cnt + key), 1ull);
+        if (key < 0 || key >= n_rows) atomicExch(bad, 1);
     }
+}
+
+// ptr from the sorted keys: ptr[r] = first position whose key >= r (no
+// atomics -- the Zipf-hot rows would serialise a histogram).
+__global__ void k_bounds(const uint32_t *sk, int64_t nnz, int32_t n_rows, int64_t *ptr) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= nnz;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        // clamped: out-of-range keys are reported by k_check, never written past ptr
+        const int64_t lo = k == 0 ? -1 : min((int64_t)sk[k - 1], (int64_t)n_rows);
+        const int64_t hi = k == nnz ? (int64_t)n_rows : min((int64_t)sk[k], (int64_t)n_rows);
+        for (int64_t r = lo + 1; r <= hi; ++r) ptr[r] = k;
+    }
+}
+
+__global__ void k_bounds_single(int64_t nnz, int32_t n_rows, int64_t *ptr) {
+    for (int32_t r = threadIdx.x; r <= n_rows; r += blockDim.x) ptr[r] = r == 0 ? 0 : nnz;
 }
 
 // Ranks of the tile's records by digit; returns per-slot local ranks (within
@@ -155,7 +168,6 @@ int key_bits(int32_t n_rows) {
 }
 
 struct CsrWs {
-    int64_t *cnt;
     int *bad;
     uint32_t *keys[2];
     int32_t *vals[2];
@@ -167,7 +179,6 @@ struct CsrWs {
 CsrWs carve_csr(void *ws, size_t cap, int64_t nnz, int32_t n_rows, size_t *need) {
     Carve c(ws, cap);
     CsrWs w;
-    w.cnt = c.take<int64_t>((size_t)n_rows + 1);
     w.bad = c.take<int>(1);
     for (int i = 0; i < 2; ++i) {
         w.keys[i] = c.take<uint32_t>((size_t)nnz);
@@ -213,36 +224,21 @@ extern "C" int mcf_csr_build(const int32_t *keys, const int32_t *cols, const flo
         return MCF_E_WORKSPACE;
     }
     int rc;
-    if ((rc = cuda_status(cudaMemsetAsync(w.cnt, 0, sizeof(int64_t) * ((size_t)n_rows + 1), s),
-                          "memset")))
-        return rc;
     if ((rc = cuda_status(cudaMemsetAsync(w.bad, 0, sizeof(int), s), "memset"))) return rc;
     const int gs = 148 * 8;
-    if (nnz > 0) k_degrees<<<gs, 256, 0, s>>>(keys, nnz, n_rows, w.cnt, w.bad);
     int err = 0;
-    scan_exclusive<int64_t>(w.cnt, ptr_out, (int64_t)n_rows + 1, w.scan_tmp, w.scan_bytes, s,
-                            &err);
-    if (err) {
-        set_error("mcf_csr_build: scan workspace");
-        return MCF_E_WORKSPACE;
+    if (nnz > 0) k_check<<<gs, 256, 0, s>>>(keys, nnz, n_rows, w.bad);
+    if (nnz == 0) {
+        k_bounds_single<<<1, 256, 0, s>>>(0, n_rows, ptr_out);
+        return check_launch("mcf_csr_build");
     }
-    if ((rc = check_launch("mcf_csr_build/degrees"))) return rc;
-    int bad = 0;
-    if ((rc = cuda_status(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, s),
-                          "memcpy")))
-        return rc;
-    if ((rc = cuda_status(cudaStreamSynchronize(s), "sync"))) return rc;
-    if (bad) {
-        set_error("mcf_csr_build: key outside [0, n_rows)");
-        return MCF_E_RANGE;
-    }
-    if (nnz == 0) return MCF_OK;
 
     const int bits = key_bits(n_rows);
     const int64_t n_tiles = ceil_div(nnz, RS_TILE);
     int32_t *perm = w.vals[0];
     if (bits == 0) {
         k_iota<<<gs, 256, 0, s>>>(perm, nnz);
+        k_bounds_single<<<1, 256, 0, s>>>(nnz, n_rows, ptr_out);
     } else {
         const int passes = (bits + 7) / 8;
         const int dbits = (bits + passes - 1) / passes;
@@ -263,6 +259,7 @@ extern "C" int mcf_csr_build(const int32_t *keys, const int32_t *cols, const flo
             cur ^= 1;
         }
         perm = w.vals[cur];
+        k_bounds<<<gs, 256, 0, s>>>(w.keys[cur], nnz, n_rows, ptr_out);
     }
     k_gather<<<gs, 256, 0, s>>>(perm, cols, vals, nnz, idx_out, val_out);
     if (perm_out)
@@ -270,5 +267,15 @@ extern "C" int mcf_csr_build(const int32_t *keys, const int32_t *cols, const flo
                                               cudaMemcpyDeviceToDevice, s),
                               "memcpy")))
             return rc;
-    return check_launch("mcf_csr_build");
+    if ((rc = check_launch("mcf_csr_build"))) return rc;
+    int bad = 0;
+    if ((rc = cuda_status(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, s),
+                          "memcpy")))
+        return rc;
+    if ((rc = cuda_status(cudaStreamSynchronize(s), "sync"))) return rc;
+    if (bad) {
+        set_error("mcf_csr_build: key outside [0, n_rows)");
+        return MCF_E_RANGE;
+    }
+    return MCF_OK;
 }

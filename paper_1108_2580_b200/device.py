@@ -176,8 +176,11 @@ class AlsEngine:
             t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.asarray(src))
             if t.shape != (dst.shape[0], self.D):
                 raise ConfigError(f"factor shape {tuple(t.shape)} != {(dst.shape[0], self.D)}")
-            dst[:, : self.D].copy_(t.to(torch.float32), non_blocking=True)
-            dst[:, self.D:].zero_()
+            if t.device.type == "cpu" and t.dtype != torch.float32:
+                t = t.to(torch.float32)
+            dst[:, : self.D].copy_(t, non_blocking=True)
+            if self.ld > self.D:
+                dst[:, self.D:].zero_()
 
     def factors(self):
         return self.P[:, : self.D], self.Q[:, : self.D]

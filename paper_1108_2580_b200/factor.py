@@ -145,11 +145,11 @@ def _ratings_for(train: Dataset, device, keep_perm: bool, num_users=None,
 
 
 def _engine_for(model: FactorModel, train: Dataset, device, keep_perm: bool) -> AlsEngine:
+    """The model's engine over the resident layouts (factors NOT uploaded)."""
     r = _ratings_for(train, device, keep_perm, model.num_users, model.num_items)
     eng = model.engine
     if eng is None or eng.r is not r:
         eng = AlsEngine(r, model.D)
-        eng.set_factors(_host(model.p), _host(model.q))
         model.engine = eng
     return eng
 
@@ -282,11 +282,13 @@ def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: Hyp
         if weights.size != len(train_data):
             raise ShapeError(f"expected {len(train_data)} weights, got {weights.size}")
     model = init_model(kind, train_data, hyper, seed, num_users=num_users, num_items=num_items)
-    if init is not None:
-        P0, Q0 = init
-        model.p, model.q = np.asarray(P0, np.float64), np.asarray(Q0, np.float64)
     eng = _engine_for(model, train_data, device, keep_perm=weights is not None)
-    eng.set_factors(model.p, model.q)
+    if init is not None:
+        # uploaded as given (fp32 stays fp32; a pinned source copies asynchronously)
+        P0, Q0 = init
+        eng.set_factors(P0, Q0)
+    else:
+        eng.set_factors(model.p, model.q)
     eng.set_weights(weights)
     lam_c, lam_n = _lam_pair(hyper.lam, reg)
     dev = eng.device
