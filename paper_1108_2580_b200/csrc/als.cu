@@ -380,103 +380,187 @@ __global__ void __launch_bounds__(256) k_als_warp(AlsParams p) {
     if (lane < p.ld) p.out[(size_t)r * p.ld + lane] = lane < D ? b : 0.f;
 }
 
+// Paired FP32 FMA (sm_100 FFMA2): acc.{x,y} += a * b.{x,y}; the scalar a is
+// a broadcast operand of the instruction (no register moves).
+__device__ __forceinline__ void ffma2(float2 &acc, float a, float bx, float by) {
+    unsigned long long A, B, C;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(bx), "f"(by));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(acc.x), "f"(acc.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(C));
+}
+
 // ---------------------------------------------------------------------------
-// CTA path, 28 < D <= 128 (one CTA per work item)
+// wide path, 28 < D <= 128 (configs 3 and 4): one CTA per work item
+//
+// The lower triangle of A is cut into 8x8 tiles (NB8 = ceil(D/8) blocks,
+// T8 = NB8(NB8+1)/2 tiles) listed row-block by row-block, so the lanes of a
+// warp share few row blocks and their row-operand loads are shared-memory
+// broadcasts.  A team of TEAM threads owns all tiles (TPT per thread);
+// 128/TEAM teams split each 32-rating batch (k-split) and are reduced in a
+// fixed order.  Per rating a thread loads 2 x 8 floats (4 LDS.128) and issues
+// 32 FFMA2 + 4 FFMA2 (rhs): 4 FMA per loaded float.  Partner rows are
+// gathered by cp.async, double buffered.  Hot rows: chunks publish their
+// partial tiles, the last chunk to finish sums them in chunk order.  The
+// solve is a CTA-cooperative right-looking Cholesky on the staged matrix.
 
-constexpr int CTA_THREADS = 256;
-constexpr int CTA_MAXNB = 32;
+constexpr int CTA_THREADS = 128;
 
-template <int NB, bool HAS_W>
+template <int NB8>
+struct WideCfg {
+    static constexpr int LDK = 8 * NB8;
+    static constexpr int T8 = NB8 * (NB8 + 1) / 2;
+    static constexpr int TEAM = T8 <= 32 ? 32 : T8 <= 64 ? 64 : 128;
+    static constexpr int TEAMS = CTA_THREADS / TEAM;
+    static constexpr int TPT = (T8 + TEAM - 1) / TEAM;
+    static constexpr int ROWS = LDK + 4;                // smem row stride (floats)
+    static constexpr int STAGE = BATCH * ROWS + 2 * BATCH;
+    static constexpr int MS = LDK + 1;                  // solve matrix stride
+    static constexpr int SMEM_FLOATS =
+        (2 * STAGE > LDK * MS ? 2 * STAGE : LDK * MS);
+    static constexpr int PSTRIDE = T8 * 72;             // 64 tile + 8 rhs floats per tile
+};
+
+__device__ __forceinline__ void tile_of(int t, int &I, int &J) {
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    I = i;
+    J = t - i * (i + 1) / 2;
+}
+
+template <int NB8, bool HAS_W>
 __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
-    constexpr int T = NB * (NB + 1) / 2;
-    constexpr int TPT = (T + CTA_THREADS - 1) / CTA_THREADS;  // tiles per thread
-    constexpr int LD = 4 * NB;
-    constexpr int PSTRIDE = T * 20;
+    using C = WideCfg<NB8>;
     extern __shared__ float4 smem4[];
-    float *xs = reinterpret_cast<float *>(smem4);   // [BATCH][LD]
-    float *ys = xs + BATCH * LD;                     // [BATCH] y, [BATCH] w
-    float *M = ys + 2 * BATCH;                       // [LD][LD + 1]
+    float *sm = reinterpret_cast<float *>(smem4);
+    float *M = sm;   // aliases the stages once the Gram is done
     __shared__ int s_flag;
     const int tid = threadIdx.x;
+    const int team = tid / C::TEAM, tt = tid % C::TEAM;
     const int64_t item = blockIdx.x;
     if (item >= p.total_items) return;
     const ItemInfo it = item_info(p, item);
     const int D = p.D;
+    const int nb4_real = (D + 3) / 4;   // 16 B blocks present in `fixed`
 
-    int bi[TPT], bj[TPT];
+    int tI[C::TPT], tJ[C::TPT];
+    bool tok[C::TPT];
 #pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-        int t = tid + q * CTA_THREADS, i = 0;
-        if (t >= T) t = -1;
-        bi[q] = bj[q] = 0;
-        if (t >= 0) {
-            while ((i + 1) * (i + 2) / 2 <= t) ++i;
-            bi[q] = i;
-            bj[q] = t - i * (i + 1) / 2;
-        }
+    for (int q = 0; q < C::TPT; ++q) {
+        const int t = tt + q * C::TEAM;
+        tok[q] = t < C::T8;
+        tile_of(tok[q] ? t : 0, tI[q], tJ[q]);
     }
-    float acc[TPT][4][4], rhs[TPT][4];
+    float2 acc[C::TPT][8][4];
+    float2 rhs[C::TPT][4];
 #pragma unroll
-    for (int q = 0; q < TPT; ++q)
+    for (int q = 0; q < C::TPT; ++q) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            rhs[q][m] = 0.f;
+        for (int m = 0; m < 8; ++m)
 #pragma unroll
-            for (int n = 0; n < 4; ++n) acc[q][m][n] = 0.f;
-        }
-    for (int64_t k = it.k0; k < it.k1; k += BATCH) {
-        __syncthreads();
-        for (int e = tid; e < BATCH * NB; e += CTA_THREADS) {
-            const int rr = e / NB, part = e - rr * NB;
+            for (int k = 0; k < 4; ++k) acc[q][m][k] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rhs[q][k] = make_float2(0.f, 0.f);
+    }
+
+    auto issue = [&](int64_t k, float *stage) {
+        float *xs = stage;
+        float *ys = stage + BATCH * C::ROWS;
+        for (int e = tid; e < BATCH * (C::LDK / 4); e += CTA_THREADS) {
+            const int rr = e / (C::LDK / 4), part = e - rr * (C::LDK / 4);
             const int64_t kk = k + rr;
-            const bool ok = kk < it.k1;
+            const bool ok = kk < it.k1 && part < nb4_real;
             const float *g = ok ? p.fixed + (size_t)p.idx[kk] * p.ld + part * 4 : p.fixed;
-            cp_async16(xs + rr * LD + part * 4, g, ok ? 16 : 0);
+            cp_async16(xs + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
         }
-        cp_async_commit();
         if (tid < BATCH) {
             const int64_t kk = k + tid;
             const bool ok = kk < it.k1;
             ys[tid] = ok ? p.val[kk] - p.y_shift : 0.f;
             ys[BATCH + tid] = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
         }
-        cp_async_wait<0>();
+        cp_async_commit();
+    };
+    const int64_t nbatch = (it.k1 - it.k0 + BATCH - 1) / BATCH;
+    if (nbatch > 0) issue(it.k0, sm);
+    for (int64_t bt = 0; bt < nbatch; ++bt) {
+        float *cur = sm + (bt & 1) * C::STAGE;
+        if (bt + 1 < nbatch) {
+            issue(it.k0 + (bt + 1) * BATCH, sm + ((bt + 1) & 1) * C::STAGE);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
+        const float *xs = cur;
+        const float *ys = cur + BATCH * C::ROWS;
+        for (int kb = team; kb < BATCH; kb += C::TEAMS) {
+            const float *xr = xs + kb * C::ROWS;
+            const float y = ys[kb];
+            const float w = HAS_W ? ys[BATCH + kb] : 1.f;
 #pragma unroll
-        for (int q = 0; q < TPT; ++q) {
-            if (tid + q * CTA_THREADS >= T) continue;
-            for (int kb = 0; kb < BATCH; ++kb) {
-                float4 a = *reinterpret_cast<const float4 *>(xs + kb * LD + 4 * bi[q]);
-                const float4 b = *reinterpret_cast<const float4 *>(xs + kb * LD + 4 * bj[q]);
-                const float y = ys[kb];
+            for (int q = 0; q < C::TPT; ++q) {
+                if (!tok[q]) continue;
+                const float4 a0 = *reinterpret_cast<const float4 *>(xr + 8 * tI[q]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(xr + 8 * tI[q] + 4);
+                const float4 b0 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[q]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[q] + 4);
+                float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 if (HAS_W) {
-                    const float w = ys[BATCH + kb];
-                    a.x *= w; a.y *= w; a.z *= w; a.w *= w;
-                }
-                const float av[4] = {a.x, a.y, a.z, a.w};
-                const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-#pragma unroll
-                    for (int n = 0; n < 4; ++n) acc[q][m][n] = fmaf(av[m], bv[n], acc[q][m][n]);
-                    rhs[q][m] = fmaf(y, av[m], rhs[q][m]);
+                    for (int m = 0; m < 8; ++m) a[m] *= w;
                 }
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    ffma2(acc[q][m][0], a[m], b0.x, b0.y);
+                    ffma2(acc[q][m][1], a[m], b0.z, b0.w);
+                    ffma2(acc[q][m][2], a[m], b1.x, b1.y);
+                    ffma2(acc[q][m][3], a[m], b1.z, b1.w);
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) ffma2(rhs[q][m], y, a[2 * m], a[2 * m + 1]);
             }
         }
+        __syncthreads();   // this stage is refilled two iterations later
     }
+
+    // multi-chunk rows: publish this chunk's partial tiles, last finisher sums
     if (it.nch > 1) {
-        float *slot0 = p.partials + (size_t)p.slot_off[it.j] * PSTRIDE;
+        float *slot0 = p.partials + (size_t)p.slot_off[it.j] * C::PSTRIDE;
+        // team-reduce into the partial: teams write in turn (fixed order)
+        for (int tm = 0; tm < C::TEAMS; ++tm) {
+            if (team == tm) {
 #pragma unroll
-        for (int q = 0; q < TPT; ++q) {
-            const int t = tid + q * CTA_THREADS;
-            if (t >= T) continue;
-            float *dst = slot0 + (size_t)it.c * PSTRIDE + t * 20;
+                for (int q = 0; q < C::TPT; ++q) {
+                    const int t = tt + q * C::TEAM;
+                    if (!tok[q]) continue;
+                    float *dst = slot0 + (size_t)it.c * C::PSTRIDE + t * 72;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
+                    for (int m = 0; m < 8; ++m)
 #pragma unroll
-                for (int n = 0; n < 4; ++n) dst[m * 4 + n] = acc[q][m][n];
-                dst[16 + m] = rhs[q][m];
+                        for (int k = 0; k < 4; ++k) {
+                            float2 v = acc[q][m][k];
+                            if (tm > 0) {
+                                v.x += dst[m * 8 + 2 * k];
+                                v.y += dst[m * 8 + 2 * k + 1];
+                            }
+                            dst[m * 8 + 2 * k] = v.x;
+                            dst[m * 8 + 2 * k + 1] = v.y;
+                        }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        float2 v = rhs[q][k];
+                        if (tm > 0) {
+                            v.x += dst[64 + 2 * k];
+                            v.y += dst[64 + 2 * k + 1];
+                        }
+                        dst[64 + 2 * k] = v.x;
+                        dst[64 + 2 * k + 1] = v.y;
+                    }
+                }
             }
+            __syncthreads();
         }
         __threadfence();
         __syncthreads();
@@ -485,27 +569,35 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
         if (s_flag != it.nch - 1) return;
         __threadfence();
         if (tid == 0) p.counters[it.j] = 0;
+        // last finisher: team 0 sums all chunks' tiles in chunk order
 #pragma unroll
-        for (int q = 0; q < TPT; ++q) {
-            const int t = tid + q * CTA_THREADS;
+        for (int q = 0; q < C::TPT; ++q) {
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                rhs[q][m] = 0.f;
+            for (int m = 0; m < 8; ++m)
 #pragma unroll
-                for (int n = 0; n < 4; ++n) acc[q][m][n] = 0.f;
-            }
-            if (t >= T) continue;
+                for (int k = 0; k < 4; ++k) acc[q][m][k] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rhs[q][k] = make_float2(0.f, 0.f);
+            const int t = tt + q * C::TEAM;
+            if (team != 0 || !tok[q]) continue;
             for (int c = 0; c < it.nch; ++c) {
-                const float *src = slot0 + (size_t)c * PSTRIDE + t * 20;
+                const float *src = slot0 + (size_t)c * C::PSTRIDE + t * 72;
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
+                for (int m = 0; m < 8; ++m)
 #pragma unroll
-                    for (int n = 0; n < 4; ++n) acc[q][m][n] += __ldcg(src + m * 4 + n);
-                    rhs[q][m] += __ldcg(src + 16 + m);
+                    for (int k = 0; k < 4; ++k) {
+                        acc[q][m][k].x += __ldcg(src + m * 8 + 2 * k);
+                        acc[q][m][k].y += __ldcg(src + m * 8 + 2 * k + 1);
+                    }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    rhs[q][k].x += __ldcg(src + 64 + 2 * k);
+                    rhs[q][k].y += __ldcg(src + 64 + 2 * k + 1);
                 }
             }
         }
     }
+
     const int r = it.r;
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     if (it.n == 0 && S == 0.f) {
@@ -517,29 +609,49 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
         return;
     }
     const float diag = p.lam_c + p.lam_n * (float)it.n + p.tau * S;
-    constexpr int MS = LD + 1;
+    constexpr int MS = C::MS;
+    // stage A (lower) + b into M; teams fold in turn (fixed order)
     __syncthreads();
+    const bool single = it.nch > 1;   // after the chunk sum only team 0 holds data
+    for (int tm = 0; tm < (single ? 1 : C::TEAMS); ++tm) {
+        if (team == tm) {
 #pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-        if (tid + q * CTA_THREADS >= T) continue;
+            for (int q = 0; q < C::TPT; ++q) {
+                if (!tok[q]) continue;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const int row = 4 * bi[q] + m;
+                for (int m = 0; m < 8; ++m) {
+                    const int row = 8 * tI[q] + m;
 #pragma unroll
-            for (int n = 0; n < 4; ++n) {
-                const int col = 4 * bj[q] + n;
-                float v = acc[q][m][n];
-                if (row == col) v += diag;
-                if (col <= row) M[row * MS + col] = v;
-            }
-            if (bi[q] == bj[q]) {
-                float bv = rhs[q][m];
-                if (p.tax_T && row < D) bv = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + row], bv);
-                M[row * MS + LD] = bv;
+                    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int col = 8 * tJ[q] + 2 * k + hh;
+                            if (col <= row) {
+                                const float v = hh ? acc[q][m][k].y : acc[q][m][k].x;
+                                M[row * MS + col] = tm == 0 ? v : M[row * MS + col] + v;
+                            }
+                        }
+                    }
+                }
+                if (tI[q] == tJ[q]) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int row = 8 * tI[q] + 2 * k + hh;
+                            const float v = hh ? rhs[q][k].y : rhs[q][k].x;
+                            M[row * MS + C::LDK] = tm == 0 ? v : M[row * MS + C::LDK] + v;
+                        }
+                    }
+                }
             }
         }
+        __syncthreads();
     }
-    if (tid == 0) s_flag = 0;
+    for (int i = tid; i < D; i += CTA_THREADS) {
+        M[i * MS + i] += diag;
+        if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
+    }
     __syncthreads();
     // right-looking Cholesky, one column per step
     for (int j = 0; j < D; ++j) {
@@ -554,33 +666,36 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
         for (int i = j + 1 + tid; i < D; i += CTA_THREADS) M[i * MS + j] *= inv;
         __syncthreads();
         const int w = D - j - 1;
-        for (int e = tid; e < w * w; e += CTA_THREADS) {
-            const int i = j + 1 + e / w, k2 = j + 1 + e % w;
-            if (k2 <= i) M[i * MS + k2] = fmaf(-M[i * MS + j], M[k2 * MS + j], M[i * MS + k2]);
+        for (int e = tid; e < w * (w + 1) / 2; e += CTA_THREADS) {
+            int i2 = (int)((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);
+            while ((i2 + 1) * (i2 + 2) / 2 <= e) ++i2;
+            while (i2 * (i2 + 1) / 2 > e) --i2;
+            const int k2 = e - i2 * (i2 + 1) / 2;
+            const int i = j + 1 + i2, kk = j + 1 + k2;
+            M[i * MS + kk] = fmaf(-M[i * MS + j], M[kk * MS + j], M[i * MS + kk]);
         }
         __syncthreads();
     }
-    // triangular solves by one warp (D <= 128: 4 rows per lane)
+    // triangular solves by one warp
     if (tid < 32) {
         for (int j = 0; j < D; ++j) {
-            if (tid == 0) M[j * MS + LD] /= M[j * MS + j];
+            if (tid == 0) M[j * MS + C::LDK] /= M[j * MS + j];
             __syncwarp();
-            const float yj = M[j * MS + LD];
-            for (int i = j + 1 + tid; i < D; i += 32) M[i * MS + LD] -= M[i * MS + j] * yj;
+            const float yj = M[j * MS + C::LDK];
+            for (int i = j + 1 + tid; i < D; i += 32) M[i * MS + C::LDK] -= M[i * MS + j] * yj;
             __syncwarp();
         }
         for (int j = D - 1; j >= 0; --j) {
-            if (tid == 0) M[j * MS + LD] /= M[j * MS + j];
+            if (tid == 0) M[j * MS + C::LDK] /= M[j * MS + j];
             __syncwarp();
-            const float xj = M[j * MS + LD];
-            for (int i = tid; i < j; i += 32) M[i * MS + LD] -= M[j * MS + i] * xj;
+            const float xj = M[j * MS + C::LDK];
+            for (int i = tid; i < j; i += 32) M[i * MS + C::LDK] -= M[j * MS + i] * xj;
             __syncwarp();
         }
         for (int i = tid; i < p.ld; i += 32)
-            p.out[(size_t)r * p.ld + i] = i < D ? M[i * MS + LD] : 0.f;
+            p.out[(size_t)r * p.ld + i] = i < D ? M[i * MS + C::LDK] : 0.f;
     }
 }
-
 
 // ---------------------------------------------------------------------------
 // pair path, D <= 20 (the hot kernel of configs 0-2)
@@ -754,17 +869,6 @@ __device__ __forceinline__ bool mbar_try(unsigned bar, unsigned parity) {
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     while (!mbar_try(bar, parity)) {
     }
-}
-
-// Paired FP32 FMA (sm_100 FFMA2): acc.{x,y} += a * b.{x,y}; the scalar a is
-// a broadcast operand of the instruction (no register moves).
-__device__ __forceinline__ void ffma2(float2 &acc, float a, float bx, float by) {
-    unsigned long long A, B, C;
-    asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(bx), "f"(by));
-    asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(acc.x), "f"(acc.y));
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(C));
 }
 
 // Per-lane accumulators of the pair path, FFMA2-shaped: for each of HALF
@@ -1172,18 +1276,23 @@ int launch_warp(const AlsParams &p, cudaStream_t s) {
     return check_launch("mcf_als_half_step(warp)");
 }
 
-template <int NB, bool W>
+template <int NB8, bool W>
 int launch_cta(const AlsParams &p, cudaStream_t s) {
-    constexpr int LD = 4 * NB;
-    const size_t smem = sizeof(float) * (BATCH * LD + 2 * BATCH + LD * (LD + 1));
+    using C = WideCfg<NB8>;
+    const size_t smem = sizeof(float) * C::SMEM_FLOATS;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_cta<NB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_cta<NB8, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
-    if (p.total_items > 0) k_als_cta<NB, W><<<(unsigned)p.total_items, CTA_THREADS, smem, s>>>(p);
-    return check_launch("mcf_als_half_step(cta)");
+    if (p.total_items > 0) k_als_cta<NB8, W><<<(unsigned)p.total_items, CTA_THREADS, smem, s>>>(p);
+    return check_launch("mcf_als_half_step(wide)");
+}
+
+int nb8_for(int D) {
+    const int nb = (D + 7) / 8;
+    return nb <= 4 ? 4 : nb <= 6 ? 6 : nb <= 7 ? 7 : nb <= 8 ? 8 : nb <= 10 ? 10 : nb <= 13 ? 13 : 16;
 }
 
 template <bool W>
@@ -1199,17 +1308,22 @@ int dispatch(const AlsParams &p, cudaStream_t s) {
         case 7: return launch_warp<7, W>(p, s);
         default: break;
     }
-    if (nb <= 9) return launch_cta<9, W>(p, s);
-    if (nb <= 13) return launch_cta<13, W>(p, s);
-    if (nb <= 16) return launch_cta<16, W>(p, s);
-    if (nb <= 25) return launch_cta<25, W>(p, s);
-    return launch_cta<32, W>(p, s);
+    switch (nb8_for(p.D)) {
+        case 4: return launch_cta<4, W>(p, s);
+        case 6: return launch_cta<6, W>(p, s);
+        case 7: return launch_cta<7, W>(p, s);
+        case 8: return launch_cta<8, W>(p, s);
+        case 10: return launch_cta<10, W>(p, s);
+        case 13: return launch_cta<13, W>(p, s);
+        default: return launch_cta<16, W>(p, s);
+    }
 }
 
 size_t pstride_of(int D) {
     const int nb = (D + 3) / 4;
-    const int T = nb * (nb + 1) / 2;
-    return (size_t)T * 20;
+    if (nb <= 7) return (size_t)(nb * (nb + 1) / 2) * 20;   // warp path, 4x4 tiles
+    const int n8 = nb8_for(D);
+    return (size_t)(n8 * (n8 + 1) / 2) * 72;                // wide path, 8x8 tiles
 }
 
 struct PlanLayout {
