@@ -114,6 +114,16 @@ def algorithmic(nnz, U, I, D):
             "bytes_launch_mean": (b_items + b_users) / 2, "flops_launch_mean": (f_items + f_users) / 2}
 
 
+def launches_per_sweep(eng) -> int:
+    """libmcf kernels per sweep: per half-step the row kernel, plus the hot-row
+    reduce kernel when the layout has hot rows (D <= 20 path)."""
+    n = 0
+    for lay in (eng.r.by_item, eng.r.by_user):
+        info = lay.plan()[1]
+        n += 1 + (1 if eng.D <= 20 and info[4] > 0 else 0)
+    return n
+
+
 def peaks():
     try:
         with open(PEAKS) as fh:
@@ -363,7 +373,7 @@ def run_ours(args, rank, world):
                                  "no flush",
                            "parallelism": f"rows sharded over {world} GPU(s)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": 2 * args.steps, "clocks": clk.summary(),
+                "gpu_launches": launches_per_sweep(eng) * args.steps, "clocks": clk.summary(),
                 "valid_rmse_after": rm, "layout_build_s": t_layout, "datagen_s": t_gen,
                 "sweep_ms_items_users": [roofline["launch_ms"]["items"],
                                          roofline["launch_ms"]["users"]]}

@@ -653,7 +653,9 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
         if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
     }
     __syncthreads();
-    // right-looking Cholesky, one column per step
+    // right-looking Cholesky, one column per step; thread i owns row i
+    // (D <= 128), so the trailing update needs no index arithmetic and
+    // column j is read unscaled (times 1/L_jj) before it is overwritten
     for (int j = 0; j < D; ++j) {
         const float piv = M[j * MS + j];
         if (!(piv > 0.f) || !isfinite(piv)) {
@@ -661,19 +663,16 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
             return;  // uniform: every thread read the same pivot
         }
         const float l = sqrtf(piv), inv = 1.f / l;
-        __syncthreads();
-        if (tid == 0) M[j * MS + j] = l;
-        for (int i = j + 1 + tid; i < D; i += CTA_THREADS) M[i * MS + j] *= inv;
-        __syncthreads();
-        const int w = D - j - 1;
-        for (int e = tid; e < w * (w + 1) / 2; e += CTA_THREADS) {
-            int i2 = (int)((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);
-            while ((i2 + 1) * (i2 + 2) / 2 <= e) ++i2;
-            while (i2 * (i2 + 1) / 2 > e) --i2;
-            const int k2 = e - i2 * (i2 + 1) / 2;
-            const int i = j + 1 + i2, kk = j + 1 + k2;
-            M[i * MS + kk] = fmaf(-M[i * MS + j], M[kk * MS + j], M[i * MS + kk]);
+        const int i = tid;
+        float lij = 0.f;
+        if (i > j && i < D) {
+            lij = M[i * MS + j] * inv;
+            for (int k = j + 1; k <= i; ++k)
+                M[i * MS + k] = fmaf(-lij, M[k * MS + j] * inv, M[i * MS + k]);
         }
+        __syncthreads();
+        if (i > j && i < D) M[i * MS + j] = lij;
+        if (i == j) M[j * MS + j] = l;
         __syncthreads();
     }
     // triangular solves by one warp
