@@ -94,13 +94,19 @@ size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
  * lam_n > 0.  A row whose pivot is <= 0 or non-finite is left untouched and
  * *fail_row (device int64) receives the minimum such row (-1 = none); all
  * other rows still complete (the reference's failing block stops early,
- * _kernels.py:197-203). */
+ * _kernels.py:197-203).
+ * obj_out (nullable, device double[2], D <= 20): the fused objective of the
+ * solved rows, obj_out[0] = sum_r sum_k w_k (y_k - x_k^T out_r)^2 and
+ * obj_out[1] = sum_r (lam_c + lam_n n_r) |out_r|^2, evaluated in the solve
+ * epilogue from the Gram (sum w y^2 - b^T x - lam |x|^2) and summed in a fixed
+ * order; exact for tau = 0 (the taxonomy term is not included). */
 int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
                       const float *wts, const float *fixed, int64_t n_fixed, float *out, int32_t D,
                       float lam_c, float lam_n, float y_shift, const float *tax_S,
                       const float *tax_T, float tau, const int32_t *row_list, int32_t n_list,
                       int32_t row_lo, int32_t chunk, const void *plan, const int64_t *plan_info,
-                      int64_t *fail_row, void *ws, size_t ws_bytes, void *stream);
+                      int64_t *fail_row, double *obj_out, void *ws, size_t ws_bytes,
+                      void *stream);
 
 /* ---- MFITR taxonomy term (segmented reduction) ---------------------------
  * For each listed item i (row_list NULL -> all n_items):

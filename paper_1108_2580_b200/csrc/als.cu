@@ -65,6 +65,8 @@ struct AlsParams {
     float *partials;           // [slots][pstride]
     int32_t *counters;         // [n_list]
     unsigned long long *fail;  // min failing row (as unsigned; ~0 = none)
+    double *obj_partial;       // [(groups + hot rows) * 2] or null (fused objective)
+    int64_t obj_groups;        // pair-path groups (hot rows follow them)
 };
 
 // ---------------------------------------------------------------------------
@@ -735,6 +737,7 @@ struct PairCfg {
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
     static constexpr int RHS0 = LDK * (LDK + 1) / 2;
     static constexpr int GRAM = RHS0 + LDK;        // packed lower + rhs
+    static constexpr int PSTR = GRAM + 1;          // partial slot: + sum w y^2
     static constexpr int GSTRIDE = GRAM | 1;       // odd stride: conflict-free per-lane rows
     static constexpr int RING_BYTES = NS * STAGE_BYTES;
     static constexpr int SOLVE_BYTES = PAIRS * GSTRIDE * 4;
@@ -816,13 +819,21 @@ struct PairPlan {
     const int32_t *hoff;       // [n_list + 1] first chunk slot of list entry j
     int64_t n_heavy;
     int32_t *group_counter;
+    double *obj_out;           // [2] = (sum sse, sum reg) or null
 };
 
 // regularise + solve one packed system (one thread) and write the row.
+// Regularise + solve one packed system (one thread), write the row, and
+// return the row's objective terms: with x = (A_d + lam I)^{-1} b,
+//   sum_k w_k (y_k - x_k^T x)^2 = sum w y^2 - b^T x - lam |x|^2   (sse)
+//   (lam_c + lam_n n) |x|^2                                        (reg)
+// (yy = sum w y^2 accumulated with the Gram; exact for tau = 0).
 template <int LDK>
-__device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n) {
+__device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float yy,
+                           double &sse, double &reg) {
     constexpr int RHS0 = LDK * (LDK + 1) / 2;
     const int D = p.D;
+    sse = reg = 0.0;
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     float *orow = p.out + (size_t)r * p.ld;
     if (n == 0 && S == 0.f) {
@@ -833,15 +844,59 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n) {
         }
         return;
     }
-    const float diag = p.lam_c + p.lam_n * (float)n + p.tau * S;
+    const float lam_row = p.lam_c + p.lam_n * (float)n;
+    const float diag = lam_row + p.tau * S;
     if (p.tax_T)
         for (int i = 0; i < D; ++i)
             g[RHS0 + i] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], g[RHS0 + i]);
+    float b[LDK];
+#pragma unroll
+    for (int i = 0; i < LDK; ++i) b[i] = i < D ? g[RHS0 + i] : 0.f;
     if (!thread_solve<LDK>(g, D, diag)) {
         report_fail(p.fail, r);
         return;
     }
+    float bx = 0.f, xx = 0.f;
+#pragma unroll
+    for (int i = 0; i < LDK; ++i) {
+        if (i < D) {
+            const float x = g[RHS0 + i];
+            bx = fmaf(b[i], x, bx);
+            xx = fmaf(x, x, xx);
+        }
+    }
+    sse = (double)yy - (double)bx - (double)diag * (double)xx;
+    reg = (double)lam_row * (double)xx;
     for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? g[RHS0 + i] : 0.f;
+}
+
+__global__ void k_obj_sum(const double *part, int64_t n, double *out) {
+    __shared__ double sh[2][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double a = 0.0, b = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        a += part[2 * i];
+        b += part[2 * i + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(FULL, a, o);
+        b += __shfl_down_sync(FULL, b, o);
+    }
+    if (lane == 0) {
+        sh[0][warp] = a;
+        sh[1][warp] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            s0 += sh[0][w];
+            s1 += sh[1][w];
+        }
+        out[0] = s0;
+        out[1] = s1;
+    }
 }
 
 __device__ __forceinline__ void prefetch_l2(const void *a) {
@@ -882,7 +937,9 @@ struct PairAcc {
     float2 dpr[HALF][4];
     float2 off[NOFF > 0 ? NOFF : 1][4][2];
     float2 rhs[HALF][2];
+    float yy;   // sum w y^2 (fused objective)
     __device__ __forceinline__ void zero() {
+        yy = 0.f;
 #pragma unroll
         for (int i = 0; i < HALF; ++i) {
             dsc[i][0] = dsc[i][1] = 0.f;
@@ -896,7 +953,9 @@ struct PairAcc {
             for (int m = 0; m < 4; ++m) off[i][m][0] = off[i][m][1] = make_float2(0.f, 0.f);
     }
     // one rating: register blocks xr (unscaled) / xa (weight-scaled), target y
-    __device__ __forceinline__ void add(const float4 (&xa)[NBK], const float4 (&xr)[NBK], float y) {
+    __device__ __forceinline__ void add(const float4 (&xa)[NBK], const float4 (&xr)[NBK], float y,
+                                        float wy) {
+        yy = fmaf(wy, y, yy);
 #pragma unroll
         for (int i = 0; i < HALF; ++i) {
             const int b = 2 * i;
@@ -1089,14 +1148,16 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
                 float4 xa[NBK];
 #pragma unroll
                 for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
+                float wy = y;
                 if (HAS_W) {
                     const float w = rw[C::LDK + 1];
+                    wy = w * y;
 #pragma unroll
                     for (int b = 0; b < NBK; ++b) {
                         xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
                     }
                 }
-                acc.add(xa, xr, y);
+                acc.add(xa, xr, y, wy);
             }
             __syncwarp();   // all lanes done with this stage before it is refilled
         };
@@ -1117,12 +1178,25 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
         // scatter the lane's accumulators into the pair's packed [A | b]
         acc.scatter(my_g, h, C::RHS0);
         __syncwarp();
+        double o_sse = 0.0, o_reg = 0.0;
         if (task < q.n_tasks) {
             if (slot >= 0) {
-                float *dst = p.partials + (size_t)slot * C::GRAM;
+                float *dst = p.partials + (size_t)slot * C::PSTR;
                 for (int i = h; i < C::GRAM; i += 2) dst[i] = my_g[i];
+                if (h == 0) dst[C::GRAM] = acc.yy;
             } else if (h == 0) {
-                finish_row<C::LDK>(p, my_g, row, n);
+                finish_row<C::LDK>(p, my_g, row, n, acc.yy, o_sse, o_reg);
+            }
+        }
+        if (p.obj_partial) {   // fixed-order butterfly: deterministic per group
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                o_sse += __shfl_xor_sync(FULL, o_sse, o);
+                o_reg += __shfl_xor_sync(FULL, o_reg, o);
+            }
+            if (lane == 0) {
+                p.obj_partial[2 * grp] = o_sse;
+                p.obj_partial[2 * grp + 1] = o_reg;
             }
         }
         __syncwarp();
@@ -1136,7 +1210,7 @@ template <int NBK>
 __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK>;
     constexpr int LDK = C::LDK;
-    __shared__ float g[4][C::GSTRIDE];
+    __shared__ float g[4][C::GSTRIDE + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t hr = (int64_t)blockIdx.x * 4 + warp;
     if (hr >= q.n_heavy) return;
@@ -1144,9 +1218,9 @@ __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
     const int r = p.row_list ? p.row_list[j] : p.row_lo + j;
     const int s0 = q.hoff[j], s1 = q.hoff[j + 1];
     float *G = g[warp];
-    for (int i = lane; i < C::GRAM; i += 32) {
+    for (int i = lane; i <= C::GRAM; i += 32) {   // incl. sum w y^2 at GRAM
         float a = 0.f;
-        for (int s = s0; s < s1; ++s) a += __ldcg(p.partials + (size_t)s * C::GRAM + i);
+        for (int s = s0; s < s1; ++s) a += __ldcg(p.partials + (size_t)s * C::PSTR + i);
         G[i] = a;
     }
     __syncwarp();
@@ -1154,12 +1228,14 @@ __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
     const int64_t n = p.ptr[r + 1] - p.ptr[r];
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     float *orow = p.out + (size_t)r * p.ld;
-    const float diag = p.lam_c + p.lam_n * (float)n + p.tau * S;
+    const float lam_row = p.lam_c + p.lam_n * (float)n;
+    const float diag = lam_row + p.tau * S;
     float a[LDK];
 #pragma unroll
     for (int c = 0; c < LDK; ++c) a[c] = (lane < D && c <= lane) ? G[pidx(lane, c)] : 0.f;
     float b = lane < D ? G[C::RHS0 + lane] : 0.f;
     if (p.tax_T && lane < D) b = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + lane], b);
+    const float b0 = b, yy = G[C::GRAM];
 #pragma unroll
     for (int c = 0; c < LDK; ++c)
         if (c == lane) a[c] += diag;
@@ -1206,6 +1282,18 @@ __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
         if (lane < j2) b = fmaf(-G[pidx(j2, lane)], xj, b);
     }
     if (lane < p.ld) orow[lane] = lane < D ? b : 0.f;
+    if (p.obj_partial) {
+        float bx = lane < D ? b0 * b : 0.f, xx = lane < D ? b * b : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            bx += __shfl_xor_sync(FULL, bx, o);
+            xx += __shfl_xor_sync(FULL, xx, o);
+        }
+        if (lane == 0) {
+            p.obj_partial[2 * (p.obj_groups + hr)] = (double)yy - (double)bx - (double)diag * xx;
+            p.obj_partial[2 * (p.obj_groups + hr) + 1] = (double)lam_row * xx;
+        }
+    }
 }
 
 // --- plan kernels for the pair path
@@ -1393,6 +1481,7 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     if (grid > 0) k_als_pair<NBK, W, FB><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
         k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
+    if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
     return check_launch("mcf_als_half_step(pair)");
 }
 
@@ -1405,11 +1494,11 @@ int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     return launch_pair<5, W, false>(p, q, s);
 }
 
-size_t pair_gram(int D) {
+size_t pair_gram(int D) {   // partial slot floats: packed [A | b] + sum w y^2
     const int nb = (D + 3) / 4;
     const int nbk = nb <= 1 ? 1 : nb <= 3 ? 3 : 5;
     const int ldk = 4 * nbk;
-    return (size_t)(ldk * (ldk + 1) / 2 + ldk);
+    return (size_t)(ldk * (ldk + 1) / 2 + ldk + 1);
 }
 
 }  // namespace
@@ -1494,7 +1583,9 @@ extern "C" int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t
 extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D) {
     if (D < 1 || n_list < 0 || slots < 0) return 0;
     const size_t per = use_pair(D) ? pair_gram(D) : pstride_of(D);
-    return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + sizeof(float) * (size_t)slots * per;
+    const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
+    return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) +
+           sizeof(float) * (size_t)slots * per;
 }
 
 extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
@@ -1503,8 +1594,8 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
                                  float lam_c, float lam_n, float y_shift, const float *tax_S,
                                  const float *tax_T, float tau, const int32_t *row_list,
                                  int32_t n_list, int32_t row_lo, int32_t chunk, const void *plan,
-                                 const int64_t *plan_info, int64_t *fail_row, void *ws,
-                                 size_t ws_bytes, void *stream) {
+                                 const int64_t *plan_info, int64_t *fail_row, double *obj_out,
+                                 void *ws, size_t ws_bytes, void *stream) {
     if (D < 1 || D > 128) {
         set_error("mcf_als_half_step: D must be in [1, 128]");
         return MCF_E_UNSUPPORTED;
@@ -1536,8 +1627,14 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
     p.total_items = total_items;
     p.fail = reinterpret_cast<unsigned long long *>(fail_row);
     // workspace: counters [n_list] + partial slots
+    if (obj_out && !use_pair(D)) {
+        set_error("mcf_als_half_step: obj_out (fused objective) is implemented for D <= 20");
+        return MCF_E_UNSUPPORTED;
+    }
     Carve c(ws, ws_bytes);
     p.counters = c.take<int32_t>((size_t)n_list + 64);
+    double *objp = c.take<double>(2 * ((size_t)n_list + (size_t)std::max<int64_t>(plan_info[3], plan_info[1]) + 64));
+    p.obj_partial = obj_out ? objp : nullptr;
     p.partials = c.take<float>(0);
     const size_t fixed_part = c.used;
     if (!ws || ws_bytes < fixed_part) {
@@ -1559,7 +1656,12 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
         q.hoff = L.hch;
         q.n_heavy = plan_info[4];
         q.group_counter = p.counters + n_list;
-        if (q.n_tasks == 0) return MCF_OK;
+        q.obj_out = obj_out;
+        p.obj_groups = ceil_div(q.n_tasks, 16);
+        if (q.n_tasks == 0) {
+            if (obj_out) return cuda_status(cudaMemsetAsync(obj_out, 0, 2 * sizeof(double), s), "memset");
+            return MCF_OK;
+        }
         return wts ? dispatch_pair<true>(p, q, s) : dispatch_pair<false>(p, q, s);
     }
     if (total_items == 0) return MCF_OK;

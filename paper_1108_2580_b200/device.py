@@ -126,7 +126,7 @@ class LayoutSolver:
 
     def solve(self, lay: SideLayout, fixed: torch.Tensor, out: torch.Tensor, lam_c=0.0, lam_n=0.0,
               y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
-              fail: torch.Tensor | None = None):
+              fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None):
         dev = lay.device
         if fail is None:
             if self.fail is None:
@@ -143,8 +143,8 @@ class LayoutSolver:
             ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(wts), ptr(fixed), fixed.shape[0],
             ptr(out), self.D,
             float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
-            ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail), ptr(ws), ws.numel(),
-            stream_ptr(dev)), "mcf_als_half_step")
+            ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail), ptr(obj_out), ptr(ws),
+            ws.numel(), stream_ptr(dev)), "mcf_als_half_step")
         return fail
 
 
@@ -202,21 +202,34 @@ class AlsEngine:
     # -- half-step -----------------------------------------------------------
     def half_step(self, side: str, lam_c: float = 0.0, lam_n: float = 0.0, y_shift: float = 0.0,
                   tax_S=None, tax_T=None, tau: float = 0.0, rows: torch.Tensor | None = None,
-                  rows_key=None, fixed: torch.Tensor | None = None):
+                  rows_key=None, fixed: torch.Tensor | None = None, obj_out=None):
         lay = self.r.layout(side)
         out = self.P if side == "users" else self.Q
         if fixed is None:
             fixed = self.Q if side == "users" else self.P
         self._solver.solve(lay, fixed, out, lam_c, lam_n, y_shift, tax_S, tax_T, tau, rows,
-                           rows_key, self._wts.get(side), self.fail)
+                           rows_key, self._wts.get(side), self.fail, obj_out)
         acc = self._fail_acc[0:1] if side == "items" else self._fail_acc[1:2]
         torch.where(acc < 0, self.fail, acc, out=acc)
         return out
 
-    def sweep(self, lam_c: float = 0.0, lam_n: float = 0.0):
-        """One full iteration: items half-step, then users (factor.py:550-555)."""
-        self.half_step("items", lam_c, lam_n)
-        self.half_step("users", lam_c, lam_n)
+    @property
+    def fused_objective(self) -> bool:
+        """The solve epilogue can report the objective (D <= 20 path)."""
+        return self.D <= 20
+
+    def sweep(self, lam_c: float = 0.0, lam_n: float = 0.0, obj: torch.Tensor | None = None):
+        """One full iteration: items half-step, then users (factor.py:550-555).
+        With `obj` (device double[4], D <= 20) the half-steps also report
+        their objective terms: (items sse, items reg, users sse, users reg)."""
+        self.half_step("items", lam_c, lam_n, obj_out=None if obj is None else obj[0:2])
+        self.half_step("users", lam_c, lam_n, obj_out=None if obj is None else obj[2:4])
+
+    @staticmethod
+    def sweep_objective(obj: torch.Tensor) -> torch.Tensor:
+        """Objective after a sweep: the users half-step's data term with the
+        final factors, plus both sides' regularisers."""
+        return obj[2:3] + obj[3:4] + obj[1:2]
 
     def check(self):
         """Synchronise and raise SingularSystemError for a failed row

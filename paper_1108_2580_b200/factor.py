@@ -298,10 +298,16 @@ def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: Hyp
         vi = torch.as_tensor(validation.items.astype(np.int32), device=dev)
         vs = torch.as_tensor(validation.scores.astype(np.float32), device=dev)
     report: list[EpochStats] = []
+    fused = objective and eng.fused_objective
+    obj_buf = torch.zeros(4, dtype=torch.float64, device=dev) if fused else None
     for ep in range(hyper.iters):
-        eng.sweep(lam_c, lam_n)
+        eng.sweep(lam_c, lam_n, obj_buf)
         model.epochs_done += 1
-        obj = eng.objective(hyper.lam, reg) if objective else None
+        obj = None
+        if fused:
+            obj = eng.sweep_objective(obj_buf)      # computed in the solve epilogue
+        elif objective:
+            obj = eng.objective(hyper.lam, reg)
         rm = eng.rmse(vu, vi, vs, (train_data.scale.lo, train_data.scale.hi)) if vu is not None else None
         eng.check()
         report.append(EpochStats(ep, hyper.gamma,

@@ -42,7 +42,7 @@ def test_host_only_queries():
     assert L.mcf_als_workspace_bytes(10, 0, 20) >= 40
     # argument validation happens before any device work
     assert L.mcf_als_half_step(None, None, None, None, None, 0, None, 0, 0, 0, 0, None, None, 0,
-                               None, 0, 0, 32, None, None, None, None, 0, None) == -5
+                               None, 0, 0, 32, None, None, None, None, None, 0, None) == -5
     assert b"D must be" in L.mcf_last_error()
 
 

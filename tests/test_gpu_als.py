@@ -333,3 +333,29 @@ def test_rmse_known_answer():
                   torch.tensor([0, 1], dtype=torch.int32, device=d),
                   torch.tensor([0.0, 0.0], device=d))
     assert abs(float(rm.item()) - np.sqrt(50.0)) < 1e-6
+
+
+@pytest.mark.parametrize("reg,D", [("weighted", 20), ("plain", 10), ("weighted", 4)])
+def test_fused_objective_matches_explicit(golden, reg, D):
+    """The objective reported by the solve epilogue equals the explicit
+    pass (predict + norms) and the float64 oracle objective."""
+    g = golden("als_cfg0.npz")
+    u, i, s = g["train_users"], g["train_items"], g["train_scores"]
+    U, I = int(g["U"]), int(g["I"])
+    eng = _engine(u, i, s, U, I, D, chunk=128)      # small chunk: hot-row path too
+    rng = np.random.default_rng(0)
+    eng.set_factors(rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D)))
+    lam = 0.065
+    lc, ln = (lam, 0.0) if reg == "plain" else (0.0, lam)
+    obj = torch.zeros(4, dtype=torch.float64, device=dev())
+    eng.sweep(lc, ln, obj)
+    eng.check()
+    fused = float(eng.sweep_objective(obj).item())
+    explicit = float(eng.objective(lam, reg).item())
+    P, Q = (t.double().cpu().numpy() for t in eng.factors())
+    if reg == "plain":
+        ref = oracle.als_objective(P, Q, u.astype(np.int64), i.astype(np.int64), s, lam)
+    else:
+        ref = oracle.weighted_objective(P, Q, u.astype(np.int64), i.astype(np.int64), s, lam)
+    assert abs(explicit - ref) < 1e-5 * ref
+    assert abs(fused - ref) < 1e-4 * ref, (fused, explicit, ref)
