@@ -308,6 +308,7 @@ def run_ours(args, rank, world):
 
     # held-out RMSE after the timed sweeps (sanity, not timed)
     rm = float(eng.rmse(wl.valid_users, wl.valid_items, wl.valid_scores).item())
+    n_launch = launches_per_sweep(eng) * args.steps
 
     # ---- CPU baseline (oracle port, bounded sample) ----
     cpu = None
@@ -373,7 +374,7 @@ def run_ours(args, rank, world):
                                  "no flush",
                            "parallelism": f"rows sharded over {world} GPU(s)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_sweep(eng) * args.steps, "clocks": clk.summary(),
+                "gpu_launches": n_launch, "clocks": clk.summary(),
                 "valid_rmse_after": rm, "layout_build_s": t_layout, "datagen_s": t_gen,
                 "sweep_ms_items_users": [roofline["launch_ms"]["items"],
                                          roofline["launch_ms"]["users"]]}

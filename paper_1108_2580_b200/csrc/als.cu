@@ -699,6 +699,243 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// wide-warp path, 28 < D <= 56 (config 4): one WARP per work item
+//
+// For NB8 <= 7 the lower triangle has at most 28 8x8 tiles, so a single warp
+// owns them all (one tile per lane) and needs no k-split, no cross-warp
+// reduction and no CTA barrier: gather (cp.async, double-buffered per warp),
+// 32 FFMA2 + 4 FFMA2 per rating per lane, stage the tiles in the warp's
+// shared memory, and solve with a warp-cooperative right-looking Cholesky
+// (lanes own rows i and i + 32; __syncwarp only).  Hot rows use the
+// last-arriver chunk reduction (fixed chunk order).
+
+template <int NB8>
+struct WideWarpCfg {
+    static constexpr int LDK = 8 * NB8;
+    static constexpr int T8 = NB8 * (NB8 + 1) / 2;
+    static_assert(T8 <= 32, "one tile per lane");
+    static constexpr int ROWS = LDK + 4;
+    static constexpr int STAGE = BATCH * ROWS + 2 * BATCH;
+    static constexpr int MS = LDK + 1;
+    static constexpr int WARP_FLOATS = (2 * STAGE > LDK * MS ? 2 * STAGE : LDK * MS);
+    static constexpr int WARPS = 4;
+    static constexpr int PSTRIDE = T8 * 72;
+};
+
+template <int NB8, bool HAS_W>
+__global__ void __launch_bounds__(128) k_als_wide_warp(AlsParams p) {
+    using C = WideWarpCfg<NB8>;
+    extern __shared__ float4 smem4[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *sm = reinterpret_cast<float *>(smem4) + warp * C::WARP_FLOATS;
+    float *M = sm;   // aliases the stages once the Gram is done
+    const int64_t item = (int64_t)blockIdx.x * C::WARPS + warp;
+    if (item >= p.total_items) return;
+    const ItemInfo it = item_info(p, item);
+    const int D = p.D;
+    const int nb4_real = (D + 3) / 4;
+    const bool tok = lane < C::T8;
+    int tI, tJ;
+    tile_of(tok ? lane : 0, tI, tJ);
+
+    float2 acc[8][4], rhs[4];
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[m][k] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
+
+    auto issue = [&](int64_t k, float *stage) {
+        float *ys = stage + BATCH * C::ROWS;
+        for (int e = lane; e < BATCH * (C::LDK / 4); e += 32) {
+            const int rr = e / (C::LDK / 4), part = e - rr * (C::LDK / 4);
+            const int64_t kk = k + rr;
+            const bool ok = kk < it.k1 && part < nb4_real;
+            const float *g = ok ? p.fixed + (size_t)p.idx[kk] * p.ld + part * 4 : p.fixed;
+            cp_async16(stage + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
+        }
+        const int64_t kk = k + lane;
+        const bool ok = kk < it.k1;
+        ys[lane] = ok ? p.val[kk] - p.y_shift : 0.f;
+        ys[BATCH + lane] = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
+        cp_async_commit();
+    };
+    const int64_t nbatch = (it.k1 - it.k0 + BATCH - 1) / BATCH;
+    if (nbatch > 0) issue(it.k0, sm);
+    for (int64_t bt = 0; bt < nbatch; ++bt) {
+        float *cur = sm + (bt & 1) * C::STAGE;
+        if (bt + 1 < nbatch) {
+            issue(it.k0 + (bt + 1) * BATCH, sm + ((bt + 1) & 1) * C::STAGE);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const float *ys = cur + BATCH * C::ROWS;
+        if (tok) {
+            for (int kb = 0; kb < BATCH; ++kb) {
+                const float *xr = cur + kb * C::ROWS;
+                const float y = ys[kb];
+                const float4 a0 = *reinterpret_cast<const float4 *>(xr + 8 * tI);
+                const float4 a1 = *reinterpret_cast<const float4 *>(xr + 8 * tI + 4);
+                const float4 b0 = *reinterpret_cast<const float4 *>(xr + 8 * tJ);
+                const float4 b1 = *reinterpret_cast<const float4 *>(xr + 8 * tJ + 4);
+                float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                if (HAS_W) {
+                    const float w = ys[BATCH + kb];
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) a[m] *= w;
+                }
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    ffma2(acc[m][0], a[m], b0.x, b0.y);
+                    ffma2(acc[m][1], a[m], b0.z, b0.w);
+                    ffma2(acc[m][2], a[m], b1.x, b1.y);
+                    ffma2(acc[m][3], a[m], b1.z, b1.w);
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) ffma2(rhs[m], y, a[2 * m], a[2 * m + 1]);
+            }
+        }
+        __syncwarp();   // this stage is refilled two batches later
+    }
+
+    if (it.nch > 1) {
+        float *slot0 = p.partials + (size_t)p.slot_off[it.j] * C::PSTRIDE;
+        if (tok) {
+            float *dst = slot0 + (size_t)it.c * C::PSTRIDE + lane * 72;
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    dst[m * 8 + 2 * k] = acc[m][k].x;
+                    dst[m * 8 + 2 * k + 1] = acc[m][k].y;
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                dst[64 + 2 * k] = rhs[k].x;
+                dst[64 + 2 * k + 1] = rhs[k].y;
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(p.counters + it.j, 1);
+        prev = __shfl_sync(FULL, prev, 0);
+        if (prev != it.nch - 1) return;
+        __threadfence();
+        if (lane == 0) p.counters[it.j] = 0;
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[m][k] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
+        if (tok) {
+            for (int c = 0; c < it.nch; ++c) {
+                const float *src = slot0 + (size_t)c * C::PSTRIDE + lane * 72;
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        acc[m][k].x += __ldcg(src + m * 8 + 2 * k);
+                        acc[m][k].y += __ldcg(src + m * 8 + 2 * k + 1);
+                    }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    rhs[k].x += __ldcg(src + 64 + 2 * k);
+                    rhs[k].y += __ldcg(src + 64 + 2 * k + 1);
+                }
+            }
+        }
+    }
+
+    const int r = it.r;
+    const float S = p.tax_S ? p.tax_S[r] : 0.f;
+    if (it.n == 0 && S == 0.f) {
+        if (p.lam_c > 0.f || p.lam_n > 0.f) {
+            for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = 0.f;
+        } else if (lane == 0) {
+            report_fail(p.fail, r);
+        }
+        return;
+    }
+    const float diag = p.lam_c + p.lam_n * (float)it.n + p.tau * S;
+    constexpr int MS = C::MS;
+    __syncwarp();
+    if (tok) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int row = 8 * tI + m;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int col = 8 * tJ + 2 * k + hh;
+                    if (col <= row) M[row * MS + col] = hh ? acc[m][k].y : acc[m][k].x;
+                }
+            }
+        }
+        if (tI == tJ) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                M[(8 * tI + 2 * k) * MS + C::LDK] = rhs[k].x;
+                M[(8 * tI + 2 * k + 1) * MS + C::LDK] = rhs[k].y;
+            }
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < D; i += 32) {
+        M[i * MS + i] += diag;
+        if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
+    }
+    __syncwarp();
+    // right-looking Cholesky: lane owns rows lane and lane + 32
+    for (int j = 0; j < D; ++j) {
+        const float piv = M[j * MS + j];
+        if (!(piv > 0.f) || !isfinite(piv)) {
+            if (lane == 0) report_fail(p.fail, r);
+            return;
+        }
+        const float l = sqrtf(piv), inv = 1.f / l;
+        float lij[2] = {0.f, 0.f};
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int i = lane + 32 * h2;
+            if (i > j && i < D) {
+                lij[h2] = M[i * MS + j] * inv;
+                for (int k = j + 1; k <= i; ++k)
+                    M[i * MS + k] = fmaf(-lij[h2], M[k * MS + j] * inv, M[i * MS + k]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int i = lane + 32 * h2;
+            if (i > j && i < D) M[i * MS + j] = lij[h2];
+        }
+        if (lane == 0) M[j * MS + j] = l;
+        __syncwarp();
+    }
+    for (int j = 0; j < D; ++j) {
+        if (lane == 0) M[j * MS + C::LDK] /= M[j * MS + j];
+        __syncwarp();
+        const float yj = M[j * MS + C::LDK];
+        for (int i = j + 1 + lane; i < D; i += 32) M[i * MS + C::LDK] -= M[i * MS + j] * yj;
+        __syncwarp();
+    }
+    for (int j = D - 1; j >= 0; --j) {
+        if (lane == 0) M[j * MS + C::LDK] /= M[j * MS + j];
+        __syncwarp();
+        const float xj = M[j * MS + C::LDK];
+        for (int i = lane; i < j; i += 32) M[i * MS + C::LDK] -= M[j * MS + i] * xj;
+        __syncwarp();
+    }
+    for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? M[i * MS + C::LDK] : 0.f;
+}
+
+// ---------------------------------------------------------------------------
 // pair path, D <= 20 (the hot kernel of configs 0-2)
 //
 // Row-parallel: a warp takes 16 tasks (rows, or CHUNK-long chunks of hot
@@ -1377,6 +1614,21 @@ int launch_cta(const AlsParams &p, cudaStream_t s) {
     return check_launch("mcf_als_half_step(wide)");
 }
 
+template <int NB8, bool W>
+int launch_wide_warp(const AlsParams &p, cudaStream_t s) {
+    using C = WideWarpCfg<NB8>;
+    const size_t smem = sizeof(float) * C::WARP_FLOATS * C::WARPS;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_als_wide_warp<NB8, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    const int64_t grid = ceil_div(p.total_items, C::WARPS);
+    if (grid > 0) k_als_wide_warp<NB8, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p);
+    return check_launch("mcf_als_half_step(wide-warp)");
+}
+
 int nb8_for(int D) {
     const int nb = (D + 7) / 8;
     return nb <= 4 ? 4 : nb <= 6 ? 6 : nb <= 7 ? 7 : nb <= 8 ? 8 : nb <= 10 ? 10 : nb <= 13 ? 13 : 16;
@@ -1396,9 +1648,9 @@ int dispatch(const AlsParams &p, cudaStream_t s) {
         default: break;
     }
     switch (nb8_for(p.D)) {
-        case 4: return launch_cta<4, W>(p, s);
-        case 6: return launch_cta<6, W>(p, s);
-        case 7: return launch_cta<7, W>(p, s);
+        case 4: return launch_wide_warp<4, W>(p, s);
+        case 6: return launch_wide_warp<6, W>(p, s);
+        case 7: return launch_wide_warp<7, W>(p, s);
         case 8: return launch_cta<8, W>(p, s);
         case 10: return launch_cta<10, W>(p, s);
         case 13: return launch_cta<13, W>(p, s);
