@@ -650,51 +650,169 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
         }
         __syncthreads();
     }
-    for (int i = tid; i < D; i += CTA_THREADS) {
-        M[i * MS + i] += diag;
-        if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
+    for (int i = tid; i < C::LDK; i += CTA_THREADS) {
+        if (i < D) {
+            M[i * MS + i] += diag;
+            if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
+        } else {   // padding rows: identity, zero rhs (their solution is 0)
+            M[i * MS + i] = 1.f;
+            M[i * MS + C::LDK] = 0.f;
+        }
     }
     __syncthreads();
-    // right-looking Cholesky, one column per step; thread i owns row i
-    // (D <= 128), so the trailing update needs no index arithmetic and
-    // column j is read unscaled (times 1/L_jj) before it is overwritten
-    for (int j = 0; j < D; ++j) {
-        const float piv = M[j * MS + j];
-        if (!(piv > 0.f) || !isfinite(piv)) {
-            if (tid == 0) report_fail(p.fail, r);
-            return;  // uniform: every thread read the same pivot
-        }
-        const float l = sqrtf(piv), inv = 1.f / l;
-        const int i = tid;
-        float lij = 0.f;
-        if (i > j && i < D) {
-            lij = M[i * MS + j] * inv;
-            for (int k = j + 1; k <= i; ++k)
-                M[i * MS + k] = fmaf(-lij, M[k * MS + j] * inv, M[i * MS + k]);
+
+    // ---- blocked right-looking Cholesky on the 8x8 tiles (team-0 threads own
+    // their tiles in registers; the current panel lives in shared memory):
+    // per block column J: factor the diagonal tile (+ its inverse), form the
+    // panel L_IJ = A_IJ L_JJ^{-T}, update the trailing tiles A_IK -= L_IJ L_KJ^T.
+    float t[C::TPT][8][8];
+    const bool own = team == 0;
+#pragma unroll
+    for (int q = 0; q < C::TPT; ++q) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int n = 0; n < 8; ++n) {
+                const int row = 8 * tI[q] + m, col = 8 * tJ[q] + n;
+                t[q][m][n] = (own && tok[q] && col <= row) ? M[row * MS + col]
+                           : (own && tok[q] && tI[q] == tJ[q]) ? M[col * MS + row] : 0.f;
+            }
+    }
+    float bvec = tid < C::LDK ? M[tid * MS + C::LDK] : 0.f;
+    __syncthreads();
+    float *PAN = M;                          // [NB8][64] current panel
+    float *LINV = M + NB8 * 64;              // [64] inverse of the diagonal tile
+    if (tid == 0) s_flag = 0;
+    __syncthreads();
+    for (int J = 0; J < NB8; ++J) {
+        // (a) diagonal tile
+#pragma unroll
+        for (int q = 0; q < C::TPT; ++q) {
+            if (!(own && tok[q] && tI[q] == J && tJ[q] == J)) continue;
+            bool bad = false;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                float d = t[q][c][c];
+#pragma unroll
+                for (int k = 0; k < c; ++k) d = fmaf(-t[q][c][k], t[q][c][k], d);
+                bad |= !(d > 0.f) || !isfinite(d);
+                const float l = sqrtf(d), inv = 1.f / l;
+                t[q][c][c] = l;
+#pragma unroll
+                for (int r2 = c + 1; r2 < 8; ++r2) {
+                    float v = t[q][r2][c];
+#pragma unroll
+                    for (int k = 0; k < c; ++k) v = fmaf(-t[q][r2][k], t[q][c][k], v);
+                    t[q][r2][c] = v * inv;
+                }
+            }
+            // inverse of the lower-triangular tile
+            float li[8][8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+#pragma unroll
+                for (int r2 = 0; r2 < 8; ++r2) li[r2][c] = 0.f;
+                li[c][c] = 1.f / t[q][c][c];
+#pragma unroll
+                for (int r2 = c + 1; r2 < 8; ++r2) {
+                    float v = 0.f;
+#pragma unroll
+                    for (int k = c; k < r2; ++k) v = fmaf(t[q][r2][k], li[k][c], v);
+                    li[r2][c] = -v / t[q][r2][r2];
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    LINV[m * 8 + n] = li[m][n];
+                    PAN[J * 64 + m * 8 + n] = n <= m ? t[q][m][n] : 0.f;
+                }
+            if (bad) s_flag = 1;
         }
         __syncthreads();
-        if (i > j && i < D) M[i * MS + j] = lij;
-        if (i == j) M[j * MS + j] = l;
+        if (s_flag) {
+            if (tid == 0) report_fail(p.fail, r);
+            return;
+        }
+        // (b) panel tiles below the diagonal
+#pragma unroll
+        for (int q = 0; q < C::TPT; ++q) {
+            if (!(own && tok[q] && tJ[q] == J && tI[q] > J)) continue;
+            float l2[8][8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    float v = 0.f;
+#pragma unroll
+                    for (int k = 0; k <= n; ++k) v = fmaf(t[q][m][k], LINV[n * 8 + k], v);
+                    l2[m][n] = v;
+                }
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    t[q][m][n] = l2[m][n];
+                    PAN[tI[q] * 64 + m * 8 + n] = l2[m][n];
+                }
+        }
+        __syncthreads();
+        // (c) trailing update
+#pragma unroll
+        for (int q = 0; q < C::TPT; ++q) {
+            if (!(own && tok[q] && tJ[q] > J)) continue;
+            const float *pi = PAN + tI[q] * 64, *pk = PAN + tJ[q] * 64;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                float ci[8], ck[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    ci[m] = pi[m * 8 + k];
+                    ck[m] = pk[m * 8 + k];
+                }
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+#pragma unroll
+                    for (int n = 0; n < 8; ++n) t[q][m][n] = fmaf(-ci[m], ck[n], t[q][m][n]);
+            }
+        }
         __syncthreads();
     }
-    // triangular solves by one warp
+    // ---- triangular solves: the L tiles go to shared memory, one warp solves
+    float *LT = M;                           // [T8][64] tile-major
+    float *vb = M + C::T8 * 64;              // [LDK] rhs -> solution
+#pragma unroll
+    for (int q = 0; q < C::TPT; ++q) {
+        if (!(own && tok[q])) continue;
+        const int tix = tI[q] * (tI[q] + 1) / 2 + tJ[q];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int n = 0; n < 8; ++n) LT[tix * 64 + m * 8 + n] = t[q][m][n];
+    }
+    if (tid < C::LDK) vb[tid] = bvec;
+    __syncthreads();
+    auto Lat = [&](int i, int k) {   // L[i][k], k <= i
+        const int I = i >> 3, K = k >> 3;
+        return LT[(I * (I + 1) / 2 + K) * 64 + (i & 7) * 8 + (k & 7)];
+    };
     if (tid < 32) {
-        for (int j = 0; j < D; ++j) {
-            if (tid == 0) M[j * MS + C::LDK] /= M[j * MS + j];
+        for (int j = 0; j < C::LDK; ++j) {
+            if (tid == 0) vb[j] /= Lat(j, j);
             __syncwarp();
-            const float yj = M[j * MS + C::LDK];
-            for (int i = j + 1 + tid; i < D; i += 32) M[i * MS + C::LDK] -= M[i * MS + j] * yj;
-            __syncwarp();
-        }
-        for (int j = D - 1; j >= 0; --j) {
-            if (tid == 0) M[j * MS + C::LDK] /= M[j * MS + j];
-            __syncwarp();
-            const float xj = M[j * MS + C::LDK];
-            for (int i = tid; i < j; i += 32) M[i * MS + C::LDK] -= M[j * MS + i] * xj;
+            const float yj = vb[j];
+            for (int i = j + 1 + tid; i < C::LDK; i += 32) vb[i] = fmaf(-Lat(i, j), yj, vb[i]);
             __syncwarp();
         }
-        for (int i = tid; i < p.ld; i += 32)
-            p.out[(size_t)r * p.ld + i] = i < D ? M[i * MS + C::LDK] : 0.f;
+        for (int j = C::LDK - 1; j >= 0; --j) {
+            if (tid == 0) vb[j] /= Lat(j, j);
+            __syncwarp();
+            const float xj = vb[j];
+            for (int i = tid; i < j; i += 32) vb[i] = fmaf(-Lat(j, i), xj, vb[i]);
+            __syncwarp();
+        }
+        for (int i = tid; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? vb[i] : 0.f;
     }
 }
 
