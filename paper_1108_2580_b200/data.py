@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ConfigError, RangeError
+from .errors import ConfigError, ParseError, RangeError
 
 
 @dataclass(frozen=True)
@@ -103,3 +103,35 @@ class Dataset:
         keys, n = ((self.users, self.num_users) if side == "users"
                    else (self.items, self.num_items))
         return np.bincount(keys, minlength=n).astype(np.int64)
+
+
+def load_ratings(path, split: str = "train", scale: ScoreScale = DEFAULT_SCALE,
+                 compact: bool = False) -> Dataset:
+    """Parse `user<TAB>item<TAB>score<TAB>time` lines; blank and '#' lines are
+    skipped; non-numeric fields, negative ids and scores outside the scale
+    raise (reference data.py:163-191)."""
+    users, items, scores, times = [], [], [], []
+    with open(path, "r", encoding="utf-8") as fh:
+        for line_no, line in enumerate(fh, start=1):
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            parts = line.split("\t")
+            if len(parts) != 4:
+                raise ParseError(path, line_no,
+                                 f"expected 4 tab-separated fields, got {len(parts)}")
+            try:
+                u, i, sc, t = int(parts[0]), int(parts[1]), float(parts[2]), int(parts[3])
+            except ValueError as exc:
+                raise ParseError(path, line_no, f"non-numeric field: {exc}") from None
+            if u < 0 or i < 0:
+                raise ParseError(path, line_no, "negative id")
+            if not scale.contains(sc):
+                raise RangeError(f"{path}:{line_no}: score {sc} outside scale "
+                                 f"[{scale.lo}, {scale.hi}]")
+            users.append(u)
+            items.append(i)
+            scores.append(sc)
+            times.append(t)
+    return Dataset.from_arrays(users, items, scores, times, split=split, scale=scale,
+                               compact=compact)

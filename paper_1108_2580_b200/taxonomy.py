@@ -18,7 +18,7 @@ from enum import IntEnum
 
 import numpy as np
 
-from .errors import TaxonomyError, UnknownIdError
+from .errors import DanglingReferenceError, ParseError, TaxonomyError, UnknownIdError
 
 
 class ItemKind(IntEnum):
@@ -153,3 +153,71 @@ def build_graph(kind, album_of, artist_link, genres: dict | None = None,
     np.cumsum(cnt, out=ptr[1:])
     return build_graph_arrays(kind, album_of, artist_link, ptr,
                               np.asarray(ids, dtype=np.int64), dropped)
+
+
+_KIND_NAMES = {"track": ItemKind.TRACK, "album": ItemKind.ALBUM, "artist": ItemKind.ARTIST}
+
+
+def load_taxonomy(path, strict: bool = True) -> TaxonomyGraph:
+    """Parse `kind|item|album_or_NA|artist_or_NA|genre,genre,...` lines
+    (reference taxonomy.py:121-196): strict mode raises on undeclared or
+    wrong-kind parents, lenient mode drops and counts them; a track with an
+    album but no artist inherits the album's artist."""
+    rows = []
+    with open(path, "r", encoding="utf-8") as fh:
+        for line_no, line in enumerate(fh, start=1):
+            line = line.rstrip("\n")
+            if not line.strip() or line.startswith("#"):
+                continue
+            parts = line.split("|")
+            if len(parts) != 5:
+                raise ParseError(path, line_no, f"expected 5 '|' fields, got {len(parts)}")
+            kname, id_s, alb_s, art_s, gen_s = parts
+            if kname not in _KIND_NAMES:
+                raise ParseError(path, line_no, f"unknown kind {kname!r}")
+            try:
+                item = int(id_s)
+                alb = -1 if alb_s == "NA" else int(alb_s)
+                art = -1 if art_s == "NA" else int(art_s)
+                gens = tuple(int(g) for g in gen_s.split(",") if g)
+            except ValueError as exc:
+                raise ParseError(path, line_no, f"non-numeric field: {exc}") from None
+            if item < 0:
+                raise ParseError(path, line_no, "negative item id")
+            rows.append((line_no, _KIND_NAMES[kname], item, alb, art, gens))
+    if not rows:
+        return build_graph(np.empty(0, np.int8), np.empty(0, np.int64), np.empty(0, np.int64), {})
+    n = max(r[2] for r in rows) + 1
+    kind = np.full(n, -1, dtype=np.int8)
+    album_of = np.full(n, -1, dtype=np.int64)
+    artist_link = np.full(n, -1, dtype=np.int64)
+    genres = {}
+    for line_no, k, item, _, _, _ in rows:
+        if kind[item] >= 0:
+            raise TaxonomyError(f"{path}:{line_no}: item {item} declared twice")
+        kind[item] = k
+    dropped = 0
+    for line_no, k, item, alb, art, gens in rows:
+        if gens:
+            genres[item] = gens
+        if k == ItemKind.ARTIST:
+            if alb >= 0 or art >= 0:
+                raise ParseError(path, line_no, "artists cannot have parents")
+            continue
+        if k == ItemKind.ALBUM and alb >= 0:
+            raise ParseError(path, line_no, "albums cannot have an album parent")
+        for ref, want, slot in ((alb, ItemKind.ALBUM, album_of), (art, ItemKind.ARTIST, artist_link)):
+            if ref < 0:
+                continue
+            if ref < n and kind[ref] == want:
+                slot[item] = ref
+            elif strict:
+                raise DanglingReferenceError(
+                    f"{path}:{line_no}: item {item} references undeclared "
+                    f"{'album' if want == ItemKind.ALBUM else 'artist'} {ref}")
+            else:
+                dropped += 1
+    for _, k, item, _, _, _ in rows:
+        if k == ItemKind.TRACK and artist_link[item] < 0 and album_of[item] >= 0:
+            artist_link[item] = artist_link[album_of[item]]
+    return build_graph(kind, album_of, artist_link, genres, dropped)

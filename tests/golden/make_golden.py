@@ -33,6 +33,8 @@ Fixtures (reference entry point -> file):
                      synth.generate_synthetic instance with random parameters
   mfitr_cfg2s.npz    config-2 shaped workload (this repo's generator, scaled):
                      reference edge weights, loss_mfitr, grad_mfitr
+  formats.npz        data.load_ratings on ratings_small.tsv; modelio.save_model
+                     bytes of an ALS and an MFITR model
 """
 from __future__ import annotations
 
@@ -305,6 +307,45 @@ def mfitr_cfg2s():
                         lam4=h.lam4, loss=loss, grad_p=grad["p"], grad_q=grad["q"])
 
 
+def formats():
+    """Files written by the reference: a ratings TSV it loads, and the
+    binary model format for an ALS and an MFITR model."""
+    from multicf import modelio
+    from multicf.data import load_ratings
+    rng = np.random.default_rng(21)
+    lines = ["# user item score time"]
+    for k in range(40):
+        lines.append(f"{rng.integers(0, 9)}\t{rng.integers(0, 7)}\t{float(rng.integers(0, 101))}"
+                     f"\t{rng.integers(1000, 2000)}")
+        if k == 10:
+            lines.append("")
+    with open(os.path.join(HERE, "ratings_small.tsv"), "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    ds = load_ratings(os.path.join(HERE, "ratings_small.tsv"))
+    hp = factor.HyperParams(lam=1.0, D=3, iters=1)
+    m = factor.init_model("als", ds, hp, 5)
+    m.p[:] = rng.normal(size=m.p.shape).astype(np.float32)
+    m.q[:] = rng.normal(size=m.q.shape).astype(np.float32)
+    m.epochs_done = 3
+    with tempfile.TemporaryDirectory() as td:
+        modelio.save_model(m, os.path.join(td, "als.bin"))
+        als_bytes = open(os.path.join(td, "als.bin"), "rb").read()
+        cfg = synth.SynthConfig(users=9, artists=2, albums_per_artist=1, tracks_per_album=2,
+                                ratings_per_user=2, dim=3)
+        g = synth.build_taxonomy(cfg)
+        mm = mfitr.init_mfitr("mfitr", ds, g, mfitr.MfitrHyper(D=3), 2, num_users=9,
+                              num_items=max(7, g.num_nodes))
+        mm.base.p[:] = rng.normal(size=mm.base.p.shape).astype(np.float32)
+        mm.base.q[:] = rng.normal(size=mm.base.q.shape).astype(np.float32)
+        mm.q_a[:] = 0.0
+        modelio.save_model(mm, os.path.join(td, "mfitr.bin"))
+        mf_bytes = open(os.path.join(td, "mfitr.bin"), "rb").read()
+    np.savez_compressed(os.path.join(HERE, "formats.npz"), users=ds.users, items=ds.items,
+                        scores=ds.scores, times=ds.times,
+                        als_bytes=np.frombuffer(als_bytes, np.uint8),
+                        mfitr_bytes=np.frombuffer(mf_bytes, np.uint8))
+
+
 def main():
     with open(os.path.join(HERE, "spec_scalars.json"), "w") as fh:
         json.dump(spec_scalars(), fh, indent=1)
@@ -315,6 +356,7 @@ def main():
     mfitr_fx()
     als_cfg0()
     mfitr_cfg2s()
+    formats()
     print("golden fixtures written to", HERE)
 
 
