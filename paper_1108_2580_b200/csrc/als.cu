@@ -466,41 +466,55 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
         for (int k = 0; k < 4; ++k) rhs[q][k] = make_float2(0.f, 0.f);
     }
 
-    auto issue = [&](int64_t k, float *stage) {
-        float *xs = stage;
-        float *ys = stage + BATCH * C::ROWS;
+    // Per-batch operands (partner ids, ratings, weights) are loaded by warp 0
+    // one batch ahead into a 3-slot ring; the partner-row gathers of batch
+    // b+1 (cp.async) overlap the FMAs of batch b.
+    __shared__ int ring_id[3][BATCH];
+    __shared__ float ring_y[3][BATCH], ring_w[3][BATCH];
+    auto load_ops = [&](int64_t b) {   // warp 0: batch b -> ring slot b % 3
+        if (tid < BATCH) {
+            const int64_t kk = it.k0 + b * BATCH + tid;
+            const bool ok = kk < it.k1;
+            ring_id[b % 3][tid] = ok ? p.idx[kk] : -1;
+            ring_y[b % 3][tid] = ok ? p.val[kk] - p.y_shift : 0.f;
+            ring_w[b % 3][tid] = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
+        }
+    };
+    auto issue = [&](int64_t b, float *stage) {
+        const int *ids = ring_id[b % 3];
         for (int e = tid; e < BATCH * (C::LDK / 4); e += CTA_THREADS) {
             const int rr = e / (C::LDK / 4), part = e - rr * (C::LDK / 4);
-            const int64_t kk = k + rr;
-            const bool ok = kk < it.k1 && part < nb4_real;
-            const float *g = ok ? p.fixed + (size_t)p.idx[kk] * p.ld + part * 4 : p.fixed;
-            cp_async16(xs + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
-        }
-        if (tid < BATCH) {
-            const int64_t kk = k + tid;
-            const bool ok = kk < it.k1;
-            ys[tid] = ok ? p.val[kk] - p.y_shift : 0.f;
-            ys[BATCH + tid] = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
+            const int id = ids[rr];
+            const bool ok = id >= 0 && part < nb4_real;
+            const float *g = ok ? p.fixed + (size_t)id * p.ld + part * 4 : p.fixed;
+            cp_async16(stage + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
         }
         cp_async_commit();
     };
     const int64_t nbatch = (it.k1 - it.k0 + BATCH - 1) / BATCH;
-    if (nbatch > 0) issue(it.k0, sm);
+    if (nbatch > 0) {
+        load_ops(0);
+        if (nbatch > 1) load_ops(1);
+        __syncthreads();
+        issue(0, sm);
+    }
     for (int64_t bt = 0; bt < nbatch; ++bt) {
         float *cur = sm + (bt & 1) * C::STAGE;
         if (bt + 1 < nbatch) {
-            issue(it.k0 + (bt + 1) * BATCH, sm + ((bt + 1) & 1) * C::STAGE);
+            issue(bt + 1, sm + ((bt + 1) & 1) * C::STAGE);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
+        if (bt + 2 < nbatch) load_ops(bt + 2);   // consumed after the next barrier
         __syncthreads();
         const float *xs = cur;
-        const float *ys = cur + BATCH * C::ROWS;
+        const float *ys = ring_y[bt % 3];
+        const float *wsv = ring_w[bt % 3];
         for (int kb = team; kb < BATCH; kb += C::TEAMS) {
             const float *xr = xs + kb * C::ROWS;
             const float y = ys[kb];
-            const float w = HAS_W ? ys[BATCH + kb] : 1.f;
+            const float w = HAS_W ? wsv[kb] : 1.f;
 #pragma unroll
             for (int q = 0; q < C::TPT; ++q) {
                 if (!tok[q]) continue;
@@ -864,27 +878,43 @@ __global__ void __launch_bounds__(128) k_als_wide_warp(AlsParams p) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
 
-    auto issue = [&](int64_t k, float *stage) {
+    // lane l holds the operands of rating l of the NEXT batch (loaded one
+    // batch ahead); the ids are broadcast with shuffles for the gathers
+    auto ld = [&](int64_t b, int &id, float &y, float &w) {
+        const int64_t kk = it.k0 + b * BATCH + lane;
+        const bool ok = kk < it.k1;
+        id = ok ? p.idx[kk] : -1;
+        y = ok ? p.val[kk] - p.y_shift : 0.f;
+        w = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
+    };
+    auto issue = [&](int id, float y, float w, float *stage) {
         float *ys = stage + BATCH * C::ROWS;
         for (int e = lane; e < BATCH * (C::LDK / 4); e += 32) {
             const int rr = e / (C::LDK / 4), part = e - rr * (C::LDK / 4);
-            const int64_t kk = k + rr;
-            const bool ok = kk < it.k1 && part < nb4_real;
-            const float *g = ok ? p.fixed + (size_t)p.idx[kk] * p.ld + part * 4 : p.fixed;
+            const int rid = __shfl_sync(FULL, id, rr);
+            const bool ok = rid >= 0 && part < nb4_real;
+            const float *g = ok ? p.fixed + (size_t)rid * p.ld + part * 4 : p.fixed;
             cp_async16(stage + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
         }
-        const int64_t kk = k + lane;
-        const bool ok = kk < it.k1;
-        ys[lane] = ok ? p.val[kk] - p.y_shift : 0.f;
-        ys[BATCH + lane] = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
+        ys[lane] = y;
+        ys[BATCH + lane] = w;
         cp_async_commit();
     };
     const int64_t nbatch = (it.k1 - it.k0 + BATCH - 1) / BATCH;
-    if (nbatch > 0) issue(it.k0, sm);
+    int nid = -1;
+    float ny = 0.f, nw = 0.f;
+    if (nbatch > 0) {
+        int id0;
+        float y0, w0;
+        ld(0, id0, y0, w0);
+        issue(id0, y0, w0, sm);
+        if (nbatch > 1) ld(1, nid, ny, nw);
+    }
     for (int64_t bt = 0; bt < nbatch; ++bt) {
         float *cur = sm + (bt & 1) * C::STAGE;
         if (bt + 1 < nbatch) {
-            issue(it.k0 + (bt + 1) * BATCH, sm + ((bt + 1) & 1) * C::STAGE);
+            issue(nid, ny, nw, sm + ((bt + 1) & 1) * C::STAGE);
+            if (bt + 2 < nbatch) ld(bt + 2, nid, ny, nw);   // used one batch later
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
