@@ -281,11 +281,21 @@ def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: Hyp
             raise ConfigError("observation weights must be >= 0")
         if weights.size != len(train_data):
             raise ShapeError(f"expected {len(train_data)} weights, got {weights.size}")
-    model = init_model(kind, train_data, hyper, seed, num_users=num_users, num_items=num_items)
+    if init is not None:
+        # given factors replace the seeded draw (no host RNG pass over U+I rows)
+        P0, Q0 = init
+        U = num_users if num_users is not None else train_data.num_users
+        I = num_items if num_items is not None else train_data.num_items
+        if tuple(P0.shape) != (U, hyper.D) or tuple(Q0.shape) != (I, hyper.D):
+            raise ShapeError(f"init factors must be ({U}, {hyper.D}) and ({I}, {hyper.D})")
+        model = FactorModel(kind, 0.0, np.zeros(U), np.zeros(I), P0, Q0, hyper.D, seed,
+                            train_data.scale)
+    else:
+        model = init_model(kind, train_data, hyper, seed, num_users=num_users,
+                           num_items=num_items)
     eng = _engine_for(model, train_data, device, keep_perm=weights is not None)
     if init is not None:
         # uploaded as given (fp32 stays fp32; a pinned source copies asynchronously)
-        P0, Q0 = init
         eng.set_factors(P0, Q0)
     else:
         eng.set_factors(model.p, model.q)
