@@ -831,76 +831,142 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// wide-warp path, 28 < D <= 56 (config 4): one WARP per work item
+// tile-warp path, 28 < D <= 104 (configs 3 and 4): one WARP per work item,
+// the whole [A | b] system in the warp's registers
 //
-// For NB8 <= 7 the lower triangle has at most 28 8x8 tiles, so a single warp
-// owns them all (one tile per lane) and needs no k-split, no cross-warp
-// reduction and no CTA barrier: gather (cp.async, double-buffered per warp),
-// 32 FFMA2 + 4 FFMA2 per rating per lane, stage the tiles in the warp's
-// shared memory, and solve with a warp-cooperative right-looking Cholesky
-// (lanes own rows i and i + 32; __syncwarp only).  Hot rows use the
-// last-arriver chunk reduction (fixed chunk order).
+// The lower triangle of A is cut into 8x8 tiles (NB8 blocks, T8 tiles);
+// tile t lives in lane t % 32, register slot t / 32 (S <= 3 slots).
+//   Gram:  per rating a lane loads its tiles' two 8-float row pieces from
+//          the gathered partner row (4 LDS.128 per tile) and issues 32 FFMA2
+//          per tile; the lane holding a diagonal tile also accumulates that
+//          block of b.  Partner rows are gathered with 16-byte cp.async into
+//          a per-warp double buffer, partner ids are staged one batch ahead
+//          in registers and broadcast with shuffles.
+//   Solve: blocked right-looking Cholesky in registers (same algorithm as
+//          the reference's row-oriented one, _kernels.py:187-203, reordered
+//          by 8x8 blocks).  Block column J: the diagonal lane factors its
+//          tile; panel lanes solve their tile against it and publish it
+//          transposed to shared memory; every lane then updates its trailing
+//          tiles with 32 FFMA2 per panel column.  Forward substitution rides
+//          along (b in shared memory, one writer per block per step); the
+//          back substitution walks block rows bottom-up (_kernels.py:204-213).
+//          Only __syncwarp: rows never wait on other warps, so a handful of
+//          warps per SM keep the FMA pipe busy while others are on barriers.
+// Hot rows are split into chunks whose partial tiles are summed in chunk
+// order by the last chunk to finish (deterministic).
 
 template <int NB8>
-struct WideWarpCfg {
+struct TileWarpCfg {
     static constexpr int LDK = 8 * NB8;
     static constexpr int T8 = NB8 * (NB8 + 1) / 2;
-    static_assert(T8 <= 32, "one tile per lane");
-    static constexpr int ROWS = LDK + 4;
-    static constexpr int STAGE = BATCH * ROWS + 2 * BATCH;
-    static constexpr int MS = LDK + 1;
-    static constexpr int WARP_FLOATS = (2 * STAGE > LDK * MS ? 2 * STAGE : LDK * MS);
+    static constexpr int S = (T8 + 31) / 32;         // register tiles per lane
+    static constexpr int BT = 16;                    // ratings per stage
+    static constexpr int ROWS = LDK + 4;             // smem row stride (floats)
+    static constexpr int STAGE = BT * ROWS + 2 * BT;
+    // solve scratch: PT [8][LDK], L_JJ [64], inverse diagonal [LDK], b [LDK],
+    // back-substitution flag
+    static constexpr int SOLVE = 8 * LDK + 64 + LDK + LDK + 4;
+    static constexpr int WARP_FLOATS = ((2 * STAGE > SOLVE ? 2 * STAGE : SOLVE) + 3) / 4 * 4;
     static constexpr int WARPS = 4;
-    static constexpr int PSTRIDE = T8 * 72;
+    static constexpr int PSTRIDE = T8 * 72;           // 64 tile + 8 rhs floats per tile
+    static_assert(S <= 3, "at most 3 register tiles per lane");
 };
 
+// Tile order: by block column, last column first (q = 0 is (NB-1, NB-1)),
+// rows ascending inside a column.  Tile q lives in lane q % 32, slot q / 32,
+// so slot 0 holds the columns the right-looking update touches longest and
+// the later slots go idle early (the update of slot s runs only while one of
+// its tiles is still trailing).
+template <int NB>
+__device__ __forceinline__ void tile_of_by_col(int q, int &I, int &K) {
+    int k = NB - 1;
+    while (q >= NB - k) {
+        q -= NB - k;
+        --k;
+    }
+    K = k;
+    I = k + q;
+}
+
+// Every lane must hold at most one diagonal tile (one rhs block per lane).
+constexpr bool diag_lanes_distinct(int nb) {
+    int pos[16] = {};
+    int q = 0;
+    for (int k = nb - 1; k >= 0; --k) {
+        pos[k] = q;
+        q += nb - k;
+    }
+    for (int a = 0; a < nb; ++a)
+        for (int b = a + 1; b < nb; ++b)
+            if (pos[a] % 32 == pos[b] % 32) return false;
+    return true;
+}
+static_assert(diag_lanes_distinct(4) && diag_lanes_distinct(6) && diag_lanes_distinct(7) &&
+                  diag_lanes_distinct(8) && diag_lanes_distinct(10) && diag_lanes_distinct(13),
+              "diagonal tiles share a lane");
+
+__device__ __forceinline__ float &tel(float2 (&t)[8][4], int m, int n) {
+    return (n & 1) ? t[m][n >> 1].y : t[m][n >> 1].x;
+}
+
 template <int NB8, bool HAS_W>
-__global__ void __launch_bounds__(128) k_als_wide_warp(AlsParams p) {
-    using C = WideWarpCfg<NB8>;
+__global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
+    using C = TileWarpCfg<NB8>;
+    constexpr int S = C::S, LDK = C::LDK, BT = C::BT;
     extern __shared__ float4 smem4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float *sm = reinterpret_cast<float *>(smem4) + warp * C::WARP_FLOATS;
-    float *M = sm;   // aliases the stages once the Gram is done
     const int64_t item = (int64_t)blockIdx.x * C::WARPS + warp;
     if (item >= p.total_items) return;
     const ItemInfo it = item_info(p, item);
     const int D = p.D;
     const int nb4_real = (D + 3) / 4;
-    const bool tok = lane < C::T8;
-    int tI, tJ;
-    tile_of(tok ? lane : 0, tI, tJ);
 
-    float2 acc[8][4], rhs[4];
+    int tI[S], tJ[S];
+    bool tok[S];
+    int dslot = -1;
 #pragma unroll
-    for (int m = 0; m < 8; ++m)
+    for (int s = 0; s < S; ++s) {
+        const int t = lane + 32 * s;
+        tok[s] = t < C::T8;
+        tile_of_by_col<NB8>(tok[s] ? t : 0, tI[s], tJ[s]);
+        if (tok[s] && tI[s] == tJ[s]) dslot = s;
+    }
+
+    float2 acc[S][8][4], rhs[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[m][k] = make_float2(0.f, 0.f);
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[s][m][k] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
 
-    // lane l holds the operands of rating l of the NEXT batch (loaded one
-    // batch ahead); the ids are broadcast with shuffles for the gathers
+    // ---- Gram ---------------------------------------------------------------
     auto ld = [&](int64_t b, int &id, float &y, float &w) {
-        const int64_t kk = it.k0 + b * BATCH + lane;
-        const bool ok = kk < it.k1;
+        const int64_t kk = it.k0 + b * BT + lane;
+        const bool ok = lane < BT && kk < it.k1;
         id = ok ? p.idx[kk] : -1;
         y = ok ? p.val[kk] - p.y_shift : 0.f;
         w = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
     };
     auto issue = [&](int id, float y, float w, float *stage) {
-        float *ys = stage + BATCH * C::ROWS;
-        for (int e = lane; e < BATCH * (C::LDK / 4); e += 32) {
-            const int rr = e / (C::LDK / 4), part = e - rr * (C::LDK / 4);
+        float *ys = stage + BT * C::ROWS;
+        for (int e = lane; e < BT * (LDK / 4); e += 32) {
+            const int rr = e / (LDK / 4), part = e - rr * (LDK / 4);
             const int rid = __shfl_sync(FULL, id, rr);
             const bool ok = rid >= 0 && part < nb4_real;
             const float *g = ok ? p.fixed + (size_t)rid * p.ld + part * 4 : p.fixed;
             cp_async16(stage + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
         }
-        ys[lane] = y;
-        ys[BATCH + lane] = w;
+        if (lane < BT) {
+            ys[lane] = y;
+            ys[BT + lane] = w;
+        }
         cp_async_commit();
     };
-    const int64_t nbatch = (it.k1 - it.k0 + BATCH - 1) / BATCH;
+    const int64_t nbatch = (it.k1 - it.k0 + BT - 1) / BT;
     int nid = -1;
     float ny = 0.f, nw = 0.f;
     if (nbatch > 0) {
@@ -914,56 +980,61 @@ __global__ void __launch_bounds__(128) k_als_wide_warp(AlsParams p) {
         float *cur = sm + (bt & 1) * C::STAGE;
         if (bt + 1 < nbatch) {
             issue(nid, ny, nw, sm + ((bt + 1) & 1) * C::STAGE);
-            if (bt + 2 < nbatch) ld(bt + 2, nid, ny, nw);   // used one batch later
+            if (bt + 2 < nbatch) ld(bt + 2, nid, ny, nw);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncwarp();
-        const float *ys = cur + BATCH * C::ROWS;
-        if (tok) {
-            for (int kb = 0; kb < BATCH; ++kb) {
-                const float *xr = cur + kb * C::ROWS;
-                const float y = ys[kb];
-                const float4 a0 = *reinterpret_cast<const float4 *>(xr + 8 * tI);
-                const float4 a1 = *reinterpret_cast<const float4 *>(xr + 8 * tI + 4);
-                const float4 b0 = *reinterpret_cast<const float4 *>(xr + 8 * tJ);
-                const float4 b1 = *reinterpret_cast<const float4 *>(xr + 8 * tJ + 4);
+        const float *ys = cur + BT * C::ROWS;
+        for (int kb = 0; kb < BT; ++kb) {
+            const float *xr = cur + kb * C::ROWS;
+            const float y = ys[kb];
+            const float w = HAS_W ? ys[BT + kb] : 1.f;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (!tok[s]) continue;
+                const float4 a0 = *reinterpret_cast<const float4 *>(xr + 8 * tI[s]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(xr + 8 * tI[s] + 4);
+                const float4 b0 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[s]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[s] + 4);
                 float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 if (HAS_W) {
-                    const float w = ys[BATCH + kb];
 #pragma unroll
                     for (int m = 0; m < 8; ++m) a[m] *= w;
                 }
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
-                    ffma2(acc[m][0], a[m], b0.x, b0.y);
-                    ffma2(acc[m][1], a[m], b0.z, b0.w);
-                    ffma2(acc[m][2], a[m], b1.x, b1.y);
-                    ffma2(acc[m][3], a[m], b1.z, b1.w);
+                    ffma2(acc[s][m][0], a[m], b0.x, b0.y);
+                    ffma2(acc[s][m][1], a[m], b0.z, b0.w);
+                    ffma2(acc[s][m][2], a[m], b1.x, b1.y);
+                    ffma2(acc[s][m][3], a[m], b1.z, b1.w);
                 }
+                if (s == dslot) {
 #pragma unroll
-                for (int m = 0; m < 4; ++m) ffma2(rhs[m], y, a[2 * m], a[2 * m + 1]);
+                    for (int m = 0; m < 4; ++m) ffma2(rhs[m], y, a[2 * m], a[2 * m + 1]);
+                }
             }
         }
         __syncwarp();   // this stage is refilled two batches later
     }
 
+    // ---- hot rows: chunk partials, summed in chunk order by the last chunk ----
     if (it.nch > 1) {
         float *slot0 = p.partials + (size_t)p.slot_off[it.j] * C::PSTRIDE;
-        if (tok) {
-            float *dst = slot0 + (size_t)it.c * C::PSTRIDE + lane * 72;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!tok[s]) continue;
+            float *dst = slot0 + (size_t)it.c * C::PSTRIDE + (lane + 32 * s) * 72;
 #pragma unroll
             for (int m = 0; m < 8; ++m)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    dst[m * 8 + 2 * k] = acc[m][k].x;
-                    dst[m * 8 + 2 * k + 1] = acc[m][k].y;
-                }
+                for (int k = 0; k < 4; ++k)
+                    *reinterpret_cast<float2 *>(dst + m * 8 + 2 * k) = acc[s][m][k];
+            if (s == dslot) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                dst[64 + 2 * k] = rhs[k].x;
-                dst[64 + 2 * k + 1] = rhs[k].y;
+                for (int k = 0; k < 4; ++k)
+                    *reinterpret_cast<float2 *>(dst + 64 + 2 * k) = rhs[k];
             }
         }
         __threadfence();
@@ -975,33 +1046,41 @@ __global__ void __launch_bounds__(128) k_als_wide_warp(AlsParams p) {
         __threadfence();
         if (lane == 0) p.counters[it.j] = 0;
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+        for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[m][k] = make_float2(0.f, 0.f);
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[s][m][k] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
-        if (tok) {
-            for (int c = 0; c < it.nch; ++c) {
-                const float *src = slot0 + (size_t)c * C::PSTRIDE + lane * 72;
+        for (int c = 0; c < it.nch; ++c) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (!tok[s]) continue;
+                const float *src = slot0 + (size_t)c * C::PSTRIDE + (lane + 32 * s) * 72;
 #pragma unroll
                 for (int m = 0; m < 8; ++m)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        acc[m][k].x += __ldcg(src + m * 8 + 2 * k);
-                        acc[m][k].y += __ldcg(src + m * 8 + 2 * k + 1);
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + m * 8 + 2 * k));
+                        acc[s][m][k].x += v.x;
+                        acc[s][m][k].y += v.y;
                     }
+                if (s == dslot) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    rhs[k].x += __ldcg(src + 64 + 2 * k);
-                    rhs[k].y += __ldcg(src + 64 + 2 * k + 1);
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + 64 + 2 * k));
+                        rhs[k].x += v.x;
+                        rhs[k].y += v.y;
+                    }
                 }
             }
         }
     }
 
     const int r = it.r;
-    const float S = p.tax_S ? p.tax_S[r] : 0.f;
-    if (it.n == 0 && S == 0.f) {
+    const float Sr = p.tax_S ? p.tax_S[r] : 0.f;
+    if (it.n == 0 && Sr == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
             for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = 0.f;
         } else if (lane == 0) {
@@ -1009,78 +1088,193 @@ __global__ void __launch_bounds__(128) k_als_wide_warp(AlsParams p) {
         }
         return;
     }
-    const float diag = p.lam_c + p.lam_n * (float)it.n + p.tau * S;
-    constexpr int MS = C::MS;
-    __syncwarp();
-    if (tok) {
+    const float diag = p.lam_c + p.lam_n * (float)it.n + p.tau * Sr;
+
+    // ---- solve ----------------------------------------------------------------
+    float *PT = sm;                 // [8][LDK] published panel column, transposed
+    float *Ls = PT + 8 * LDK;       // [64] L_JJ, row-major
+    float *invd = Ls + 64;          // [LDK] 1 / L_ii
+    float *bv = invd + LDK;         // [LDK] b -> y -> x
+    int *flag = reinterpret_cast<int *>(bv + LDK);
+    __syncwarp();                   // stages are dead (all cp.async drained)
+    if (dslot >= 0) {
+        // diagonal tile: + (lam_c + lam_n n + tau S) on the diagonal, identity
+        // on the padding rows; its b block (+ tau T)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-            const int row = 8 * tI + m;
+        for (int s = 0; s < S; ++s) {
+            if (s != dslot) continue;
+            const int I = tI[s];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int col = 8 * tJ + 2 * k + hh;
-                    if (col <= row) M[row * MS + col] = hh ? acc[m][k].y : acc[m][k].x;
-                }
-            }
-        }
-        if (tI == tJ) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                M[(8 * tI + 2 * k) * MS + C::LDK] = rhs[k].x;
-                M[(8 * tI + 2 * k + 1) * MS + C::LDK] = rhs[k].y;
+            for (int m = 0; m < 8; ++m) {
+                const int i = 8 * I + m;
+                float &d = tel(acc[s], m, m);
+                d = i < D ? d + diag : 1.f;
+                const float bm = (m & 1) ? rhs[m >> 1].y : rhs[m >> 1].x;
+                bv[i] = i < D ? (p.tax_T ? fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], bm) : bm) : 0.f;
             }
         }
     }
+    if (lane == 0) *flag = 0;
     __syncwarp();
-    for (int i = lane; i < D; i += 32) {
-        M[i * MS + i] += diag;
-        if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
-    }
-    __syncwarp();
-    // right-looking Cholesky: lane owns rows lane and lane + 32
-    for (int j = 0; j < D; ++j) {
-        const float piv = M[j * MS + j];
-        if (!(piv > 0.f) || !isfinite(piv)) {
+
+    for (int J = 0; J < NB8; ++J) {
+        // (1) diagonal lane: factor L_JJ, publish it, forward-solve y_J
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s != dslot || tI[s] != J) continue;
+            float2 (&t)[8][4] = acc[s];
+            bool ok = true;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float d = tel(t, c, c);
+                ok = ok && d > 0.f && d < INFINITY;
+                const float inv = rsqrtf(d), l = d * inv;   // MUFU.RSQ: ~2 ulp
+                tel(t, c, c) = l;
+                invd[8 * J + c] = inv;
+#pragma unroll
+                for (int rr = c + 1; rr < 8; ++rr) tel(t, rr, c) *= inv;
+#pragma unroll
+                for (int c2 = c + 1; c2 < 8; ++c2)
+#pragma unroll
+                    for (int rr = c2; rr < 8; ++rr)
+                        tel(t, rr, c2) = fmaf(-tel(t, rr, c), tel(t, c2, c), tel(t, rr, c2));
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+#pragma unroll
+                for (int n = 0; n < 8; ++n) Ls[m * 8 + n] = n <= m ? tel(t, m, n) : 0.f;
+            float yv[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                float v = bv[8 * J + c];
+#pragma unroll
+                for (int c2 = 0; c2 < c; ++c2) v = fmaf(-tel(t, c, c2), yv[c2], v);
+                yv[c] = v * invd[8 * J + c];
+                bv[8 * J + c] = yv[c];
+            }
+            if (!ok) *flag = 1;
+        }
+        __syncwarp();
+        if (*flag) {
             if (lane == 0) report_fail(p.fail, r);
             return;
         }
-        const float l = sqrtf(piv), inv = 1.f / l;
-        float lij[2] = {0.f, 0.f};
+        // (2) panel: owners publish A_IJ transposed (PT[c][i]); all lanes solve
+        // rows i of the panel against L_JJ in place and update b_i; owners
+        // reload the solved tile (kept for the back substitution)
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-            const int i = lane + 32 * h2;
-            if (i > j && i < D) {
-                lij[h2] = M[i * MS + j] * inv;
-                for (int k = j + 1; k <= i; ++k)
-                    M[i * MS + k] = fmaf(-lij[h2], M[k * MS + j] * inv, M[i * MS + k]);
+        for (int s = 0; s < S; ++s) {
+            if (!tok[s] || tJ[s] != J || tI[s] == J) continue;
+            float2 (&t)[8][4] = acc[s];
+            const int I = tI[s];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                float4 *dst = reinterpret_cast<float4 *>(PT + c * LDK + 8 * I);
+                dst[0] = make_float4(tel(t, 0, c), tel(t, 1, c), tel(t, 2, c), tel(t, 3, c));
+                dst[1] = make_float4(tel(t, 4, c), tel(t, 5, c), tel(t, 6, c), tel(t, 7, c));
+            }
+        }
+        __syncwarp();
+        {
+            float yv[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) yv[c] = bv[8 * J + c];
+            for (int i = 8 * (J + 1) + lane; i < LDK; i += 32) {
+                float x[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) x[c] = PT[c * LDK + i];
+                float bi = bv[i];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float4 l0 = *reinterpret_cast<const float4 *>(Ls + 8 * c);
+                    const float4 l1 = *reinterpret_cast<const float4 *>(Ls + 8 * c + 4);
+                    const float lr[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+                    float v = x[c];
+#pragma unroll
+                    for (int c2 = 0; c2 < c; ++c2) v = fmaf(-x[c2], lr[c2], v);
+                    x[c] = v * invd[8 * J + c];
+                    PT[c * LDK + i] = x[c];
+                    bi = fmaf(-x[c], yv[c], bi);
+                }
+                bv[i] = bi;
             }
         }
         __syncwarp();
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-            const int i = lane + 32 * h2;
-            if (i > j && i < D) M[i * MS + j] = lij[h2];
+        for (int s = 0; s < S; ++s) {
+            if (!tok[s] || tJ[s] != J || tI[s] == J) continue;
+            float2 (&t)[8][4] = acc[s];
+            const int I = tI[s];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float4 v0 = *reinterpret_cast<const float4 *>(PT + c * LDK + 8 * I);
+                const float4 v1 = *reinterpret_cast<const float4 *>(PT + c * LDK + 8 * I + 4);
+                tel(t, 0, c) = v0.x; tel(t, 1, c) = v0.y; tel(t, 2, c) = v0.z; tel(t, 3, c) = v0.w;
+                tel(t, 4, c) = v1.x; tel(t, 5, c) = v1.y; tel(t, 6, c) = v1.z; tel(t, 7, c) = v1.w;
+            }
         }
-        if (lane == 0) M[j * MS + j] = l;
+        // (3) trailing tiles (I, K), J < K <= I:  A_IK -= L_IJ L_KJ^T
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!tok[s] || tJ[s] <= J) continue;
+            const int I = tI[s], K = tJ[s];
+#pragma unroll 2
+            for (int c = 0; c < 8; ++c) {
+                const float4 a0 = *reinterpret_cast<const float4 *>(PT + c * LDK + 8 * I);
+                const float4 a1 = *reinterpret_cast<const float4 *>(PT + c * LDK + 8 * I + 4);
+                const float4 b0 = *reinterpret_cast<const float4 *>(PT + c * LDK + 8 * K);
+                const float4 b1 = *reinterpret_cast<const float4 *>(PT + c * LDK + 8 * K + 4);
+                const float a[8] = {-a0.x, -a0.y, -a0.z, -a0.w, -a1.x, -a1.y, -a1.z, -a1.w};
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    ffma2(acc[s][m][0], a[m], b0.x, b0.y);
+                    ffma2(acc[s][m][1], a[m], b0.z, b0.w);
+                    ffma2(acc[s][m][2], a[m], b1.x, b1.y);
+                    ffma2(acc[s][m][3], a[m], b1.z, b1.w);
+                }
+            }
+        }
+        // the next step's diagonal lane writes Ls / PT only after the barrier
+        // that follows its factorisation, so one __syncwarp per phase suffices
+    }
+
+    // back substitution, block rows bottom-up: x_J = L_JJ^-T b_J, then every
+    // tile (J, K < J) pushes L_JK^T x_J into b_K (one writer per K)
+    for (int J = NB8 - 1; J >= 0; --J) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (s != dslot || tI[s] != J) continue;
+            float2 (&t)[8][4] = acc[s];
+            float xv[8];
+#pragma unroll
+            for (int c = 7; c >= 0; --c) {
+                float v = bv[8 * J + c];
+#pragma unroll
+                for (int c2 = c + 1; c2 < 8; ++c2) v = fmaf(-tel(t, c2, c), xv[c2], v);
+                xv[c] = v * invd[8 * J + c];
+                bv[8 * J + c] = xv[c];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!tok[s] || tI[s] != J || tJ[s] == J) continue;
+            float2 (&t)[8][4] = acc[s];
+            const int K = tJ[s];
+            float xv[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) xv[m] = bv[8 * J + m];
+#pragma unroll
+            for (int n = 0; n < 8; ++n) {
+                float v = bv[8 * K + n];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) v = fmaf(-tel(t, m, n), xv[m], v);
+                bv[8 * K + n] = v;
+            }
+        }
         __syncwarp();
     }
-    for (int j = 0; j < D; ++j) {
-        if (lane == 0) M[j * MS + C::LDK] /= M[j * MS + j];
-        __syncwarp();
-        const float yj = M[j * MS + C::LDK];
-        for (int i = j + 1 + lane; i < D; i += 32) M[i * MS + C::LDK] -= M[i * MS + j] * yj;
-        __syncwarp();
-    }
-    for (int j = D - 1; j >= 0; --j) {
-        if (lane == 0) M[j * MS + C::LDK] /= M[j * MS + j];
-        __syncwarp();
-        const float xj = M[j * MS + C::LDK];
-        for (int i = lane; i < j; i += 32) M[i * MS + C::LDK] -= M[j * MS + i] * xj;
-        __syncwarp();
-    }
-    for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? M[i * MS + C::LDK] : 0.f;
+    for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? bv[i] : 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -1763,18 +1957,18 @@ int launch_cta(const AlsParams &p, cudaStream_t s) {
 }
 
 template <int NB8, bool W>
-int launch_wide_warp(const AlsParams &p, cudaStream_t s) {
-    using C = WideWarpCfg<NB8>;
+int launch_tile_warp(const AlsParams &p, cudaStream_t s) {
+    using C = TileWarpCfg<NB8>;
     const size_t smem = sizeof(float) * C::WARP_FLOATS * C::WARPS;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_wide_warp<NB8, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_tile_warp<NB8, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     const int64_t grid = ceil_div(p.total_items, C::WARPS);
-    if (grid > 0) k_als_wide_warp<NB8, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p);
-    return check_launch("mcf_als_half_step(wide-warp)");
+    if (grid > 0) k_als_tile_warp<NB8, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p);
+    return check_launch("mcf_als_half_step(tile-warp)");
 }
 
 int nb8_for(int D) {
@@ -1796,12 +1990,12 @@ int dispatch(const AlsParams &p, cudaStream_t s) {
         default: break;
     }
     switch (nb8_for(p.D)) {
-        case 4: return launch_wide_warp<4, W>(p, s);
-        case 6: return launch_wide_warp<6, W>(p, s);
-        case 7: return launch_wide_warp<7, W>(p, s);
-        case 8: return launch_cta<8, W>(p, s);
-        case 10: return launch_cta<10, W>(p, s);
-        case 13: return launch_cta<13, W>(p, s);
+        case 4: return launch_tile_warp<4, W>(p, s);
+        case 6: return launch_tile_warp<6, W>(p, s);
+        case 7: return launch_tile_warp<7, W>(p, s);
+        case 8: return launch_tile_warp<8, W>(p, s);
+        case 10: return launch_tile_warp<10, W>(p, s);
+        case 13: return launch_tile_warp<13, W>(p, s);
         default: return launch_cta<16, W>(p, s);
     }
 }
