@@ -1446,7 +1446,7 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     }
     sse = (double)yy - (double)bx - (double)diag * (double)xx;
     reg = (double)lam_row * (double)xx;
-    for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? round22(g[RHS0 + i]) : 0.f;
+    for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? g[RHS0 + i] : 0.f;
 }
 
 __global__ void k_obj_sum(const double *part, int64_t n, double *out) {
@@ -1782,278 +1782,6 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
     }
 }
 
-// ---------------------------------------------------------------------------
-// tensor-core path, D <= 20 (the hot kernel of configs 0-2): warp-level
-// mma.sync on tf32 operands split 3xTF32-style for fp32-level accuracy
-//
-// A warp takes 16 tasks of similar length (same plan as the pair path:
-// hot-row chunks first, then rows by length, groups pulled from an atomic
-// counter) and walks them ONE AFTER ANOTHER in stages of 32 ratings, so a
-// warp never idles on a shorter task of its group.  A stage holds 32
-// partner rows augmented with the rating, X = [x | y] (32 x 24 floats,
-// lane l gathers rating l: its id and rating are one coalesced load), and
-// is consumed as four k-blocks of 8 ratings, each accumulating the lower
-// block triangle of X^T X with m16n8k8 MMAs:
-//     rows 0-15 x cols 0-7, rows 8-23 x cols 0-7 | 8-15 | 16-23
-// which holds A (i, j < D), b (row LDX = y column) and sum y^2 (corner).
-// fp32-level accuracy from tf32 operands: the factor tables carry 22
-// significant bits (round22), so x = big + small with big = x rounded to
-// tf32 and small = x - big is exact in tf32, and
-//     X^T X = big^T big + big^T small + small^T big + small^T small
-// where only the last term (<= 2^-22 relative) is dropped: 3 MMAs per tile.
-// Each lane owns 2 * NB8 values of an 8 x 24 k-block (X[t][8c + g],
-// X[t + 4][8c + g]) which are exactly its A and B fragments: 6
-// conflict-free LDS per k-block, no redundant loads.
-// Partner rows arrive by 16-byte cp.async L stages ahead of the MMAs; ids
-// and ratings one stage earlier into registers.  A finished task's packed
-// [A | b] + sum y^2 goes to the group's solve buffer (or, for a hot chunk,
-// to its partial slot); after the 16 tasks, lanes 0-15 solve one system
-// each (finish_row, the thread-level Cholesky).
-
-template <int NBK>
-struct MmaCfg {
-    using P = PairCfg<NBK>;
-    static constexpr int LDK = P::LDK;          // packed layout of the solve / partial slots
-    static constexpr int TASKS = 16;
-    static constexpr int HALF = 8;              // tasks per solve round (2 rounds per group)
-    static constexpr int BT = 32;               // ratings per stage
-    static constexpr int L = 2;                 // row stages in flight
-    static constexpr int ROWS = 24;             // staged row stride: conflict-free fragments
-    static constexpr int STAGE = BT * ROWS + BT;   // + sqrt(w) per rating
-    static constexpr int GSTRIDE = P::GSTRIDE;
-    static constexpr int SOLVE = HALF * GSTRIDE;
-    static constexpr int WARP_FLOATS = ((L * STAGE + SOLVE) + 31) / 32 * 32;
-    static constexpr int WARPS = 4;
-};
-
-__device__ __forceinline__ void mma_tf32(float (&c)[4], unsigned a0, unsigned a1, unsigned a2,
-                                         unsigned a3, unsigned b0, unsigned b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};\n"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-template <int NBK, int NB8, bool HAS_W>
-__global__ void __launch_bounds__(MmaCfg<NBK>::WARPS * 32, 4) k_als_mma(AlsParams p, PairPlan q) {
-    using C = MmaCfg<NBK>;
-    constexpr int L = C::L, BT = C::BT;
-    constexpr int NT = NB8 == 3 ? 4 : NB8 == 2 ? 2 : 1;   // MMA tiles
-    constexpr int RHS0 = C::LDK * (C::LDK + 1) / 2;
-    constexpr int GRAM = RHS0 + C::LDK;
-    extern __shared__ float4 smem4[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, t = lane & 3;
-    float *wb = reinterpret_cast<float *>(smem4) + warp * C::WARP_FLOATS;
-    float *stages = wb;                    // [L][BT][ROWS] + [L][BT] sqrt(w)
-    float *gbuf = wb + L * C::STAGE;       // [HALF][GSTRIDE]
-    const int D = p.D;
-    const int LDX = 4 * ((D + 3) / 4);     // y column of the staged rows
-    const int nch = LDX / 4;               // 16-byte chunks per partner row
-
-    for (int i = lane; i < L * C::STAGE; i += 32) stages[i] = 0.f;
-    __syncwarp();
-
-    // tile i: A rows 8 ta(i) .. +15, B cols 8 tb(i) .. +7
-    auto ta = [](int i) { return NB8 == 3 && i > 0 ? 1 : 0; };
-    auto tb = [](int i) { return NB8 == 3 ? (i == 0 ? 0 : i - 1) : (NB8 == 2 ? i : 0); };
-    const int64_t n_groups = (q.n_tasks + C::TASKS - 1) / C::TASKS;
-
-    for (;;) {
-        int64_t grp = 0;
-        if (lane == 0) grp = atomicAdd(q.group_counter, 1);
-        grp = __shfl_sync(FULL, grp, 0);
-        if (grp >= n_groups) break;
-        // lane j < 16 holds task j of the group
-        const int64_t task = grp * C::TASKS + lane;
-        int row = 0, slot = -1, n = 0;
-        int64_t k0 = 0;
-        if (lane < C::TASKS && task < q.n_tasks) {
-            row = q.task_row[task];
-            k0 = q.task_k0[task];
-            n = q.task_n[task];
-            slot = q.task_slot[task];
-        }
-        const int ks = (n + BT - 1) / BT;
-        int st0 = ks;   // exclusive prefix of stages over lanes
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, st0, o);
-            if (lane >= o) st0 += y;
-        }
-        const int total = __shfl_sync(FULL, st0, 31);
-        st0 -= ks;
-        const unsigned has = __ballot_sync(FULL, ks > 0);
-
-        // stage s -> task tau, rating offset, task length
-        auto locate = [&](int s, int &tau, int &off, int &tn, int64_t &tk0) {
-            const unsigned m = __ballot_sync(FULL, st0 <= s) & has;
-            tau = 31 - __clz(m);
-            off = BT * (s - __shfl_sync(FULL, st0, tau));
-            tn = __shfl_sync(FULL, n, tau);
-            tk0 = __shfl_sync(FULL, k0, tau);
-        };
-        // lane l's operands of stage s: partner id, rating, weight
-        auto load_ops = [&](int s, int &id, float &y, float &w) {
-            id = -1;
-            y = 0.f;
-            w = 0.f;
-            if (s < total) {
-                int tau, off, tn;
-                int64_t tk0;
-                locate(s, tau, off, tn, tk0);
-                if (off + lane < tn) {   // raw loads: first used one stage later
-                    const int64_t k = tk0 + off + lane;
-                    id = __ldcs(p.idx + k);
-                    y = __ldcs(p.val + k);
-                    w = HAS_W ? __ldcs(p.wts + k) : 1.f;
-                }
-            }
-        };
-        auto issue_rows = [&](int s, int id, float y, float w) {
-            if (s < total) {
-                float *st = stages + (s % L) * C::STAGE;
-                st[lane * C::ROWS + LDX] = id >= 0 ? y - p.y_shift : 0.f;
-                if (HAS_W) st[BT * C::ROWS + lane] = sqrtf(w);
-                const bool ok = id >= 0;
-                const float *src = p.fixed + (size_t)(ok ? id : 0) * p.ld;
-                for (int c = 0; c < nch; ++c)
-                    cp_async16(st + lane * C::ROWS + 4 * c, src + 4 * c, ok ? 16 : 0);
-            }
-            cp_async_commit();
-        };
-
-        float acc[NT][4], acx[NT][4];   // big^T big | cross terms (independent chains)
-#pragma unroll
-        for (int i = 0; i < NT; ++i)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[i][k] = acx[i][k] = 0.f;
-
-        int nid;
-        float ny, nw;
-        for (int j = 0; j < L; ++j) {
-            load_ops(j, nid, ny, nw);
-            issue_rows(j, nid, ny, nw);
-        }
-        load_ops(L, nid, ny, nw);
-        // solve round h: lanes j < HALF finish task HALF h + j from buffer slot j
-        double o_sse = 0.0, o_reg = 0.0;
-        auto solve_half = [&](int h) {
-            __syncwarp();
-            const int src = C::HALF * h + (lane & (C::HALF - 1));
-            const int srow = __shfl_sync(FULL, row, src), sslot = __shfl_sync(FULL, slot, src);
-            const int sn = __shfl_sync(FULL, n, src), sks = __shfl_sync(FULL, ks, src);
-            const bool live = lane < C::HALF && grp * C::TASKS + src < q.n_tasks;
-            if (live) {
-                float *my_g = gbuf + lane * C::GSTRIDE;
-                const float yy = sks > 0 ? my_g[GRAM] : 0.f;
-                if (sslot >= 0) {
-                    float *dst = p.partials + (size_t)sslot * (GRAM + 1);
-                    for (int i = 0; i < GRAM; ++i) dst[i] = my_g[i];
-                    dst[GRAM] = yy;
-                } else {
-                    double a1, a2;
-                    finish_row<C::LDK>(p, my_g, srow, sn, yy, a1, a2);
-                    o_sse += a1;
-                    o_reg += a2;
-                }
-            }
-            __syncwarp();
-        };
-        int cur_tau = -1, cur_end = 0;
-        const int s_split = __shfl_sync(FULL, st0, C::HALF);   // first stage of task HALF
-        int s = 0;
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-        const int s_stop = h == 0 ? s_split : total;
-        for (; s < s_stop; ++s) {
-            cp_async_wait<L - 1>();
-            __syncwarp();
-            if (s >= cur_end) {   // first stage of the next task
-                int off, tn;
-                int64_t tk0;
-                locate(s, cur_tau, off, tn, tk0);
-                cur_end = __shfl_sync(FULL, st0 + ks, cur_tau);
-            }
-            const float *st = stages + (s % L) * C::STAGE;
-#pragma unroll
-            for (int kb = 0; kb < BT / 8; ++kb) {
-                const float *r0 = st + (8 * kb + t) * C::ROWS + g;
-                const float *r1 = r0 + 4 * C::ROWS;
-                float v[3][2];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    v[c][0] = c < NB8 ? r0[8 * c] : 0.f;
-                    v[c][1] = c < NB8 ? r1[8 * c] : 0.f;
-                }
-                if (HAS_W) {
-                    const float w0 = st[BT * C::ROWS + 8 * kb + t], w1 = st[BT * C::ROWS + 8 * kb + t + 4];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        v[c][0] *= w0;
-                        v[c][1] *= w1;
-                    }
-                }
-                // big = round-to-nearest tf32 (integer add + mask), small = x - big:
-                // exact for the 22-bit tables (round22), 3 instructions per value
-                unsigned hi[3][2], lo[3][2];
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        hi[c][h] = (__float_as_uint(v[c][h]) + 0x1000u) & 0xffffe000u;
-                        lo[c][h] = __float_as_uint(v[c][h] - __uint_as_float(hi[c][h]));
-                    }
-#pragma unroll
-                for (int i = 0; i < NT; ++i) {
-                    const int a2 = ta(i), b = tb(i);
-                    mma_tf32(acc[i], hi[a2][0], hi[a2 + 1][0], hi[a2][1], hi[a2 + 1][1], hi[b][0], hi[b][1]);
-                    mma_tf32(acx[i], hi[a2][0], hi[a2 + 1][0], hi[a2][1], hi[a2 + 1][1], lo[b][0], lo[b][1]);
-                    mma_tf32(acx[i], lo[a2][0], lo[a2 + 1][0], lo[a2][1], lo[a2 + 1][1], hi[b][0], hi[b][1]);
-                }
-            }
-            if (s + 1 == cur_end) {
-                // task done: scatter the lower triangle, b and sum y^2 into its packed slot
-                float *gs = gbuf + (cur_tau & (C::HALF - 1)) * C::GSTRIDE;
-#pragma unroll
-                for (int i = 0; i < NT; ++i) {
-                    const int a2 = ta(i), b = tb(i);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int r = 8 * a2 + g + (e >= 2 ? 8 : 0);
-                        const int cc = 8 * b + 2 * t + (e & 1);
-                        const float val = acc[i][e] + acx[i][e];
-                        acc[i][e] = acx[i][e] = 0.f;
-                        if (NB8 == 3 && i == 0 && e >= 2) continue;   // rows 8-15: tile 1
-                        if (r < D && cc <= r) gs[pidx(r, cc)] = val;
-                        else if (r == LDX && cc < D) gs[RHS0 + cc] = val;
-                        else if (r == LDX && cc == LDX) gs[GRAM] = val;
-                    }
-                }
-            }
-            __syncwarp();   // stage s % L is refilled now
-            issue_rows(s + L, nid, ny, nw);
-            load_ops(s + L + 1, nid, ny, nw);
-        }
-        if (h == 1) cp_async_wait<0>();
-        solve_half(h);   // the next half's gathers stay in flight meanwhile
-        }
-        if (p.obj_partial) {   // fixed-order butterfly: deterministic per group
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                o_sse += __shfl_xor_sync(FULL, o_sse, o);
-                o_reg += __shfl_xor_sync(FULL, o_reg, o);
-            }
-            if (lane == 0) {
-                p.obj_partial[2 * grp] = o_sse;
-                p.obj_partial[2 * grp + 1] = o_reg;
-            }
-        }
-        __syncwarp();
-    }
-}
-
 // Hot rows: one warp per row sums its chunk partials in chunk order, then
 // the warp solves cooperatively (lane i owns row i of A, right-looking
 // Cholesky with shuffles).
@@ -2132,7 +1860,7 @@ __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
         const float xj = __shfl_sync(FULL, b, j2);
         if (lane < j2) b = fmaf(-G[pidx(j2, lane)], xj, b);
     }
-    if (lane < p.ld) orow[lane] = lane < D ? round22(b) : 0.f;
+    if (lane < p.ld) orow[lane] = lane < D ? b : 0.f;
     if (p.obj_partial) {
         float bx = lane < D ? b0 * b : 0.f, xx = lane < D ? b * b : 0.f;
 #pragma unroll
@@ -2351,40 +2079,13 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     return check_launch("mcf_als_half_step(pair)");
 }
 
-template <int NBK, int NB8, bool W>
-int launch_mma(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
-    using C = MmaCfg<NBK>;
-    const size_t smem = sizeof(float) * (size_t)C::WARP_FLOATS * C::WARPS;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_als_mma<NBK, NB8, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = true;
-    }
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_mma<NBK, NB8, W>, C::WARPS * 32,
-                                                  smem);
-    const int64_t groups = ceil_div(q.n_tasks, C::TASKS);
-    const int64_t want = ceil_div(groups, C::WARPS);
-    const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_mma<NBK, NB8, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
-    if (q.n_heavy > 0)
-        k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
-    if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
-    return check_launch("mcf_als_half_step(mma)");
-}
-
-// D <= 20: tensor-core Gram (mma.sync tf32, hi/lo split).  NB8 = 8-column
-// blocks of the staged [x | y] row (y at column 4 ceil(D / 4)).
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int nb = (p.D + 3) / 4;
-    if (nb <= 1) return launch_mma<1, 1, W>(p, q, s);
-    if (nb == 2) return launch_mma<3, 2, W>(p, q, s);
-    if (nb == 3) return launch_mma<3, 2, W>(p, q, s);
-    return launch_mma<5, 3, W>(p, q, s);
+    if (nb <= 1) return launch_pair<1, W, false>(p, q, s);
+    if (nb <= 3) return launch_pair<3, W, false>(p, q, s);
+    if (nb == 5) return launch_pair<5, W, true>(p, q, s);
+    return launch_pair<5, W, false>(p, q, s);
 }
 
 size_t pair_gram(int D) {   // partial slot floats: packed [A | b] + sum w y^2

@@ -43,14 +43,6 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Factor tables of the D <= 20 path are stored with 22 significant bits
-// (round to nearest, |error| <= 2^-23 relative): then x = big + small with
-// big = x rounded to tf32 and small = x - big is an exact split into two
-// tf32 values, which the tensor-core Gram relies on.
-__device__ __forceinline__ float round22(float x) {
-    return __uint_as_float((__float_as_uint(x) + 2u) & ~3u);
-}
-
 // Device-wide exclusive scan (3 phases, recursive on block sums).
 // in/out may alias.  Returns bytes of temp needed when temp == nullptr.
 template <typename T>

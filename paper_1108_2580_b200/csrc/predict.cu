@@ -115,7 +115,7 @@ __global__ void k_add_gathered(const float *A, const float *B, const int32_t *ma
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = e / ld;
         const int m = map[r];
-        out[e] = round22(m >= 0 ? A[e] + B[(size_t)m * ld + (e - r * ld)] : A[e]);
+        out[e] = m >= 0 ? A[e] + B[(size_t)m * ld + (e - r * ld)] : A[e];
     }
 }
 

@@ -181,9 +181,6 @@ class AlsEngine:
             dst[:, : self.D].copy_(t, non_blocking=True)
             if self.ld > self.D:
                 dst[:, self.D:].zero_()
-            # 22 significant bits, as every device producer of factor rows
-            # stores them (csrc/common.cuh round22): exact tf32 big/small split
-            dst.view(torch.int32).add_(2).bitwise_and_(-4)
 
     def factors(self):
         return self.P[:, : self.D], self.Q[:, : self.D]
