@@ -79,9 +79,7 @@ int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t n_list, in
                  void *stream);
 /* Bytes of half-step workspace: n_list row counters + `slots` partial
  * Grams at dimension D (slots = plan_info[3] when D <= 20, else
- * plan_info[0]: for 29 <= D <= 104 without weights every work item
- * publishes its Gram from the tensor-core kernel; plan_info[1] suffices for
- * the other D > 20 paths). */
+ * plan_info[1]). */
 size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
 
 /* Solve every planned row r exactly (Cholesky of the D x D system):

@@ -44,7 +44,6 @@ namespace mcf {
 namespace {
 
 constexpr int BATCH = 32;
-int nb8_for(int D);
 
 struct AlsParams {
     const int64_t *ptr;
@@ -910,39 +909,7 @@ __device__ __forceinline__ float &tel(float2 (&t)[8][4], int m, int n) {
     return (n & 1) ? t[m][n >> 1].y : t[m][n >> 1].x;
 }
 
-// Adds one published partial (T8 tiles x 72 floats, tile order of the lanes)
-// into the lane's register tiles / rhs block.
-template <int NB8>
-__device__ __forceinline__ void add_partial(const float *part, int lane, const bool *tok, int dslot,
-                                            float2 (&acc)[TileWarpCfg<NB8>::S][8][4], float2 (&rhs)[4]) {
-    constexpr int S = TileWarpCfg<NB8>::S;
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-        if (!tok[s]) continue;
-        const float *src = part + (lane + 32 * s) * 72;
-#pragma unroll
-        for (int m = 0; m < 8; ++m)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + m * 8 + 2 * k));
-                acc[s][m][k].x += v.x;
-                acc[s][m][k].y += v.y;
-            }
-        if (s == dslot) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + 64 + 2 * k));
-                rhs[k].x += v.x;
-                rhs[k].y += v.y;
-            }
-        }
-    }
-}
-
-// FROM_PARTIALS: the Gram of every work item was published by the tensor-core
-// kernel (k_gram_tc); one warp per ROW sums its items' partials in item order
-// and solves.
-template <int NB8, bool HAS_W, bool FROM_PARTIALS>
+template <int NB8, bool HAS_W>
 __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
     using C = TileWarpCfg<NB8>;
     constexpr int S = C::S, LDK = C::LDK, BT = C::BT;
@@ -950,7 +917,8 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float *sm = reinterpret_cast<float *>(smem4) + warp * C::WARP_FLOATS;
     const int64_t item = (int64_t)blockIdx.x * C::WARPS + warp;
-    if (item >= (FROM_PARTIALS ? (int64_t)p.n_list : p.total_items)) return;
+    if (item >= p.total_items) return;
+    const ItemInfo it = item_info(p, item);
     const int D = p.D;
     const int nb4_real = (D + 3) / 4;
 
@@ -975,19 +943,6 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
 
-    int r;
-    int64_t n_row;
-    if (FROM_PARTIALS) {
-        const int j = (int)item;
-        r = p.row_list ? p.row_list[j] : p.row_lo + j;
-        n_row = p.ptr[r + 1] - p.ptr[r];
-        const int first = p.item_off[j], nch = p.item_off[j + 1] - first;
-        for (int c = 0; c < nch; ++c)
-            add_partial<NB8>(p.partials + (size_t)(first + c) * C::PSTRIDE, lane, tok, dslot, acc, rhs);
-    } else {
-    const ItemInfo it = item_info(p, item);
-    r = it.r;
-    n_row = it.n;
     // ---- Gram ---------------------------------------------------------------
     auto ld = [&](int64_t b, int &id, float &y, float &w) {
         const int64_t kk = it.k0 + b * BT + lane;
@@ -1098,14 +1053,34 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
                 for (int k = 0; k < 4; ++k) acc[s][m][k] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
-        for (int c = 0; c < it.nch; ++c)
-            add_partial<NB8>(slot0 + (size_t)c * C::PSTRIDE, lane, tok, dslot, acc, rhs);
+        for (int c = 0; c < it.nch; ++c) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (!tok[s]) continue;
+                const float *src = slot0 + (size_t)c * C::PSTRIDE + (lane + 32 * s) * 72;
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + m * 8 + 2 * k));
+                        acc[s][m][k].x += v.x;
+                        acc[s][m][k].y += v.y;
+                    }
+                if (s == dslot) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + 64 + 2 * k));
+                        rhs[k].x += v.x;
+                        rhs[k].y += v.y;
+                    }
+                }
+            }
+        }
     }
 
-    }   // !FROM_PARTIALS
-
+    const int r = it.r;
     const float Sr = p.tax_S ? p.tax_S[r] : 0.f;
-    if (n_row == 0 && Sr == 0.f) {
+    if (it.n == 0 && Sr == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
             for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = 0.f;
         } else if (lane == 0) {
@@ -1113,7 +1088,7 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
         }
         return;
     }
-    const float diag = p.lam_c + p.lam_n * (float)n_row + p.tau * Sr;
+    const float diag = p.lam_c + p.lam_n * (float)it.n + p.tau * Sr;
 
     // ---- solve ----------------------------------------------------------------
     float *PT = sm;                 // [8][LDK] published panel column, transposed
@@ -1951,320 +1926,6 @@ __global__ void k_pair_fill(const int64_t *ptr, const int32_t *row_list, int32_t
 // ---------------------------------------------------------------------------
 // dispatch
 
-// ---------------------------------------------------------------------------
-// tensor-core Gram, 29 <= D <= 104, unweighted (configs 3 and 4): tcgen05,
-// warp-specialised and pipelined across work items
-//
-// Per work item (a row, or a <= chunk-long piece of a hot row) the CTA
-// accumulates C = hi^T hi + hi^T (2 lo) for X = [x | y] (ratings x F
-// columns: partner row, the rating at column Y = 4 ceil(D/4), zeros to F),
-// hi = x rounded to tf32 (integer add + mask), lo = x - hi; then
-//     G = (C + C^T) / 2 = hi^T hi + hi^T lo + lo^T hi
-// (fp32-level: only lo^T lo, <= 2^-22 relative, is dropped).  One TMEM
-// accumulator per item, two in flight.
-//   warps 0-3  producers: per 32-rating stage each thread gathers its share
-//              of the partner rows with 4-byte cp.async straight into the
-//              K-major no-swizzle canonical layout (core matrix = 8 feature
-//              rows x 4 ratings; the same tile is A = X^T and B = X), waits
-//              for its own copies, splits its elements in place (hi) and
-//              into the lo buffer, fence.proxy.async, arrives on full[s].
-//   warp 4     MMA issuer: waits full[s], 4 k-groups x 2 tcgen05.mma
-//              (kind::tf32, M x F x 8), tcgen05.commit -> empty[s]; after
-//              the item's last stage commit -> accfull[a].
-//   warps 5-8  epilogue: wait accfull[a], tcgen05.ld the accumulator rows
-//              into a shared transpose buffer, release the accumulator
-//              (accempty[a]), write G symmetrised as the item's partial in the
-//              tile-warp lane order (T8 tiles x 72 floats, b in the diagonal
-//              tiles' rhs slots, rows / columns >= D zeroed).
-// k_als_tile_warp<..., FROM_PARTIALS> then sums each row's item partials in
-// item order and solves (deterministic).  Items are dealt statically
-// (blockIdx.x + j gridDim.x) so every role walks the same sequence.
-
-template <int M, int F>
-struct GramWsCfg {
-    static constexpr int BT = 32;                  // ratings per stage (4 k-groups of 8)
-    static constexpr int FG = F / 8;               // 8-feature core-matrix rows
-    static constexpr int LBO = FG * 128;           // bytes between 4-rating chunks
-    static constexpr int BUF = (BT / 4) * LBO;     // one operand buffer
-    static constexpr int SLACK = (M / 8 > FG ? (M / 8 - FG) * 128 : 0) + 128;   // A over-read
-    static constexpr int BUFS = BUF + SLACK;
-    static constexpr int NST = 3;                  // stages in flight
-    static constexpr int PL = 2;                   // row copies issued ahead (< NST)
-    static constexpr int PRODUCERS = 128, EPILOGUE = 128;
-    static constexpr int THREADS = PRODUCERS + 32 + EPILOGUE;
-    static constexpr int ACC_COLS = M == 64 ? 64 : 128;
-    static constexpr int TMEM_COLS = 2 * ACC_COLS;   // two items in flight
-    static constexpr int TSTRIDE = F + 1;
-    // staging rows (bulk copies land here, row-major): stride = 8 or 24 mod 32
-    // floats so the transposing reads of 4 ratings x 8 features are conflict-free
-    static constexpr int RSTR = F + ((F % 32 == 8 || F % 32 == 24) ? 0 : 8);
-    static constexpr int STG = BT * RSTR * 4;
-    static constexpr int OPER = NST * 2 * BUFS;      // hi | lo per stage
-    static constexpr int STAGING = NST * STG;
-    static constexpr int TRANS = ((F * TSTRIDE * 4) + 127) / 128 * 128;
-    static constexpr int SMEM = OPER + STAGING + TRANS + 1024;
-    static_assert(F % 8 == 0 && F <= M, "F columns");
-    static_assert(M == 64 ? F % 8 == 0 : F % 16 == 0, "UMMA N granularity");
-};
-
-__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-    // no swizzle, K-major, descriptor version 1 (sm_100)
-    return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
-}
-
-__device__ __forceinline__ void umma_tf32(uint32_t taddr, uint64_t da, uint64_t db, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(taddr),
-        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mbar_wait_bounded(unsigned bar, unsigned parity) {
-    for (long i = 0; !mbar_try(bar, parity); ++i)
-        if (i > (1l << 31)) __trap();   // a lost arrival must fail, not hang the GPU
-}
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <int M, int F, int NB8>
-__global__ void __launch_bounds__(GramWsCfg<M, F>::THREADS, 1) k_gram_ws(AlsParams p) {
-    using C = GramWsCfg<M, F>;
-    constexpr int BT = C::BT, LBO = C::LBO, NST = C::NST;
-    constexpr int PSTRIDE = NB8 * (NB8 + 1) / 2 * 72;
-    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(F >> 3) << 17) |
-                               ((uint32_t)(M >> 4) << 24);   // f32 <- tf32 x tf32, both K-major
-    static_assert(F >= 8 * NB8, "tile range inside the Gram");
-    extern __shared__ __align__(1024) unsigned char gsm_raw[];
-    unsigned char *gsm = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) unsigned long long full[NST], empty[NST], landed[NST], accfull[2], accempty[2];
-    __shared__ uint32_t tmem_base;
-    __shared__ float sy[NST][BT];
-    __shared__ int snv[NST];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int D = p.D, Y = 4 * ((D + 3) / 4);
-    const uint32_t gsm_s = static_cast<uint32_t>(__cvta_generic_to_shared(gsm));
-    float *T = reinterpret_cast<float *>(gsm + C::OPER + C::STAGING);   // [F][TSTRIDE]
-    const uint32_t stg_s = gsm_s + (uint32_t)C::OPER;
-    auto bar_s = [](unsigned long long *b) { return static_cast<unsigned>(__cvta_generic_to_shared(b)); };
-
-    for (int i = tid; i < C::OPER / 4; i += C::THREADS) reinterpret_cast<float *>(gsm)[i] = 0.f;
-    if (tid == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(bar_s(&full[s]), C::PRODUCERS);
-            mbar_init(bar_s(&empty[s]), 1);
-            mbar_init(bar_s(&landed[s]), 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(bar_s(&accfull[a]), 1);
-            mbar_init(bar_s(&accempty[a]), C::EPILOGUE);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 4) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base))),
-                     "n"(C::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tmem_base;
-
-    auto stages_of = [&](const ItemInfo &it) {
-        const int n = (int)(it.k1 - it.k0);
-        return n > 0 ? (n + BT - 1) / BT : 1;   // an empty row still gets a (zero) Gram
-    };
-
-    if (warp < 4) {
-        // ------------------------------------------------------------ producers
-        // warp 0 lane k issues the bulk copy of rating k's partner row PL
-        // stages ahead (one TMA request per row, completion on landed[s]);
-        // all 128 threads then transpose the staged rows into the K-major
-        // hi / lo operand tiles, one 4-rating x 8-feature core matrix per
-        // warp step (conflict-free both ways), and hand the stage to the MMA.
-        constexpr int PL = C::PL;
-        struct Cursor {
-            int64_t item;
-            ItemInfo it;
-            int s, nst;
-        };
-        auto start = [&](Cursor &c, int64_t item) {
-            c.item = item;
-            c.s = 0;
-            if (item < p.total_items) {
-                c.it = item_info(p, item);
-                c.nst = stages_of(c.it);
-            }
-        };
-        auto advance = [&](Cursor &c) {
-            if (++c.s == c.nst) start(c, c.item + gridDim.x);
-        };
-        const uint32_t row_bytes = (uint32_t)p.ld * 4u;
-        auto issue = [&](const Cursor &c, int g) {   // warp 0 only
-            const int st = g % NST;
-            const int64_t kk = c.it.k0 + (int64_t)c.s * BT + lane;
-            const int64_t rem = c.it.k1 - (c.it.k0 + (int64_t)c.s * BT);
-            const int nv = rem < BT ? (int)rem : BT;
-            const bool ok = lane < nv;
-            sy[st][lane] = ok ? __ldcs(p.val + kk) - p.y_shift : 0.f;
-            snv[st] = nv;
-            const unsigned lb = bar_s(&landed[st]);
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb),
-                             "r"(row_bytes * (uint32_t)max(nv, 0))
-                             : "memory");
-            __syncwarp();
-            if (ok) {
-                const int id = __ldcs(p.idx + kk);
-                const uint32_t dst = stg_s + (uint32_t)(st * C::STG + lane * C::RSTR * 4);
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                    "l"(p.fixed + (size_t)id * p.ld), "r"(row_bytes), "r"(lb)
-                    : "memory");
-            }
-        };
-        Cursor ci, cp;   // issue cursor (PL ahead), process cursor
-        start(ci, blockIdx.x);
-        start(cp, blockIdx.x);
-        int gi = 0;
-        if (warp == 0)
-            for (; gi < PL && ci.item < p.total_items; ++gi) {
-                issue(ci, gi);
-                advance(ci);
-            }
-        gi = __shfl_sync(FULL, gi, 0);
-        for (int g = 0; cp.item < p.total_items; ++g) {
-            const int st = g % NST;
-            if (warp == 0 && ci.item < p.total_items) {   // copies of stage g + PL
-                issue(ci, gi);
-                advance(ci);
-                ++gi;
-            }
-            mbar_wait_bounded(bar_s(&landed[st]), (g / NST) & 1);           // rows in smem
-            mbar_wait_bounded(bar_s(&empty[st]), ((g / NST) & 1) ^ 1);      // MMA done with st
-            const float *stg = reinterpret_cast<const float *>(gsm + C::OPER + st * C::STG);
-            float *hi = reinterpret_cast<float *>(gsm + (2 * st) * C::BUFS);
-            float *lo = reinterpret_cast<float *>(gsm + (2 * st + 1) * C::BUFS);
-            const int nv = snv[st];
-            const int kl = lane & 3, fl = lane >> 2;
-            for (int cm = warp; cm < 8 * C::FG; cm += 4) {   // core matrix (kq, fq)
-                const int kq = cm / C::FG, fq = cm - kq * C::FG;
-                const int k = 4 * kq + kl, f = 8 * fq + fl;
-                float x = 0.f;
-                if (k < nv) x = f < Y ? (f < D ? stg[k * C::RSTR + f] : 0.f) : (f == Y ? sy[st][k] : 0.f);
-                const float h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
-                const int o = (kq * LBO + fq * 128) / 4 + lane;   // (f%8)*4 + (k%4) == lane
-                hi[o] = h;
-                lo[o] = 2.f * (x - h);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(bar_s(&full[st]));
-            named_bar(2, C::PRODUCERS);   // staging st and sy / snv[st] are reused PL stages on
-            advance(cp);
-        }
-    } else if (warp == 4) {
-        // ------------------------------------------------------------ MMA issuer
-        int g = 0, j = 0;
-        for (int64_t item = blockIdx.x; item < p.total_items; item += gridDim.x, ++j) {
-            const ItemInfo it = item_info(p, item);
-            const int nst = stages_of(it);
-            const int a = j & 1;
-            const uint32_t tacc = tmem + (uint32_t)(a * C::ACC_COLS);
-            mbar_wait_bounded(bar_s(&accempty[a]), ((j >> 1) & 1) ^ 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            for (int s = 0; s < nst; ++s, ++g) {
-                const int st = g % NST;
-                mbar_wait_bounded(bar_s(&full[st]), (g / NST) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lane == 0) {
-                    const uint32_t hs = gsm_s + (uint32_t)((2 * st) * C::BUFS);
-                    const uint32_t ls = gsm_s + (uint32_t)((2 * st + 1) * C::BUFS);
-#pragma unroll
-                    for (int kg = 0; kg < BT / 8; ++kg) {
-                        const uint32_t off = (uint32_t)(kg * 2 * LBO);
-                        const uint64_t dh = umma_sdesc(hs + off, LBO, 128);
-                        const uint64_t dl = umma_sdesc(ls + off, LBO, 128);
-                        umma_tf32(tacc, dh, dh, IDESC, (s == 0 && kg == 0) ? 0u : 1u);
-                        umma_tf32(tacc, dh, dl, IDESC, 1u);
-                    }
-                    asm volatile(
-                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                            bar_s(&empty[st]))
-                        : "memory");
-                    if (s == nst - 1)
-                        asm volatile(
-                            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                bar_s(&accfull[a]))
-                            : "memory");
-                }
-                __syncwarp();
-            }
-        }
-    } else {
-        // ------------------------------------------------------------ epilogue
-        const int q4 = warp & 3;   // TMEM subpartition of this warp (warps 5..8 -> 1,2,3,0)
-        const int row = M == 128 ? 32 * q4 + lane : (lane < 16 ? 16 * q4 + lane : -1);
-        const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
-        int j = 0;
-        for (int64_t item = blockIdx.x; item < p.total_items; item += gridDim.x, ++j) {
-            const int a = j & 1;
-            const uint32_t tacc = tmem + (uint32_t)(a * C::ACC_COLS);
-            mbar_wait_bounded(bar_s(&accfull[a]), (j >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-            for (int jc = 0; jc < F / 8; ++jc) {
-                uint32_t v[8];
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                               "=r"(v[6]), "=r"(v[7])
-                             : "r"(tacc + lane_off + 8 * jc));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row >= 0 && row < F)
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) T[row * C::TSTRIDE + 8 * jc + e] = __uint_as_float(v[e]);
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(bar_s(&accempty[a]));   // the accumulator may be reused
-            named_bar(1, C::EPILOGUE);
-            // G = (C + C^T) / 2 -> partial tiles; thread = one row of G
-            float *part = p.partials + (size_t)item * PSTRIDE;
-            if (row >= 0 && row < 8 * NB8) {
-                const int I = row >> 3;
-                for (int jc = 0; jc <= I; ++jc) {
-                    const int q = (NB8 - jc - 1) * (NB8 - jc) / 2 + (I - jc);
-                    float o[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int jj = 8 * jc + e;
-                        const float gv = 0.5f * (T[row * C::TSTRIDE + jj] + T[jj * C::TSTRIDE + row]);
-                        o[e] = (row < D && jj < D && jj <= row) ? gv : 0.f;
-                    }
-                    float4 *dst = reinterpret_cast<float4 *>(part + q * 72 + (row & 7) * 8);
-                    dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-                    dst[1] = make_float4(o[4], o[5], o[6], o[7]);
-                }
-                const int qd = (NB8 - I - 1) * (NB8 - I) / 2;
-                part[qd * 72 + 64 + (row & 7)] =
-                    row < D ? 0.5f * (T[row * C::TSTRIDE + Y] + T[Y * C::TSTRIDE + row]) : 0.f;
-            }
-            named_bar(1, C::EPILOGUE);   // T is rewritten by the next item
-        }
-    }
-    __syncthreads();
-    if (warp == 4)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                     "n"(C::TMEM_COLS));
-}
-
 template <int NB, bool W>
 int launch_warp(const AlsParams &p, cudaStream_t s) {
     using C = WarpCfg<NB>;
@@ -2301,59 +1962,13 @@ int launch_tile_warp(const AlsParams &p, cudaStream_t s) {
     const size_t smem = sizeof(float) * C::WARP_FLOATS * C::WARPS;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_tile_warp<NB8, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_tile_warp<NB8, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     const int64_t grid = ceil_div(p.total_items, C::WARPS);
-    if (grid > 0) k_als_tile_warp<NB8, W, false><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p);
+    if (grid > 0) k_als_tile_warp<NB8, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p);
     return check_launch("mcf_als_half_step(tile-warp)");
-}
-
-template <int M, int F, int NB8>
-int launch_gram_tc(const AlsParams &p, cudaStream_t s) {
-    if (4 * ((p.D + 3) / 4) + 1 > F || nb8_for(p.D) != NB8) {
-        set_error("mcf_als_half_step: internal tensor-core configuration mismatch");
-        return MCF_E_UNSUPPORTED;
-    }
-    using C = GramWsCfg<M, F>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_gram_ws<M, F, NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        cudaFuncSetAttribute(k_als_tile_warp<NB8, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(float) * TileWarpCfg<NB8>::WARP_FLOATS * TileWarpCfg<NB8>::WARPS));
-        attr = true;
-    }
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram_ws<M, F, NB8>, C::THREADS, C::SMEM);
-    per_sm = std::max(1, std::min(per_sm, 512 / C::TMEM_COLS));   // TMEM columns per SM
-    const int64_t grid = std::min<int64_t>(p.total_items, (int64_t)sms * per_sm);
-    if (grid > 0) k_gram_ws<M, F, NB8><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(p);
-    using T = TileWarpCfg<NB8>;
-    const int64_t g2 = ceil_div(p.n_list, T::WARPS);
-    if (g2 > 0)
-        k_als_tile_warp<NB8, false, true><<<(unsigned)g2, T::WARPS * 32,
-                                            sizeof(float) * T::WARP_FLOATS * T::WARPS, s>>>(p);
-    return check_launch("mcf_als_half_step(gram-tc)");
-}
-
-// tensor-core Gram for 29 <= D <= 104 without per-observation weights
-bool use_gram_tc(int D, bool weighted) { return !weighted && D >= 29 && D <= 104; }
-
-int dispatch_gram_tc(const AlsParams &p, cudaStream_t s) {
-    // F >= max(Y + 1, 8 NB8) with Y = 4 ceil(D/4) the rating column; M = 64 when F fits
-    const int Y1 = 4 * ((p.D + 3) / 4) + 1;
-    switch (nb8_for(p.D)) {
-        case 4: return launch_gram_tc<64, 40, 4>(p, s);
-        case 6: return Y1 <= 48 ? launch_gram_tc<64, 48, 6>(p, s) : launch_gram_tc<64, 56, 6>(p, s);
-        case 7: return Y1 <= 56 ? launch_gram_tc<64, 56, 7>(p, s) : launch_gram_tc<64, 64, 7>(p, s);
-        case 8: return launch_gram_tc<128, 80, 8>(p, s);
-        case 10: return launch_gram_tc<128, 96, 10>(p, s);
-        default: return launch_gram_tc<128, 112, 13>(p, s);
-    }
 }
 
 int nb8_for(int D) {
@@ -2644,13 +2259,5 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
         return wts ? dispatch_pair<true>(p, q, s) : dispatch_pair<false>(p, q, s);
     }
     if (total_items == 0) return MCF_OK;
-    if (use_gram_tc(D, wts != nullptr)) {
-        // every work item publishes its Gram: total_items partial slots
-        if (ws_bytes < fixed_part + sizeof(float) * (size_t)total_items * pstride_of(D)) {
-            set_error("mcf_als_half_step: workspace too small (size it with slots = plan_info[0])");
-            return MCF_E_WORKSPACE;
-        }
-        return dispatch_gram_tc(p, s);
-    }
     return wts ? dispatch<true>(p, s) : dispatch<false>(p, s);
 }

@@ -133,9 +133,7 @@ class LayoutSolver:
                 self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
             fail = self.fail
         buf, info, rl, n_list = lay.plan(rows, rows_key, self.chunk)
-        # D <= 20: hot-chunk slots; D > 20: one slot per work item (the
-        # tensor-core Gram path publishes every item's Gram)
-        slots = info[3] if self.D <= 20 else info[0]
+        slots = info[3] if self.D <= 20 else info[1]
         k = (id(lay), rows_key)
         need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
         if k not in self._ws or self._ws[k].numel() < need:
