@@ -8,7 +8,8 @@
  * negative MCF_E* code with a message readable through mcf_last_error().
  * Calls are safe from any host thread on their own stream with disjoint
  * outputs.  Factor matrices are row-major [rows][ld] float32 with
- * ld = mcf_factor_ld(D) = round_up(D, 4) and zero padding columns.
+ * ld = mcf_factor_ld(D) = round_up(D, 4) for D <= 4, else round_up(D, 8)
+ * (whole 32-byte sectors), and zero padding columns.
  *
  * Reference operator each entry point replaces (paths relative to
  * /root/reference/pkg/src/multicf):

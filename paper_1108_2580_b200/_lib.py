@@ -11,7 +11,8 @@ import os
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcf.so")
+# MCF_LIB: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("MCF_LIB") or os.path.join(_HERE, "libmcf.so")
 _LIB = None
 
 c_int, c_i32, c_i64, c_f32, c_size = ctypes.c_int, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
@@ -70,4 +71,4 @@ def ptr(t) -> int | None:
 
 
 def factor_ld(D: int) -> int:
-    return (D + 3) // 4 * 4
+    return (D + 3) // 4 * 4 if D <= 4 else (D + 7) // 8 * 8

@@ -35,6 +35,7 @@
 // threads, CTA-cooperative Cholesky (correctness path for configs 3/4; the
 // tensor-core path for D >= 64 replaces it).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -1301,33 +1302,49 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
 // solves.
 
 template <int NBK>
-struct PairCfg {
+struct PairGeom {
     static_assert(NBK % 2 == 1, "odd block count");
     static constexpr int LDK = 4 * NBK;
-    static constexpr int R = 2;                    // ratings per pipeline stage per pair
-    static constexpr int ROW = LDK + 4;            // x | y, w, pad, pad
-    // pair slot stride: (SLOT / 4) % 8 == 6 puts the 4 pairs of a quarter-warp
-    // on disjoint bank groups for the two consecutive blocks they read
-    static constexpr int SLOT = ((R * ROW / 4 + 7 - 6) / 8 * 8 + 6) * 4;
-    static constexpr int PAIRS = 16;
-    static constexpr int STAGE_BYTES = PAIRS * SLOT * 4;
-    static constexpr int NS = 7;                   // pipeline stages (6 stages = 12 ratings of lead)
     static constexpr int HALF = (NBK + 1) / 2;
     static constexpr int NACC = HALF * 10 + ((NBK - 1) / 2) * HALF * 16 + HALF * 4;
     static constexpr int RHS0 = LDK * (LDK + 1) / 2;
     static constexpr int GRAM = RHS0 + LDK;        // packed lower + rhs
     static constexpr int PSTR = GRAM + 1;          // partial slot: + sum w y^2
     static constexpr int GSTRIDE = GRAM | 1;       // odd stride: conflict-free per-lane rows
+};
+
+// smallest 16-byte unit count >= u that is 2 or 6 mod 8: the 4 pairs of a
+// quarter-warp then start on disjoint bank groups (units 0,2,4,6 or 0,6,4,2)
+// and the two lanes of a pair (adjacent blocks) fill the odd ones
+__host__ __device__ constexpr int slot_units(int u) {
+    return (u % 8 == 2 || u % 8 == 6) ? u : slot_units(u + 1);
+}
+
+template <int NBK, int R_>
+struct PairCfg : PairGeom<NBK> {
+    using G = PairGeom<NBK>;
+    static constexpr int LDK = G::LDK;
+    static constexpr int R = R_;                   // ratings per pipeline stage per pair
+    // pair slot of one stage: R partner rows | R ratings | R weights
+    static constexpr int RROW = LDK;
+    static constexpr int YOFF = R * RROW;
+    static constexpr int WOFF = YOFF + R;
+    static constexpr int SLOT = 4 * slot_units((WOFF + R + 3) / 4);   // floats
+    static constexpr int PAIRS = 16;
+    static constexpr int STAGE_BYTES = PAIRS * SLOT * 4;
+    static constexpr int NS = R == 2 ? 7 : 4;      // pipeline stages (lead = (NS-1)*R ratings)
     static constexpr int RING_BYTES = NS * STAGE_BYTES;
-    static constexpr int SOLVE_BYTES = PAIRS * GSTRIDE * 4;
+    static constexpr int SOLVE_BYTES = PAIRS * G::GSTRIDE * 4;
     // the gather ring and the solve buffer are never live at the same time
     static constexpr int RING_AREA =
         ((RING_BYTES > SOLVE_BYTES ? RING_BYTES : SOLVE_BYTES) + 127) / 128 * 128;
-    static constexpr int NR = 8;                   // id ring entries (>= NS)
-    static constexpr int WARP_BYTES = RING_AREA + PAIRS * NR * R * 4;
+    static constexpr int NR = R == 2 ? 8 : 4;      // id ring entries (>= NS - 1 ahead)
+    static constexpr int IDSTR = NR * R + 4;       // ints per pair (+4: pairs on distinct banks)
+    static constexpr int WARP_BYTES = RING_AREA + PAIRS * IDSTR * 4;
     static constexpr int WARPS = 4;
     static constexpr int MIN_CTAS = 2;             // 8 warps / SM (register bound: 138 accumulators)
     static constexpr int PF = 64;                  // L2 prefetch distance (ratings)
+    static_assert(NR >= NS - 1 && (R == 2 || R == 4), "pair ring geometry");
 };
 
 __device__ __forceinline__ constexpr int pidx(int i, int j) { return i * (i + 1) / 2 + j; }
@@ -1608,17 +1625,19 @@ struct PairAcc {
 
 // Each lane pair gathers its own partner rows with cp.async (16 B blocks
 // split between the two lanes, zero-fill past the task end) and the ratings
-// with 4 B cp.async, R = 2 ratings per pipeline stage; every lane's copies
-// are tracked by the stage's mbarrier (cp.async.mbarrier.arrive.noinc, 32
+// with 4 B cp.async, R ratings per pipeline stage; every lane's copies are
+// tracked by the stage's mbarrier (cp.async.mbarrier.arrive.noinc, 32
 // arrivals), so a stage is waited on individually, NS-2 stages after its
 // issue.  Partner ids travel the same way: issuing stage s also cp.asyncs
 // the ids of stage s+NS-1 into a small per-pair ring in shared memory, and
 // they are read (after stage s's barrier has been waited on) when stage
 // s+NS-1 is issued -- no register ever waits on an in-flight load.
-template <int NBK, bool HAS_W, bool FULLBLK>
-__global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CTAS) k_als_pair(AlsParams p, PairPlan q) {
-    using C = PairCfg<NBK>;
-    constexpr int R = C::R;
+// L2 policy: the once-read idx/val/weight streams are loaded evict_first,
+// so they do not push the fixed factor rows (50-80 MB at config 1) out of L2.
+template <int NBK, int R, bool HAS_W, bool FULLBLK>
+__global__ void __launch_bounds__(PairCfg<NBK, R>::WARPS * 32, PairCfg<NBK, R>::MIN_CTAS)
+k_als_pair(AlsParams p, PairPlan q) {
+    using C = PairCfg<NBK, R>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[C::WARPS][C::NS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1629,13 +1648,15 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
     float *my_g = reinterpret_cast<float *>(wbase) + pair * C::GSTRIDE;  // aliases the ring
     const unsigned my_slot_s = wbase_s + pair * C::SLOT * 4;
     const float *my_slot = reinterpret_cast<const float *>(wbase) + pair * C::SLOT;
-    // ids ring: [PAIRS][NR][R] int32 after the gather ring / solve area
-    int *ring_ids = reinterpret_cast<int *>(wbase + C::RING_AREA) + pair * C::NR * C::R;
-    const unsigned ring_ids_s = wbase_s + C::RING_AREA + pair * C::NR * C::R * 4;
+    // ids ring: [PAIRS][IDSTR] int32 after the gather ring / solve area
+    const int *ring_ids = reinterpret_cast<const int *>(wbase + C::RING_AREA) + pair * C::IDSTR;
+    const unsigned ring_ids_s = wbase_s + C::RING_AREA + pair * C::IDSTR * 4;
     const int nb_real = FULLBLK ? NBK : (p.D + 3) / 4;
     int boff[NBK];   // float offset of register block b inside a row
 #pragma unroll
     for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
+    uint64_t pol_stream;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < C::NS; ++s) mbar_init(bar0 + 8 * s, 32);
@@ -1675,38 +1696,45 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
         acc.zero();
 
         const unsigned gbase = gst;
-        auto ld_idx = [&](int k) -> int { return k < n ? idxp[k] : -1; };
-        // gathers of stage s (ratings R*s .. R*s+R-1): partner ids in ia/ib;
+        // gathers of stage s (ratings R*s .. R*s+R-1, partner ids in ids[]);
         // also brings the ids of stage s+NS-1 into the ring
-        auto issue = [&](int s, int ia, int ib) {
+        auto issue = [&](int s, const int (&ids)[R]) {
             const unsigned gs = gbase + (unsigned)s;
             const unsigned ss = my_slot_s + (gs % C::NS) * C::STAGE_BYTES;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int col = r == 0 ? ia : ib;
+                const int col = ids[r];
                 const bool ok = col >= 0;
                 const float *src = p.fixed + (size_t)(ok ? col : 0) * p.ld;
-                const unsigned rs = ss + r * C::ROW * 4;
+                const unsigned rs = ss + r * C::RROW * 4;
+                // lanes h = 0, 1 copy adjacent 16-byte blocks in one instruction
+                // (one 32-byte sector when the row is sector-aligned)
 #pragma unroll
                 for (int b = h; b < NBK; b += 2)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(rs + 16 * b),
-                                 "l"(src + 4 * b), "r"((ok && (FULLBLK || b < nb_real)) ? 16 : 0));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
+                                 ::"r"(rs + 16 * b), "l"(src + 4 * b),
+                                 "r"((ok && (FULLBLK || b < nb_real)) ? 16 : 0));
             }
-            // lane h brings the rating (and weight) of row h ...
-            const int k = R * s + h;
-            const bool okv = k < n;
-            const unsigned ys = ss + h * C::ROW * 4 + 4 * C::LDK;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(ys),
-                         "l"(valp + (okv ? k : 0)), "r"(okv ? 4 : 0));
-            if (HAS_W)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(ys + 4),
-                             "l"(wtsp + (okv ? k : 0)), "r"(okv ? 4 : 0));
-            // ... and the partner id of row h of stage s + NS - 1
-            const int ku = R * (s + C::NS - 1) + h;
-            const bool oku = ku < n;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
-                         ::"r"(ring_ids_s + 4 * (R * ((gs + C::NS - 1) % C::NR) + h)),
-                         "l"(idxp + (oku ? ku : 0)), "r"(oku ? 4 : 0));
+            // lane h brings the ratings (and weights) of rows h, h+2, ... and
+            // the partner ids of the same rows of stage s + NS - 1
+            const unsigned ids_dst = ring_ids_s + 4 * (R * ((gs + C::NS - 1) % C::NR));
+#pragma unroll
+            for (int r = h; r < R; r += 2) {
+                const int k = R * s + r;
+                const bool okv = k < n;
+                asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
+                             ::"r"(ss + 4 * (C::YOFF + r)), "l"(valp + (okv ? k : 0)),
+                             "r"(okv ? 4 : 0), "l"(pol_stream));
+                if (HAS_W)
+                    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
+                                 ::"r"(ss + 4 * (C::WOFF + r)), "l"(wtsp + (okv ? k : 0)),
+                                 "r"(okv ? 4 : 0), "l"(pol_stream));
+                const int ku = R * (s + C::NS - 1) + r;
+                const bool oku = ku < n;
+                asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
+                             ::"r"(ids_dst + 4 * r), "l"(idxp + (oku ? ku : 0)), "r"(oku ? 4 : 0),
+                             "l"(pol_stream));
+            }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar0 + 8 * (gs % C::NS))
                          : "memory");
             const int pf = R * s + C::PF;
@@ -1717,19 +1745,27 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
             const unsigned gs = gbase + (unsigned)t;
             mbar_wait(bar0 + 8 * (gs % C::NS), (gs / C::NS) & 1);
             const float *sl = my_slot + (gs % C::NS) * (C::STAGE_BYTES / 4);
+            float ys[R];
+            if constexpr (R == 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(sl + C::YOFF);
+                ys[0] = v.x; ys[1] = v.y; ys[2] = v.z; ys[3] = v.w;
+            } else {
+                const float2 v = *reinterpret_cast<const float2 *>(sl + C::YOFF);
+                ys[0] = v.x; ys[1] = v.y;
+            }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const float *rw = sl + r * C::ROW;
+                const float *rw = sl + r * C::RROW;
                 float4 xr[NBK];
 #pragma unroll
                 for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(rw + boff[b]);
-                const float y = rw[C::LDK] - p.y_shift;
+                const float y = ys[r] - p.y_shift;
                 float4 xa[NBK];
 #pragma unroll
                 for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
                 float wy = y;
                 if (HAS_W) {
-                    const float w = rw[C::LDK + 1];
+                    const float w = sl[C::WOFF + r];
                     wy = w * y;
 #pragma unroll
                     for (int b = 0; b < NBK; ++b) {
@@ -1742,14 +1778,29 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
         };
 
         // prologue: stages 0 .. NS-2 with ids loaded directly
-        for (int s = 0; s < C::NS - 1 && s < nst; ++s) issue(s, ld_idx(R * s), ld_idx(R * s + 1));
+        for (int s = 0; s < C::NS - 1 && s < nst; ++s) {
+            int ids[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) ids[r] = R * s + r < n ? idxp[R * s + r] : -1;
+            issue(s, ids);
+        }
         for (int t = 0; t < nst; ++t) {
             consume(t);   // waits stage t: the ids of stage t+NS-1 have landed too
             const int s = t + C::NS - 1;
             if (s < nst) {
-                const int2 ids = *reinterpret_cast<const int2 *>(ring_ids + R * ((gbase + s) % C::NR));
+                const int *rid = ring_ids + R * ((gbase + s) % C::NR);
+                int ids[R];
+                if constexpr (R == 4) {
+                    const int4 v = *reinterpret_cast<const int4 *>(rid);
+                    ids[0] = v.x; ids[1] = v.y; ids[2] = v.z; ids[3] = v.w;
+                } else {
+                    const int2 v = *reinterpret_cast<const int2 *>(rid);
+                    ids[0] = v.x; ids[1] = v.y;
+                }
                 // a zero-filled id (past the task end) reads as 0: mask by the task length
-                issue(s, R * s < n ? ids.x : -1, R * s + 1 < n ? ids.y : -1);
+#pragma unroll
+                for (int r = 0; r < R; ++r) ids[r] = R * s + r < n ? ids[r] : -1;
+                issue(s, ids);
             }
         }
         gst = gbase + (unsigned)nst;
@@ -1787,7 +1838,7 @@ __global__ void __launch_bounds__(PairCfg<NBK>::WARPS * 32, PairCfg<NBK>::MIN_CT
 // Cholesky with shuffles).
 template <int NBK>
 __global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
-    using C = PairCfg<NBK>;
+    using C = PairGeom<NBK>;
     constexpr int LDK = C::LDK;
     __shared__ float g[4][C::GSTRIDE + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -2053,39 +2104,52 @@ PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_
 
 bool use_pair(int D) { return D <= 20; }
 
-template <int NBK, bool W, bool FB>
+template <int NBK, int R, bool W, bool FB>
 int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
-    using C = PairCfg<NBK>;
+    using C = PairCfg<NBK, R>;
     const size_t smem = (size_t)C::WARP_BYTES * C::WARPS;
 
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_pair<NBK, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_pair<NBK, R, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, W, FB>, C::WARPS * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, R, W, FB>, C::WARPS * 32,
                                                   smem);
     const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
     const int64_t want = ceil_div(groups, C::WARPS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_pair<NBK, W, FB><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
+    if (grid > 0) k_als_pair<NBK, R, W, FB><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
         k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
     if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
     return check_launch("mcf_als_half_step(pair)");
 }
 
+// ratings per pipeline stage of the D <= 20 pair kernel (MCF_PAIR_R=2 selects
+// the 2-rating / 7-stage variant; default 4 ratings / 4 stages)
+int pair_r() {
+    static int r = [] {
+        const char *e = getenv("MCF_PAIR_R");
+        return (e && atoi(e) == 2) ? 2 : 4;
+    }();
+    return r;
+}
+
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int nb = (p.D + 3) / 4;
-    if (nb <= 1) return launch_pair<1, W, false>(p, q, s);
-    if (nb <= 3) return launch_pair<3, W, false>(p, q, s);
-    if (nb == 5) return launch_pair<5, W, true>(p, q, s);
-    return launch_pair<5, W, false>(p, q, s);
+    if (nb <= 1) return launch_pair<1, 4, W, false>(p, q, s);
+    if (nb <= 3) return launch_pair<3, 4, W, false>(p, q, s);
+    if (nb == 5) {
+        if (pair_r() == 2) return launch_pair<5, 2, W, true>(p, q, s);
+        return launch_pair<5, 4, W, true>(p, q, s);
+    }
+    return launch_pair<5, 4, W, false>(p, q, s);
 }
 
 size_t pair_gram(int D) {   // partial slot floats: packed [A | b] + sum w y^2

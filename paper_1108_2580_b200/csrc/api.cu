@@ -23,5 +23,7 @@ int check_launch(const char *where) { return cuda_status(cudaGetLastError(), whe
 
 extern "C" int mcf_version(void) { return 1; }
 extern "C" const char *mcf_last_error(void) { return mcf::g_last_error.c_str(); }
-extern "C" int mcf_factor_ld(int D) { return (D + 3) / 4 * 4; }
+// rows of more than 4 floats are padded to whole 32-byte L2 sectors: a
+// sector-aligned row is gathered with the fewest sector requests
+extern "C" int mcf_factor_ld(int D) { return D <= 4 ? (D + 3) / 4 * 4 : (D + 7) / 8 * 8; }
 extern "C" int mcf_max_dim(void) { return 128; }

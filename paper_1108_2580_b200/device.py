@@ -7,8 +7,8 @@ HBM layout (per GPU):
     [n+1], idx int32 [nnz] (the partner id), val float32 [nnz] (the rating),
     perm int32 [nnz] (record index, kept only when per-observation weights
     must be permuted);  8 B per rating per layout.
-  * factor tables P [U][ld], Q [I][ld] float32, ld = round_up(D, 4) with zero
-    padding so every partner row is a whole number of 16-byte vectors.
+  * factor tables P [U][ld], Q [I][ld] float32, ld = mcf_factor_ld(D) (round_up(D, 8)
+    for D > 4) with zero padding, so every partner row is sector-aligned.
   * per (layout, row set) a work plan (int32 chunk offsets, partial-Gram
     slot offsets, item->row map) and the partial-Gram workspace.
 """

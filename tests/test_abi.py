@@ -36,7 +36,7 @@ def test_host_only_queries():
         pytest.skip("libmcf.so not built")
     L = _lib.lib()
     assert L.mcf_version() == 1
-    assert [L.mcf_factor_ld(d) for d in (1, 4, 10, 20, 100)] == [4, 4, 12, 20, 100]
+    assert [L.mcf_factor_ld(d) for d in (1, 4, 10, 20, 100)] == [4, 4, 16, 24, 104]
     assert L.mcf_max_dim() == 128
     assert L.mcf_csr_workspace_bytes(1000, 10) > 8 * 1000
     assert L.mcf_als_workspace_bytes(10, 0, 20) >= 40
