@@ -50,6 +50,7 @@ from paper_1108_2580_b200 import synth  # noqa: E402
 
 PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
 TRAFFIC = os.path.join(REPO, "profiles", "roofline_traffic.json")
+FP32 = os.path.join(REPO, "profiles", "fp32_peak.json")   # tools/micro/fp32_peak on this pool
 METRIC = "ALS ratings/sec per full sweep"
 
 
@@ -112,6 +113,49 @@ def algorithmic(nnz, U, I, D):
     f_users = nnz * (D * D + 3 * D) + f_rows(U)
     return {"bytes_sweep": b_items + b_users, "flops_sweep": f_items + f_users,
             "bytes_launch_mean": (b_items + b_users) / 2, "flops_launch_mean": (f_items + f_users) / 2}
+
+
+def fp32_peak():
+    """Measured FFMA2 peak of this pool's B200 (tools/micro/fp32_peak, kept in
+    profiles/fp32_peak.json); nominal 148 SM x 128 FMA x 2 x 1.965 GHz else."""
+    try:
+        with open(FP32) as fh:
+            return float(json.load(fh)["fp32_tflops"]), "measured (tools/micro/fp32_peak)"
+    except Exception:
+        return 74.4, "nominal"
+
+
+def kernel_name(D: int) -> str:
+    if D <= 20:
+        return "k_als_pair<5,4> (fused Gram + lam*n + Cholesky + solve; + k_als_heavy for hot rows)"
+    if D <= 28:
+        return "k_als_warp (4x4 register tiles, warp Cholesky)"
+    if D <= 104:
+        return "k_als_tile_warp (warp per row, 8x8 register tiles, blocked register Cholesky)"
+    return "k_als_cta"
+
+
+def roofline_for(D, bytes_launch, flops_launch, launch_s, traffic=None, kernel=None):
+    """roofline time = max(bytes / HBM, flops / FP32 peak) per
+    launch; the bound is whichever is larger and `achieved` is reported in
+    that resource's unit (GB/s or TFLOP/s), the other view beside it."""
+    hbm, hbm_kind = peaks()
+    f32, f32_kind = fp32_peak()
+    t_hbm = bytes_launch / (hbm * 1e9)
+    t_f32 = flops_launch / (f32 * 1e12)
+    gbs = bytes_launch / launch_s / 1e9
+    tfs = flops_launch / launch_s / 1e12
+    if t_hbm >= t_f32:
+        r = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+             "peak_kind": hbm_kind, "achieved_tflops": tfs, "fp32_peak_tflops": f32}
+    else:
+        r = {"bound": "fp32", "achieved": tfs, "peak": f32, "unit": "TFLOP/s", "frac": tfs / f32,
+             "peak_kind": f32_kind, "achieved_gbs": gbs, "hbm_peak_gbs": hbm}
+    r.update({"traffic": traffic, "kernel": kernel or kernel_name(D),
+              "roofline_ms_per_launch": 1e3 * max(t_hbm, t_f32),
+              "algorithmic_bytes_per_launch": bytes_launch,
+              "algorithmic_flops_per_launch": flops_launch})
+    return r
 
 
 def launches_per_sweep(eng) -> int:
@@ -288,23 +332,17 @@ def run_ours(args, rank, world):
     value = nnz / (ms_per_step / 1000.0)
 
     alg = algorithmic(nnz, cfg.users, cfg.items, cfg.D)
-    hbm, peak_kind = peaks()
     mean_launch_s = statistics.mean(half_ms) / 1000.0
-    achieved = alg["bytes_launch_mean"] / mean_launch_s / 1e9
     traffic = None
     if os.path.exists(TRAFFIC):
         try:
             traffic = json.load(open(TRAFFIC)).get(cfg.name)
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "k_als_pair<5> (fused Gram + lam*n + Cholesky + solve; + k_als_heavy for hot rows)",
-                "launch_ms": {"items": statistics.mean(half_ms[0::2]),
-                              "users": statistics.mean(half_ms[1::2])},
-                "achieved_tflops": alg["flops_launch_mean"] / mean_launch_s / 1e12,
-                "algorithmic_bytes_per_launch": alg["bytes_launch_mean"],
-                "algorithmic_flops_per_launch": alg["flops_launch_mean"]}
+    roofline = roofline_for(cfg.D, alg["bytes_launch_mean"], alg["flops_launch_mean"],
+                            mean_launch_s, traffic)
+    roofline["launch_ms"] = {"items": statistics.mean(half_ms[0::2]),
+                             "users": statistics.mean(half_ms[1::2])}
 
     # held-out RMSE after the timed sweeps (sanity, not timed)
     rm = float(eng.rmse(wl.valid_users, wl.valid_items, wl.valid_scores).item())
@@ -419,8 +457,12 @@ def run_mfitr(args, cfg, wl, t_gen):
     alg = algorithmic(nnz, cfg.users, cfg.items, cfg.D)
     E = wl.graph.num_edges
     extra = E * (12 + 8 * cfg.D) + 4 * cfg.items * (cfg.D + 1)
-    hbm, peak_kind = peaks()
-    achieved = (alg["bytes_sweep"] + extra) / (ms / 1000.0) / 1e9
+    extra_f = 2 * E * (2 * cfg.D + 1)
+    # per sweep (one step = 4 item layers + users; the layers share the launch budget)
+    roof = roofline_for(cfg.D, alg["bytes_sweep"] + extra, alg["flops_sweep"] + extra_f,
+                        ms / 1000.0, kernel=kernel_name(cfg.D) + " per item layer + users; "
+                        "k_tax_terms per layer")
+    roof["per"] = "sweep"
     art = torch.as_tensor(wl.graph.artist_array(cfg.items).astype(np.int32), device=dev)
     _, sse = eng.predict(wl.valid_users, wl.valid_items, wl.valid_scores, want_pred=False,
                          mu=r.global_mean, art=art, Q_a=torch.zeros_like(eng.Q))
@@ -434,9 +476,7 @@ def run_mfitr(args, cfg, wl, t_gen):
                        "nnz_train": nnz, "D": cfg.D, "lambda2": cfg.lam,
                        "lambda3": cfg.tax_weight, "lambda4": cfg.tax_weight,
                        "edges": E, "step": "one ALS-MFITR sweep: 4 item layers + users"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "k_als_pair<5> per layer + k_tax_terms"},
+            "roofline": roof,
             "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clk.summary(),
             "valid_rmse_after": rm, "layout_build_s": t_layout, "datagen_s": t_gen}
     print(json.dumps(line), flush=True)
@@ -484,9 +524,10 @@ def run_sharded(args, rank, world, cfg, wl, t_gen):
     half_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(2 * args.steps)]
     D = cfg.D
     local_bytes = (run.nnz_local["items"] + run.nnz_local["users"]) * (4 * D + 8) / 2
+    local_flops = (run.nnz_local["items"] + run.nnz_local["users"]) * (D * D + 3 * D) / 2
     mean_launch_s = max_over_ranks(statistics.mean(half_ms), world) / 1000.0
-    hbm, peak_kind = peaks()
-    achieved = local_bytes / mean_launch_s / 1e9
+    roof = roofline_for(D, local_bytes, local_flops, mean_launch_s,
+                        kernel=kernel_name(D) + " per rank (local shard) + all-gather")
     P, Q = run.factors()
     from paper_1108_2580_b200.device import AlsEngine, DeviceRatings
     z = torch.zeros(0, dtype=torch.int32, device=dev)
@@ -504,9 +545,7 @@ def run_sharded(args, rank, world, cfg, wl, t_gen):
                            "l2": "inputs > L2; no flush",
                            "parallelism": f"rows sharded over {world} GPUs (nnz-balanced), "
                                           "opposite factor replicated"},
-                "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                             "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
-                             "kernel": "k_als_pair<5> per rank (local shard) + all-gather"},
+                "roofline": roof,
                 "cpu_baseline": None, "e2e": None, "gpu_launches": 4 * args.steps,
                 "clocks": clk.summary(), "valid_rmse_after": rm, "layout_build_s": t_layout,
                 "datagen_s": t_gen}
