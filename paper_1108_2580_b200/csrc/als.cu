@@ -36,7 +36,6 @@
 // tensor-core path for D >= 64 replaces it).
 #include <algorithm>
 #include <cstdlib>
-#include <cstring>
 #include <string>
 
 #include "common.cuh"
@@ -1834,340 +1833,6 @@ k_als_pair(AlsParams p, PairPlan q) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialised pair kernel (D <= 20): per CTA (one per SM) 8 consumer
-// warps (two warpgroups, setmaxnreg 232) run only the Gram FMAs and the
-// solve; 4 producer warps (one warpgroup, setmaxnreg 40) issue every gather,
-// producer warp w serving consumers 2w and 2w+1.  Each SM sub-partition
-// holds 2 consumers + 1 producer (2 x 224 + 56 <= 512 registers per lane).  Per consumer: an NS-stage ring of R-rating stages (layout as
-// PairCfg), full barriers (32 cp.async noinc arrivals from the producer
-// lanes), empty barriers (consumer lane 0), a group descriptor published by
-// the producer (desc barrier) and a group-done barrier (the solve aliases the
-// ring, so the producer starts a consumer's next group only after it).  The
-// producer keeps each consumer's state in registers (statically unrolled
-// over the 8 consumers) and never blocks on one consumer: it polls the
-// barriers and moves on.  Partner ids run NS-1 stages ahead through a small
-// per-pair smem ring exactly as in k_als_pair; a group's first NS-1 stages of
-// ids are fetched as soon as the producer takes the group (pro barrier).
-template <int NBK, int R>
-struct WsCfg : PairGeom<NBK> {
-    using G = PairGeom<NBK>;
-    static constexpr int LDK = G::LDK;
-    static constexpr int CONS = 8;                 // consumer warps per CTA
-    static constexpr int PAIRS = 16;
-    static constexpr int YOFF = R * LDK;
-    static constexpr int WOFF = YOFF + R;
-    static constexpr int SLOT = 4 * slot_units((WOFF + R + 3) / 4);   // floats
-    static constexpr int STAGE_BYTES = PAIRS * SLOT * 4;
-    static constexpr int NS = 4;
-    static constexpr int RING_BYTES = NS * STAGE_BYTES;
-    static constexpr int SOLVE_BYTES = PAIRS * G::GSTRIDE * 4;
-    static constexpr int RING_AREA =
-        ((RING_BYTES > SOLVE_BYTES ? RING_BYTES : SOLVE_BYTES) + 127) / 128 * 128;
-    static constexpr int NR = 4;                   // id ring entries
-    static constexpr int IDSTR = NR * R + 4;
-    static constexpr int CONS_BYTES = RING_AREA + PAIRS * IDSTR * 4;
-    static constexpr int DESC_INTS = 4 * PAIRS + 4;   // {row, n, slot, -} per pair + {grp, nst}
-    static constexpr int SMEM = CONS * CONS_BYTES + CONS * DESC_INTS * 4;
-    static constexpr int PROD = 4;                 // producer warps (one warpgroup)
-    static constexpr int PER = CONS / PROD;        // consumers per producer
-    static constexpr int THREADS = (CONS + PROD) * 32;
-    static constexpr int PF = 64;
-    static_assert(NS == 4 && NR == 4 && (R == 2 || R == 4), "ring geometry");
-};
-
-struct WsBars {
-    unsigned long long full[8][4], empty[8][4], desc[8], done[8], pro[8];
-};
-
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-template <int NBK, int R, bool HAS_W, bool FULLBLK>
-__global__ void __launch_bounds__(WsCfg<NBK, R>::THREADS, 1)
-k_als_pair_ws(AlsParams p, PairPlan q) {
-    using C = WsCfg<NBK, R>;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    __shared__ __align__(8) WsBars B;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pair = lane >> 1, h = lane & 1;
-    const unsigned smem_s = static_cast<unsigned>(__cvta_generic_to_shared(smem_raw));
-    const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(&B.full[0][0]));
-    const unsigned empty0 = static_cast<unsigned>(__cvta_generic_to_shared(&B.empty[0][0]));
-    const unsigned desc0 = static_cast<unsigned>(__cvta_generic_to_shared(&B.desc[0]));
-    const unsigned done0 = static_cast<unsigned>(__cvta_generic_to_shared(&B.done[0]));
-    const unsigned pro0 = static_cast<unsigned>(__cvta_generic_to_shared(&B.pro[0]));
-    int *desc_mem = reinterpret_cast<int *>(smem_raw + C::CONS * C::CONS_BYTES);
-    if (threadIdx.x == 0) {
-        for (int c = 0; c < C::CONS; ++c) {
-            for (int s = 0; s < C::NS; ++s) {
-                mbar_init(full0 + 8 * (c * 4 + s), 32);
-                mbar_init(empty0 + 8 * (c * 4 + s), 1);
-            }
-            mbar_init(desc0 + 8 * c, 1);
-            mbar_init(done0 + 8 * c, 1);
-            mbar_init(pro0 + 8 * c, 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int64_t n_groups = (q.n_tasks + C::PAIRS - 1) / C::PAIRS;
-
-    if (warp >= C::CONS) {
-        // ------------------------------------------------------------ producer
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-        const int cbase0 = (warp - C::CONS) * C::PER;
-        uint64_t pol_stream;
-        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
-        const int nb_real = FULLBLK ? NBK : (p.D + 3) / 4;
-        struct St {
-            int64_t k0;
-            int n, nst, s, grp, row, slot, phase, pub;
-            unsigned gbase;
-        } S[C::PER];
-#pragma unroll
-        for (int c = 0; c < C::PER; ++c) {
-            S[c].k0 = 0; S[c].n = 0; S[c].nst = 0; S[c].s = 0; S[c].grp = 0;
-            S[c].row = 0; S[c].slot = -1; S[c].phase = 0; S[c].pub = 0; S[c].gbase = 0;
-        }
-        int live = C::PER;
-        while (live > 0) {
-            bool moved = false;
-#pragma unroll
-            for (int cc = 0; cc < C::PER; ++cc) {
-                St &st = S[cc];
-                const int c = cbase0 + cc;
-                const unsigned ring_s = smem_s + c * C::CONS_BYTES;
-                const unsigned my_slot_s = ring_s + pair * C::SLOT * 4;
-                const unsigned ids_s = ring_s + C::RING_AREA + pair * C::IDSTR * 4;
-                if (st.phase == 0) {   // take the next group, fetch its first ids
-                    int g = 0;
-                    if (lane == 0) g = atomicAdd(q.group_counter, 1);
-                    g = __shfl_sync(FULL, g, 0);
-                    st.gbase += (unsigned)st.nst;
-                    st.grp = g;
-                    if (g >= n_groups) {
-                        st.phase = 3;
-                        st.nst = 0;
-                    } else {
-                        const int64_t task = (int64_t)g * C::PAIRS + pair;
-                        st.row = 0; st.slot = -1; st.n = 0; st.k0 = 0;
-                        if (task < q.n_tasks) {
-                            st.row = q.task_row[task];
-                            st.k0 = q.task_k0[task];
-                            st.n = q.task_n[task];
-                            st.slot = q.task_slot[task];
-                        }
-                        int nmax = st.n;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, o));
-                        st.nst = (nmax + R - 1) / R;
-                        st.s = 0;
-                        const int32_t *idxp = p.idx + st.k0;
-                        if (st.n > 0)
-                            for (int o = 0; o < min(st.n, C::PF); o += 32)
-                                prefetch_l2(h ? (const void *)(p.val + st.k0 + o) : (const void *)(idxp + o));
-                        // ids of stages 0 .. NS-2 (rows h, h+2 of each) -> ring
-#pragma unroll
-                        for (int j = 0; j < C::NS - 1; ++j) {
-                            if (j < st.nst) {
-#pragma unroll
-                                for (int r = h; r < R; r += 2) {
-                                    const int k = R * j + r;
-                                    const bool ok = k < st.n;
-                                    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                                                 ::"r"(ids_s + 4 * (R * ((st.gbase + j) % C::NR) + r)),
-                                                 "l"(idxp + (ok ? k : 0)), "r"(ok ? 4 : 0), "l"(pol_stream));
-                                }
-                            }
-                        }
-                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(pro0 + 8 * c)
-                                     : "memory");
-                        st.phase = 1;
-                    }
-                    moved = true;
-                }
-                if (st.phase == 1 || st.phase == 3) {   // publish once the consumer is done
-                    const bool ready = mbar_try(done0 + 8 * c, (st.pub & 1) ^ 1) &&
-                                       (st.phase == 3 || mbar_try(pro0 + 8 * c, (st.pub & 1)));
-                    if (ready) {
-                        int *d = desc_mem + c * C::DESC_INTS;
-                        if (h == 0) *reinterpret_cast<int4 *>(d + 4 * pair) = make_int4(st.row, st.n, st.slot, 0);
-                        if (lane == 0)
-                            *reinterpret_cast<int4 *>(d + 4 * C::PAIRS) =
-                                make_int4(st.phase == 3 ? -1 : st.grp, st.nst, 0, 0);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(desc0 + 8 * c);
-                        st.pub += 1;
-                        if (st.phase == 3) {
-                            st.phase = 4;
-                            --live;
-                        } else {
-                            st.phase = 2;
-                        }
-                        moved = true;
-                    }
-                }
-                if (st.phase == 2) {   // issue stages while the ring has room
-#pragma unroll 1
-                    for (int k = 0; k < C::NS && st.s < st.nst; ++k) {
-                        const unsigned gs = st.gbase + (unsigned)st.s;
-                        const unsigned slot = gs % C::NS;
-                        if (!mbar_try(empty0 + 8 * (c * 4 + slot), ((gs / C::NS) & 1) ^ 1)) break;
-                        if (st.s >= C::NS - 1) {   // ids came with stage s - NS + 1
-                            const unsigned gp = gs - (C::NS - 1);
-                            if (!mbar_try(full0 + 8 * (c * 4 + gp % C::NS), (gp / C::NS) & 1)) break;
-                        }
-                        const int *rid = reinterpret_cast<const int *>(smem_raw + (ids_s - smem_s)) +
-                                         R * (gs % C::NR);
-                        int ids[R];
-                        if constexpr (R == 4) {
-                            const int4 v = *reinterpret_cast<const int4 *>(rid);
-                            ids[0] = v.x; ids[1] = v.y; ids[2] = v.z; ids[3] = v.w;
-                        } else {
-                            const int2 v = *reinterpret_cast<const int2 *>(rid);
-                            ids[0] = v.x; ids[1] = v.y;
-                        }
-                        const int s = st.s, n = st.n;
-                        const unsigned ss = my_slot_s + slot * C::STAGE_BYTES;
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const bool ok = R * s + r < n;
-                            const float *src = p.fixed + (size_t)(ok ? ids[r] : 0) * p.ld;
-                            const unsigned rs = ss + r * C::LDK * 4;
-#pragma unroll
-                            for (int b = h; b < NBK; b += 2)
-                                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
-                                             ::"r"(rs + 16 * b), "l"(src + 4 * b),
-                                             "r"((ok && (FULLBLK || b < nb_real)) ? 16 : 0));
-                        }
-                        const float *valp = p.val + st.k0;
-                        const float *wtsp = HAS_W ? p.wts + st.k0 : nullptr;
-                        const int32_t *idxp = p.idx + st.k0;
-                        const bool more = s + C::NS - 1 < st.nst;
-#pragma unroll
-                        for (int r = h; r < R; r += 2) {
-                            const int kk = R * s + r;
-                            const bool okv = kk < n;
-                            asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                                         ::"r"(ss + 4 * (C::YOFF + r)), "l"(valp + (okv ? kk : 0)),
-                                         "r"(okv ? 4 : 0), "l"(pol_stream));
-                            if (HAS_W)
-                                asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                                             ::"r"(ss + 4 * (C::WOFF + r)), "l"(wtsp + (okv ? kk : 0)),
-                                             "r"(okv ? 4 : 0), "l"(pol_stream));
-                            if (more) {
-                                const int ku = R * (s + C::NS - 1) + r;
-                                const bool oku = ku < n;
-                                asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                                             ::"r"(ids_s + 4 * (R * ((gs + C::NS - 1) % C::NR) + r)),
-                                             "l"(idxp + (oku ? ku : 0)), "r"(oku ? 4 : 0), "l"(pol_stream));
-                            }
-                        }
-                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];"
-                                     ::"r"(full0 + 8 * (c * 4 + slot)) : "memory");
-                        const int pf = R * s + C::PF;
-                        if (pf < n && ((st.k0 + pf) & 31) < R)
-                            prefetch_l2(h ? (const void *)(valp + pf) : (const void *)(idxp + pf));
-                        st.s = s + 1;
-                        moved = true;
-                    }
-                    if (st.s >= st.nst) st.phase = 0;
-                }
-            }
-            if (!moved) __nanosleep(20);
-        }
-        return;
-    }
-
-    // ------------------------------------------------------------------ consumer
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    const int c = warp;
-    unsigned char *cbase = smem_raw + c * C::CONS_BYTES;
-    float *my_g = reinterpret_cast<float *>(cbase) + pair * C::GSTRIDE;
-    const float *my_slot = reinterpret_cast<const float *>(cbase) + pair * C::SLOT;
-    const int *d = desc_mem + c * C::DESC_INTS;
-    int boff[NBK];
-#pragma unroll
-    for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
-    unsigned gst = 0;
-    for (int ng = 0;; ++ng) {
-        mbar_wait(desc0 + 8 * c, ng & 1);
-        const int4 gi = *reinterpret_cast<const int4 *>(d + 4 * C::PAIRS);
-        if (gi.x < 0) break;
-        const int4 ti = *reinterpret_cast<const int4 *>(d + 4 * pair);
-        const int grp = gi.x, nst = gi.y, row = ti.x, n = ti.y, slot = ti.z;
-        PairAcc<NBK> acc;
-        acc.zero();
-        for (int t = 0; t < nst; ++t) {
-            const unsigned gs = gst + (unsigned)t;
-            mbar_wait(full0 + 8 * (c * 4 + gs % C::NS), (gs / C::NS) & 1);
-            const float *sl = my_slot + (gs % C::NS) * (C::STAGE_BYTES / 4);
-            float ys[R];
-            if constexpr (R == 4) {
-                const float4 v = *reinterpret_cast<const float4 *>(sl + C::YOFF);
-                ys[0] = v.x; ys[1] = v.y; ys[2] = v.z; ys[3] = v.w;
-            } else {
-                const float2 v = *reinterpret_cast<const float2 *>(sl + C::YOFF);
-                ys[0] = v.x; ys[1] = v.y;
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const float *rw = sl + r * C::LDK;
-                float4 xr[NBK];
-#pragma unroll
-                for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(rw + boff[b]);
-                const float y = ys[r] - p.y_shift;
-                float4 xa[NBK];
-#pragma unroll
-                for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
-                float wy = y;
-                if (HAS_W) {
-                    const float w = sl[C::WOFF + r];
-                    wy = w * y;
-#pragma unroll
-                    for (int b = 0; b < NBK; ++b) {
-                        xa[b].x *= w; xa[b].y *= w; xa[b].z *= w; xa[b].w *= w;
-                    }
-                }
-                acc.add(xa, xr, y, wy);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8 * (c * 4 + gs % C::NS));
-        }
-        gst += (unsigned)nst;
-        // every stage of this group has been consumed (all cp.async landed):
-        // the ring is free for the packed systems
-        acc.scatter(my_g, h, C::RHS0);
-        __syncwarp();
-        double o_sse = 0.0, o_reg = 0.0;
-        const int64_t task = (int64_t)grp * C::PAIRS + pair;
-        if (task < q.n_tasks) {
-            if (slot >= 0) {
-                float *dst = p.partials + (size_t)slot * C::PSTR;
-                for (int i = h; i < C::GRAM; i += 2) dst[i] = my_g[i];
-                if (h == 0) dst[C::GRAM] = acc.yy;
-            } else if (h == 0) {
-                finish_row<C::LDK>(p, my_g, row, n, acc.yy, o_sse, o_reg);
-            }
-        }
-        if (p.obj_partial) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                o_sse += __shfl_xor_sync(FULL, o_sse, o);
-                o_reg += __shfl_xor_sync(FULL, o_reg, o);
-            }
-            if (lane == 0) {
-                p.obj_partial[2 * grp] = o_sse;
-                p.obj_partial[2 * grp + 1] = o_reg;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(done0 + 8 * c);
-    }
-}
-
 // Hot rows: one warp per row sums its chunk partials in chunk order, then
 // the warp solves cooperatively (lane i owns row i of A, right-looking
 // Cholesky with shuffles).
@@ -2465,57 +2130,12 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     return check_launch("mcf_als_half_step(pair)");
 }
 
-template <int NBK, int R, bool W, bool FB>
-int launch_pair_ws(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
-    using C = WsCfg<NBK, R>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_als_pair_ws<NBK, R, W, FB>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        attr = true;
-    }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
-    const int64_t grid = std::min<int64_t>(ceil_div(groups, C::CONS), (int64_t)sms);
-    if (grid > 0) k_als_pair_ws<NBK, R, W, FB><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(p, q);
-    if (q.n_heavy > 0)
-        k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
-    if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
-    return check_launch("mcf_als_half_step(pair ws)");
-}
-
-// D <= 20 kernel variant: "ws" (warp-specialised, default) or "v8"
-// (every warp issues its own gathers); MCF_PAIR_KERNEL selects
-bool pair_ws() {
-    static bool ws = [] {
-        const char *e = getenv("MCF_PAIR_KERNEL");
-        return !(e && strcmp(e, "v8") == 0);
-    }();
-    return ws;
-}
-
-// ratings per pipeline stage of the D <= 20 pair kernel (MCF_PAIR_R=2 selects
-// the 2-rating / 7-stage variant; default 4 ratings / 4 stages)
-int pair_r() {
-    static int r = [] {
-        const char *e = getenv("MCF_PAIR_R");
-        return (e && atoi(e) == 2) ? 2 : 4;
-    }();
-    return r;
-}
-
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int nb = (p.D + 3) / 4;
     if (nb <= 1) return launch_pair<1, 4, W, false>(p, q, s);
     if (nb <= 3) return launch_pair<3, 4, W, false>(p, q, s);
-    if (nb == 5) {
-        if (pair_ws()) return launch_pair_ws<5, 4, W, true>(p, q, s);
-        if (pair_r() == 2) return launch_pair<5, 2, W, true>(p, q, s);
-        return launch_pair<5, 4, W, true>(p, q, s);
-    }
+    if (nb == 5) return launch_pair<5, 4, W, true>(p, q, s);
     return launch_pair<5, 4, W, false>(p, q, s);
 }
 
