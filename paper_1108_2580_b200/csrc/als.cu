@@ -911,14 +911,10 @@ __device__ __forceinline__ float &tel(float2 (&t)[8][4], int m, int n) {
 }
 
 template <int NB8, bool HAS_W>
-__global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
+__device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item, float *sm,
+                                               int lane) {
     using C = TileWarpCfg<NB8>;
     constexpr int S = C::S, LDK = C::LDK, BT = C::BT;
-    extern __shared__ float4 smem4[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float *sm = reinterpret_cast<float *>(smem4) + warp * C::WARP_FLOATS;
-    const int64_t item = (int64_t)blockIdx.x * C::WARPS + warp;
-    if (item >= p.total_items) return;
     const ItemInfo it = item_info(p, item);
     const int D = p.D;
     const int nb4_real = (D + 3) / 4;
@@ -934,15 +930,15 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
         if (tok[s] && tI[s] == tJ[s]) dslot = s;
     }
 
-    float2 acc[S][8][4], rhs[4];
+    // augmented Gram: the rating y rides in column D of every staged row, so
+    // sum w [x|y][x|y]^T carries b = sum w y x in row D (no separate rhs FMAs)
+    float2 acc[S][8][4];
 #pragma unroll
     for (int s = 0; s < S; ++s)
 #pragma unroll
         for (int m = 0; m < 8; ++m)
 #pragma unroll
             for (int k = 0; k < 4; ++k) acc[s][m][k] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
 
     // ---- Gram ---------------------------------------------------------------
     auto ld = [&](int64_t b, int &id, float &y, float &w) {
@@ -988,13 +984,14 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
         }
         __syncwarp();
         const float *ys = cur + BT * C::ROWS;
+        if (lane < BT) cur[lane * C::ROWS + D] = ys[lane];   // the copies have landed
+        __syncwarp();
         for (int kb = 0; kb < BT; ++kb) {
             const float *xr = cur + kb * C::ROWS;
-            const float y = ys[kb];
             const float w = HAS_W ? ys[BT + kb] : 1.f;
+            // every slot runs (an unused slot repeats tile 0): no branches
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                if (!tok[s]) continue;
                 const float4 a0 = *reinterpret_cast<const float4 *>(xr + 8 * tI[s]);
                 const float4 a1 = *reinterpret_cast<const float4 *>(xr + 8 * tI[s] + 4);
                 const float4 b0 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[s]);
@@ -1010,10 +1007,6 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
                     ffma2(acc[s][m][1], a[m], b0.z, b0.w);
                     ffma2(acc[s][m][2], a[m], b1.x, b1.y);
                     ffma2(acc[s][m][3], a[m], b1.z, b1.w);
-                }
-                if (s == dslot) {
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) ffma2(rhs[m], y, a[2 * m], a[2 * m + 1]);
                 }
             }
         }
@@ -1032,11 +1025,6 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     *reinterpret_cast<float2 *>(dst + m * 8 + 2 * k) = acc[s][m][k];
-            if (s == dslot) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    *reinterpret_cast<float2 *>(dst + 64 + 2 * k) = rhs[k];
-            }
         }
         __threadfence();
         __syncwarp();
@@ -1052,8 +1040,6 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
             for (int m = 0; m < 8; ++m)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[s][m][k] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) rhs[k] = make_float2(0.f, 0.f);
         for (int c = 0; c < it.nch; ++c) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
@@ -1067,14 +1053,6 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
                         acc[s][m][k].x += v.x;
                         acc[s][m][k].y += v.y;
                     }
-                if (s == dslot) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src + 64 + 2 * k));
-                        rhs[k].x += v.x;
-                        rhs[k].y += v.y;
-                    }
-                }
             }
         }
     }
@@ -1098,6 +1076,24 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
     float *bv = invd + LDK;         // [LDK] b -> y -> x
     int *flag = reinterpret_cast<int *>(bv + LDK);
     __syncwarp();                   // stages are dead (all cp.async drained)
+    {   // row D of the augmented Gram is b^T: publish it to bv, then clear it
+        const int ID = D >> 3, mD = D & 7;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!tok[s] || tI[s] != ID) continue;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                if (m != mD) continue;
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    const int col = 8 * tJ[s] + n;
+                    if (col < D) bv[col] = tel(acc[s], m, n);
+                    tel(acc[s], m, n) = 0.f;
+                }
+            }
+        }
+    }
+    __syncwarp();
     if (dslot >= 0) {
         // diagonal tile: + (lam_c + lam_n n + tau S) on the diagonal, identity
         // on the padding rows; its b block (+ tau T)
@@ -1110,7 +1106,7 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
                 const int i = 8 * I + m;
                 float &d = tel(acc[s], m, m);
                 d = i < D ? d + diag : 1.f;
-                const float bm = (m & 1) ? rhs[m >> 1].y : rhs[m >> 1].x;
+                const float bm = i < D ? bv[i] : 0.f;
                 bv[i] = i < D ? (p.tax_T ? fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], bm) : bm) : 0.f;
             }
         }
@@ -1276,6 +1272,25 @@ __global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
         __syncwarp();
     }
     for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? bv[i] : 0.f;
+}
+
+// persistent: every warp pulls work items from an atomic counter (no CTA
+// waits on its slowest warp); the item order is the plan's
+template <int NB8, bool HAS_W>
+__global__ void __launch_bounds__(128) k_als_tile_warp(AlsParams p) {
+    using C = TileWarpCfg<NB8>;
+    extern __shared__ float4 smem4[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *sm = reinterpret_cast<float *>(smem4) + warp * C::WARP_FLOATS;
+    int *ctr = p.counters + p.n_list + 1;
+    for (;;) {
+        int64_t item = 0;
+        if (lane == 0) item = atomicAdd(ctr, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= p.total_items) break;
+        tile_warp_item<NB8, HAS_W>(p, item, sm, lane);
+        __syncwarp();   // the next item's gathers reuse the solve scratch
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -2017,7 +2032,13 @@ int launch_tile_warp(const AlsParams &p, cudaStream_t s) {
                              (int)smem);
         attr = true;
     }
-    const int64_t grid = ceil_div(p.total_items, C::WARPS);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_tile_warp<NB8, W>, C::WARPS * 32,
+                                                  smem);
+    const int64_t grid = std::min<int64_t>(ceil_div(p.total_items, C::WARPS),
+                                           (int64_t)sms * std::max(per_sm, 1));
     if (grid > 0) k_als_tile_warp<NB8, W><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p);
     return check_launch("mcf_als_half_step(tile-warp)");
 }
@@ -2040,7 +2061,7 @@ int dispatch(const AlsParams &p, cudaStream_t s) {
         case 7: return launch_warp<7, W>(p, s);
         default: break;
     }
-    switch (nb8_for(p.D)) {
+    switch (nb8_for(p.D + 1)) {   // + 1: the augmented rating column
         case 4: return launch_tile_warp<4, W>(p, s);
         case 6: return launch_tile_warp<6, W>(p, s);
         case 7: return launch_tile_warp<7, W>(p, s);
@@ -2054,7 +2075,7 @@ int dispatch(const AlsParams &p, cudaStream_t s) {
 size_t pstride_of(int D) {
     const int nb = (D + 3) / 4;
     if (nb <= 7) return (size_t)(nb * (nb + 1) / 2) * 20;   // warp path, 4x4 tiles
-    const int n8 = nb8_for(D);
+    const int n8 = nb8_for(D + 1);
     return (size_t)(n8 * (n8 + 1) / 2) * 72;                // wide path, 8x8 tiles
 }
 
