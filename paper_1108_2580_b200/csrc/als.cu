@@ -948,6 +948,9 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
         y = ok ? p.val[kk] - p.y_shift : 0.f;
         w = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
     };
+    // staged row layout, "split halves": the low 4 floats of 8-block I sit
+    // in 16-byte unit I, the high 4 in unit NB8 + I, so the a-side loads of
+    // 8 lanes holding consecutive block rows I hit 8 distinct bank groups
     auto issue = [&](int id, float y, float w, float *stage) {
         float *ys = stage + BT * C::ROWS;
         for (int e = lane; e < BT * (LDK / 4); e += 32) {
@@ -955,7 +958,8 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
             const int rid = __shfl_sync(FULL, id, rr);
             const bool ok = rid >= 0 && part < nb4_real;
             const float *g = ok ? p.fixed + (size_t)rid * p.ld + part * 4 : p.fixed;
-            cp_async16(stage + rr * C::ROWS + part * 4, g, ok ? 16 : 0);
+            const int unit = (part & 1) ? NB8 + (part >> 1) : (part >> 1);
+            cp_async16(stage + rr * C::ROWS + unit * 4, g, ok ? 16 : 0);
         }
         if (lane < BT) {
             ys[lane] = y;
@@ -984,7 +988,8 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
         }
         __syncwarp();
         const float *ys = cur + BT * C::ROWS;
-        if (lane < BT) cur[lane * C::ROWS + D] = ys[lane];   // the copies have landed
+        if (lane < BT)   // the copies have landed; column D in split-halves order
+            cur[lane * C::ROWS + ((D & 4) ? 4 * NB8 : 0) + 4 * (D >> 3) + (D & 3)] = ys[lane];
         __syncwarp();
         for (int kb = 0; kb < BT; ++kb) {
             const float *xr = cur + kb * C::ROWS;
@@ -992,10 +997,10 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
             // every slot runs (an unused slot repeats tile 0): no branches
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                const float4 a0 = *reinterpret_cast<const float4 *>(xr + 8 * tI[s]);
-                const float4 a1 = *reinterpret_cast<const float4 *>(xr + 8 * tI[s] + 4);
-                const float4 b0 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[s]);
-                const float4 b1 = *reinterpret_cast<const float4 *>(xr + 8 * tJ[s] + 4);
+                const float4 a0 = *reinterpret_cast<const float4 *>(xr + 4 * tI[s]);
+                const float4 a1 = *reinterpret_cast<const float4 *>(xr + 4 * (NB8 + tI[s]));
+                const float4 b0 = *reinterpret_cast<const float4 *>(xr + 4 * tJ[s]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(xr + 4 * (NB8 + tJ[s]));
                 float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 if (HAS_W) {
 #pragma unroll
