@@ -98,6 +98,10 @@ __global__ void k_plan_fill(const int32_t *item_off, int32_t n_list, int32_t *it
 // ---------------------------------------------------------------------------
 // shared pieces
 
+__device__ __forceinline__ void prefetch_l2(const void *a) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
 __device__ __forceinline__ void report_fail(unsigned long long *fail, int r) {
     atomicMin(fail, static_cast<unsigned long long>(r));
 }
@@ -941,12 +945,17 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
             for (int k = 0; k < 4; ++k) acc[s][m][k] = make_float2(0.f, 0.f);
 
     // ---- Gram ---------------------------------------------------------------
+    // raw loads only (consumed one stage later by issue(), so their latency
+    // hides behind a stage of FMAs); the streams are L2-prefetched 4 stages ahead
     auto ld = [&](int64_t b, int &id, float &y, float &w) {
         const int64_t kk = it.k0 + b * BT + lane;
         const bool ok = lane < BT && kk < it.k1;
         id = ok ? p.idx[kk] : -1;
-        y = ok ? p.val[kk] - p.y_shift : 0.f;
+        y = ok ? p.val[kk] : 0.f;
         w = ok ? (HAS_W ? p.wts[kk] : 1.f) : 0.f;
+        const int64_t pf = it.k0 + (b + 4) * BT;
+        if (lane < 2 && pf < it.k1 && ((b & 1) == 0))
+            prefetch_l2(lane ? (const void *)(p.val + pf) : (const void *)(p.idx + pf));
     };
     // staged row layout, "split halves": the low 4 floats of 8-block I sit
     // in 16-byte unit I, the high 4 in unit NB8 + I, so the a-side loads of
@@ -962,7 +971,7 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
             cp_async16(stage + rr * C::ROWS + unit * 4, g, ok ? 16 : 0);
         }
         if (lane < BT) {
-            ys[lane] = y;
+            ys[lane] = id >= 0 ? y - p.y_shift : 0.f;
             ys[BT + lane] = w;
         }
         cp_async_commit();
@@ -1515,9 +1524,6 @@ __global__ void k_obj_sum(const double *part, int64_t n, double *out) {
     }
 }
 
-__device__ __forceinline__ void prefetch_l2(const void *a) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-}
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -1853,27 +1859,61 @@ k_als_pair(AlsParams p, PairPlan q) {
     }
 }
 
-// Hot rows: one warp per row sums its chunk partials in chunk order, then
-// the warp solves cooperatively (lane i owns row i of A, right-looking
+// Hot rows: a CTA takes 8 hot rows; all 8 warps sum each row's chunk
+// partials (chunks split over the warps, combined in a fixed order), then
+// warp w solves row w cooperatively (lane i owns row i of A, right-looking
 // Cholesky with shuffles).
 template <int NBK>
-__global__ void __launch_bounds__(128) k_als_heavy(AlsParams p, PairPlan q) {
+__global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
     using C = PairGeom<NBK>;
     constexpr int LDK = C::LDK;
-    __shared__ float g[4][C::GSTRIDE + 1];
+    constexpr int HW = 8;                            // warps (and hot rows) per CTA
+    constexpr int NE = (C::GRAM + 1 + 31) / 32;      // partial elements per lane
+    __shared__ float part[HW][C::GRAM + 1];
+    __shared__ float Gs[HW][C::GSTRIDE + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t hr = (int64_t)blockIdx.x * 4 + warp;
+    // phase 1, row by row: warp w sums chunks s0+w, s0+w+HW, ... (incl.
+    // sum w y^2 at GRAM), the HW warp sums are then added in warp order --
+    // a fixed order, so the result is deterministic
+    for (int k = 0; k < HW; ++k) {
+        const int64_t hk = (int64_t)blockIdx.x * HW + k;
+        if (hk >= q.n_heavy) break;
+        const int jk = q.sorted_j[hk];
+        const int c0 = q.hoff[jk], c1 = q.hoff[jk + 1];
+        float a[NE];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) a[e] = 0.f;
+        for (int c = c0 + warp; c < c1; c += HW) {
+            const float *src = p.partials + (size_t)c * C::PSTR;
+            float v[NE];
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const int i = lane + 32 * e;
+                v[e] = i <= C::GRAM ? __ldcg(src + i) : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < NE; ++e) a[e] += v[e];
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int i = lane + 32 * e;
+            if (i <= C::GRAM) part[warp][i] = a[e];
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i <= C::GRAM; i += 32 * HW) {
+            float t = 0.f;
+#pragma unroll
+            for (int w = 0; w < HW; ++w) t += part[w][i];
+            Gs[k][i] = t;
+        }
+        __syncthreads();
+    }
+    // phase 2: warp w solves hot row HW * block + w
+    const int64_t hr = (int64_t)blockIdx.x * HW + warp;
     if (hr >= q.n_heavy) return;
     const int j = q.sorted_j[hr];
     const int r = p.row_list ? p.row_list[j] : p.row_lo + j;
-    const int s0 = q.hoff[j], s1 = q.hoff[j + 1];
-    float *G = g[warp];
-    for (int i = lane; i <= C::GRAM; i += 32) {   // incl. sum w y^2 at GRAM
-        float a = 0.f;
-        for (int s = s0; s < s1; ++s) a += __ldcg(p.partials + (size_t)s * C::PSTR + i);
-        G[i] = a;
-    }
-    __syncwarp();
+    float *G = Gs[warp];
     const int D = p.D;
     const int64_t n = p.ptr[r + 1] - p.ptr[r];
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
@@ -2151,7 +2191,7 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
     if (grid > 0) k_als_pair<NBK, R, W, FB><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
-        k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 4), 128, 0, s>>>(p, q);
+        k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 8), 256, 0, s>>>(p, q);
     if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
     return check_launch("mcf_als_half_step(pair)");
 }
