@@ -234,7 +234,7 @@ def _random_split(U, I, nnz, seed, hot=None):
             rng.integers(0, 101, keys.size).astype(np.float32))
 
 
-@pytest.mark.parametrize("D", [1, 3, 5, 8, 16, 20, 28, 29, 32, 50, 64, 100, 128])
+@pytest.mark.parametrize("D", [1, 3, 5, 8, 16, 20, 21, 28, 29, 32, 50, 56, 64, 96, 100, 103, 104, 128])
 @pytest.mark.parametrize("reg", ["plain", "weighted"])
 def test_dims_reanchored(D, reg):
     """Every compiled D range (warp path NB <= 7, CTA path above) and both
