@@ -27,6 +27,10 @@
  *   mcf_sq_norms       the regulariser of factor.als_objective factor.py:541-547
  *                      / factor.loss_mf (factor.py:270-278)
  *   mcf_add_gathered   q_i + q_a[artist(i)] of mfitr._rating_terms mfitr.py:203-216
+ *   mcf_als_half_step_bias  the lam1 (bias) / lam2 (factor) regularisers of
+ *                      mfitr.loss_mfitr for augmented [f | b] blocks  mfitr.py:226-242
+ *   mcf_mfitr_fixed, mcf_mfitr_targets  the block terms of mfitr._rating_terms
+ *                      (prediction mu + b_u + b_i + b_a + (q_i + q_a).p_u)  mfitr.py:203-216
  */
 #ifndef MCF_H
 #define MCF_H
@@ -107,6 +111,42 @@ int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
                       const float *tax_T, float tau, const int32_t *row_list, int32_t n_list,
                       int32_t row_lo, int32_t chunk, const void *plan, const int64_t *plan_info,
                       int64_t *fail_row, double *obj_out, void *ws, size_t ws_bytes,
+                      void *stream);
+
+/* mcf_als_half_step with one "bias" coordinate (MFITR full blocks,
+ * SURVEY §8(f)): coordinate bias_dim (0 <= bias_dim < D) of every row system
+ * gets the regulariser bias_lam_c + bias_lam_n * n_r instead of
+ * lam_c + lam_n * n_r + tau * S_r, and no taxonomy T term.  This is the
+ * per-observation lam1 (biases) vs lam2 (factors) split of the reference's
+ * loss_mfitr (mfitr.py:226-242) for the augmented unknowns [f | b].  No fused
+ * objective.  Other arguments as mcf_als_half_step. */
+int mcf_als_half_step_bias(const int64_t *ptr, const int32_t *idx, const float *val,
+                           const float *wts, const float *fixed, int64_t n_fixed, float *out,
+                           int32_t D, float lam_c, float lam_n, float y_shift,
+                           const float *tax_S, const float *tax_T, float tau,
+                           const int32_t *row_list, int32_t n_list, int32_t row_lo,
+                           int32_t chunk, const void *plan, const int64_t *plan_info,
+                           int64_t *fail_row, void *ws, size_t ws_bytes, int32_t bias_dim,
+                           float bias_lam_c, float bias_lam_n, void *stream);
+
+/* ---- MFITR full-model blocks (mfitr.py:203-216 prediction) -----------------
+ * Tables are [rows][mcf_factor_ld(D + 1)] with the factor in columns 0..D-1
+ * and the bias in column D.
+ * mcf_mfitr_fixed: the gather table of an augmented solve,
+ *   out[r] = [main[r][:D] + (art && art[r] >= 0 ? add[art[r]][:D] : 0) | 1 | 0..]
+ * (users step: main = Q, add = artist table; items / artists steps: main = P).
+ * mcf_mfitr_targets: per-rating targets of one layout in CSR order,
+ *   mode 0 (users layout, partner = item i):  r - mu - b_i - b_a[art(i)]
+ *   mode 1 (items layout, row = item i, partner = user u):
+ *                       r - mu - b_u - [art(i) >= 0] (b_a + q_a . p_u)
+ *   mode 2 (artists layout, row = artist, partner = user u, aux = item i):
+ *                       r - mu - b_u - b_i - q_i . p_u
+ * (Pa = [p | b_u], Qa = [q | b_i], Aa = [q_a | b_a] indexed by artist id). */
+int mcf_mfitr_fixed(const float *main_t, const float *add_t, const int32_t *art, int64_t n,
+                    int32_t D, float *out, void *stream);
+int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t *idx, const float *val,
+                      const int32_t *aux, int32_t n_rows, const float *Pa, const float *Qa,
+                      const float *Aa, const int32_t *art, float mu, int32_t D, float *out,
                       void *stream);
 
 /* ---- MFITR taxonomy term (segmented reduction) ---------------------------

@@ -68,7 +68,23 @@ struct AlsParams {
     unsigned long long *fail;  // min failing row (as unsigned; ~0 = none)
     double *obj_partial;       // [(groups + hot rows) * 2] or null (fused objective)
     int64_t obj_groups;        // pair-path groups (hot rows follow them)
+    // optional bias coordinate (MFITR full blocks): its own regulariser
+    // bias_lam_c + bias_lam_n * n, no taxonomy terms; -1 = none
+    int bias_dim;
+    float bias_lam_c, bias_lam_n;
 };
+
+// diagonal regulariser of coordinate i of row system with n ratings.  A
+// bias of a row without ratings (an item only the taxonomy touches) has a
+// zero Gram row and zero right-hand side: pivot 1 -> bias 0 (any value
+// minimises the loss then; 0 is the reference's initial value).
+__device__ __forceinline__ float diag_at(const AlsParams &p, int i, float diag, float n) {
+    return i == p.bias_dim ? (n > 0.f ? fmaf(p.bias_lam_n, n, p.bias_lam_c) : 1.f) : diag;
+}
+// taxonomy T term of coordinate i (none on the bias coordinate)
+__device__ __forceinline__ float tax_rhs(const AlsParams &p, int r, int i, float b) {
+    return (p.tax_T && i != p.bias_dim) ? fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], b) : b;
+}
 
 // ---------------------------------------------------------------------------
 // plan
@@ -322,12 +338,12 @@ __global__ void __launch_bounds__(256) k_als_warp(AlsParams p) {
             for (int n = 0; n < 4; ++n) {
                 const int col = 4 * bj + n;
                 float v = acc[m][n];
-                if (row == col) v += diag;
+                if (row == col) v += diag_at(p, row, diag, (float)it.n);
                 if (col <= row) M[row * MS + col] = v;
             }
             if (bi == bj) {
                 float bv = rhs[m];
-                if (p.tax_T && row < D) bv = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + row], bv);
+                if (row < D) bv = tax_rhs(p, r, row, bv);
                 M[row * MS + C::LD] = bv;
             }
         }
@@ -671,8 +687,8 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
     }
     for (int i = tid; i < C::LDK; i += CTA_THREADS) {
         if (i < D) {
-            M[i * MS + i] += diag;
-            if (p.tax_T) M[i * MS + C::LDK] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], M[i * MS + C::LDK]);
+            M[i * MS + i] += diag_at(p, i, diag, (float)it.n);
+            M[i * MS + C::LDK] = tax_rhs(p, r, i, M[i * MS + C::LDK]);
         } else {   // padding rows: identity, zero rhs (their solution is 0)
             M[i * MS + i] = 1.f;
             M[i * MS + C::LDK] = 0.f;
@@ -1119,9 +1135,8 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
             for (int m = 0; m < 8; ++m) {
                 const int i = 8 * I + m;
                 float &d = tel(acc[s], m, m);
-                d = i < D ? d + diag : 1.f;
-                const float bm = i < D ? bv[i] : 0.f;
-                bv[i] = i < D ? (p.tax_T ? fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], bm) : bm) : 0.f;
+                d = i < D ? d + diag_at(p, i, diag, (float)it.n) : 1.f;
+                bv[i] = i < D ? tax_rhs(p, r, i, bv[i]) : 0.f;
             }
         }
     }
@@ -1382,7 +1397,8 @@ __device__ __forceinline__ constexpr int pidx(int i, int j) { return i * (i + 1)
 // row i held in registers (one shared-memory load per FMA).  g: packed
 // lower triangle (pidx) and rhs at RHS0 (overwritten with the solution).
 template <int LDK>
-__device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add) {
+__device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add, int bias_dim = -1,
+                                             float bias_add = 0.f) {
     constexpr int RHS0 = LDK * (LDK + 1) / 2;
     float inv[LDK];
     bool ok = true;
@@ -1400,7 +1416,7 @@ __device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add) {
                 r[j] = t * inv[j];
                 g[pidx(i, j)] = r[j];
             }
-            float d = r[i] + diag_add;
+            float d = r[i] + (i == bias_dim ? bias_add : diag_add);
 #pragma unroll
             for (int k = 0; k < i; ++k) d = fmaf(-r[k], r[k], d);
             ok = ok && (d > 0.f) && isfinite(d);
@@ -1472,12 +1488,11 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     const float lam_row = p.lam_c + p.lam_n * (float)n;
     const float diag = lam_row + p.tau * S;
     if (p.tax_T)
-        for (int i = 0; i < D; ++i)
-            g[RHS0 + i] = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + i], g[RHS0 + i]);
+        for (int i = 0; i < D; ++i) g[RHS0 + i] = tax_rhs(p, r, i, g[RHS0 + i]);
     float b[LDK];
 #pragma unroll
     for (int i = 0; i < LDK; ++i) b[i] = i < D ? g[RHS0 + i] : 0.f;
-    if (!thread_solve<LDK>(g, D, diag)) {
+    if (!thread_solve<LDK>(g, D, diag, p.bias_dim, diag_at(p, p.bias_dim, diag, (float)n))) {
         report_fail(p.fail, r);
         return;
     }
@@ -1924,11 +1939,11 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
 #pragma unroll
     for (int c = 0; c < LDK; ++c) a[c] = (lane < D && c <= lane) ? G[pidx(lane, c)] : 0.f;
     float b = lane < D ? G[C::RHS0 + lane] : 0.f;
-    if (p.tax_T && lane < D) b = fmaf(p.tau, p.tax_T[(size_t)r * p.ld + lane], b);
+    if (lane < D) b = tax_rhs(p, r, lane, b);
     const float b0 = b, yy = G[C::GRAM];
 #pragma unroll
     for (int c = 0; c < LDK; ++c)
-        if (c == lane) a[c] += diag;
+        if (c == lane) a[c] += diag_at(p, lane, diag, (float)n);
     bool bad = false;
 #pragma unroll
     for (int j2 = 0; j2 < LDK; ++j2) {
@@ -2299,14 +2314,14 @@ extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t
            sizeof(float) * (size_t)slots * per;
 }
 
-extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
-                                 const float *wts, const float *fixed, int64_t n_fixed, float *out,
-                                 int32_t D,
-                                 float lam_c, float lam_n, float y_shift, const float *tax_S,
-                                 const float *tax_T, float tau, const int32_t *row_list,
-                                 int32_t n_list, int32_t row_lo, int32_t chunk, const void *plan,
-                                 const int64_t *plan_info, int64_t *fail_row, double *obj_out,
-                                 void *ws, size_t ws_bytes, void *stream) {
+static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *val,
+                          const float *wts, const float *fixed, int64_t n_fixed, float *out,
+                          int32_t D, float lam_c, float lam_n, float y_shift, const float *tax_S,
+                          const float *tax_T, float tau, const int32_t *row_list, int32_t n_list,
+                          int32_t row_lo, int32_t chunk, const void *plan,
+                          const int64_t *plan_info, int64_t *fail_row, double *obj_out, void *ws,
+                          size_t ws_bytes, void *stream, int32_t bias_dim, float bias_lam_c,
+                          float bias_lam_n) {
     if (D < 1 || D > 128) {
         set_error("mcf_als_half_step: D must be in [1, 128]");
         return MCF_E_UNSUPPORTED;
@@ -2337,6 +2352,13 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
     p.item_row = L.item_row;
     p.total_items = total_items;
     p.fail = reinterpret_cast<unsigned long long *>(fail_row);
+    p.bias_dim = bias_dim;
+    p.bias_lam_c = bias_lam_c;
+    p.bias_lam_n = bias_lam_n;
+    if (bias_dim >= D || (bias_dim >= 0 && obj_out)) {
+        set_error("mcf_als_half_step: bias_dim must be < D, and excludes the fused objective");
+        return MCF_E_ARG;
+    }
     // workspace: counters [n_list] + partial slots
     if (obj_out && !use_pair(D)) {
         set_error("mcf_als_half_step: obj_out (fused objective) is implemented for D <= 20");
@@ -2377,4 +2399,35 @@ extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const f
     }
     if (total_items == 0) return MCF_OK;
     return wts ? dispatch<true>(p, s) : dispatch<false>(p, s);
+}
+
+extern "C" int mcf_als_half_step(const int64_t *ptr, const int32_t *idx, const float *val,
+                                 const float *wts, const float *fixed, int64_t n_fixed, float *out,
+                                 int32_t D,
+                                 float lam_c, float lam_n, float y_shift, const float *tax_S,
+                                 const float *tax_T, float tau, const int32_t *row_list,
+                                 int32_t n_list, int32_t row_lo, int32_t chunk, const void *plan,
+                                 const int64_t *plan_info, int64_t *fail_row, double *obj_out,
+                                 void *ws, size_t ws_bytes, void *stream) {
+    return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
+                          tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
+                          obj_out, ws, ws_bytes, stream, -1, 0.f, 0.f);
+}
+
+extern "C" int mcf_als_half_step_bias(const int64_t *ptr, const int32_t *idx, const float *val,
+                                      const float *wts, const float *fixed, int64_t n_fixed,
+                                      float *out, int32_t D, float lam_c, float lam_n,
+                                      float y_shift, const float *tax_S, const float *tax_T,
+                                      float tau, const int32_t *row_list, int32_t n_list,
+                                      int32_t row_lo, int32_t chunk, const void *plan,
+                                      const int64_t *plan_info, int64_t *fail_row, void *ws,
+                                      size_t ws_bytes, int32_t bias_dim, float bias_lam_c,
+                                      float bias_lam_n, void *stream) {
+    if (bias_dim < 0) {
+        set_error("mcf_als_half_step_bias: bias_dim must be >= 0");
+        return MCF_E_ARG;
+    }
+    return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
+                          tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
+                          nullptr, ws, ws_bytes, stream, bias_dim, bias_lam_c, bias_lam_n);
 }

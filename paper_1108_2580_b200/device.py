@@ -126,7 +126,11 @@ class LayoutSolver:
 
     def solve(self, lay: SideLayout, fixed: torch.Tensor, out: torch.Tensor, lam_c=0.0, lam_n=0.0,
               y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
-              fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None):
+              fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None,
+              val: torch.Tensor | None = None, bias=None):
+        """bias = (dim, lam_c, lam_n): coordinate `dim` is a bias with its own
+        regulariser (mcf_als_half_step_bias); val: per-rating targets in the
+        layout's CSR order instead of the ratings."""
         dev = lay.device
         if fail is None:
             if self.fail is None:
@@ -139,8 +143,17 @@ class LayoutSolver:
         if k not in self._ws or self._ws[k].numel() < need:
             self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = self._ws[k]
+        vals = lay.val if val is None else val
+        if bias is not None:
+            check(_lib.lib().mcf_als_half_step_bias(
+                ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
+                ptr(out), self.D, float(lam_c), float(lam_n), float(y_shift), ptr(tax_S),
+                ptr(tax_T), float(tau), ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail),
+                ptr(ws), ws.numel(), int(bias[0]), float(bias[1]), float(bias[2]),
+                stream_ptr(dev)), "mcf_als_half_step_bias")
+            return fail
         check(_lib.lib().mcf_als_half_step(
-            ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(wts), ptr(fixed), fixed.shape[0],
+            ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
             ptr(out), self.D,
             float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
             ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail), ptr(obj_out), ptr(ws),

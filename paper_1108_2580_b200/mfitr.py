@@ -251,39 +251,259 @@ class MfitrSolver:
         return sse + h.lam2 * reg + graph
 
 
+class MfitrFullSolver:
+    """Every MFITR parameter block on device (time terms off), SURVEY §8(f)1:
+    block-coordinate descent on loss_mfitr (mfitr.py:226-242) over augmented
+    unknowns [f | b] (factor columns 0..D-1, bias in column D):
+
+      items   [q_i | b_i] layer by layer (tracks, albums, artists, rest; no
+              edge joins two items of one layer, taxonomy.py:102-103), with
+              the taxonomy term on q only;
+      artists [q_a | b_a] over the ratings of each artist's items (q_a, b_a
+              indexed by the artist's item id, mfitr.py:92-149);
+      users   [p_u | b_u].
+
+    Each block is one exact least-squares solve (mcf_als_half_step_bias):
+    lam2 * n on the factor coordinates and lam1 * n on the bias -- the
+    per-observation regularisers of loss_mfitr -- with the block's fixed
+    terms folded into per-rating targets (mcf_mfitr_targets) and the
+    gathered rows [x | 1] built by mcf_mfitr_fixed.  mu stays the train mean
+    (the reference never updates mu, mfitr.py:142 / factor.py:161)."""
+
+    def __init__(self, ratings, graph: TaxonomyGraph, w: np.ndarray, hyper: MfitrHyper, mu: float,
+                 art: np.ndarray, P0, Q0, Qa0=None, b_u=None, b_i=None, b_a=None,
+                 chunk: int | None = None):
+        from .device import DEFAULT_CHUNK, LayoutSolver, SideLayout
+        dev = ratings.device
+        self.r, self.hyper, self.mu, self.device = ratings, hyper, float(mu), dev
+        U, I, D = ratings.num_users, ratings.num_items, int(hyper.D)
+        self.U, self.I, self.D = U, I, D
+        self.ld = _lib.factor_ld(D + 1)
+        z = lambda n: torch.zeros(n, self.ld, dtype=torch.float32, device=dev)  # noqa: E731
+        self.Pa, self.Qa, self.Aa = z(U), z(I), z(I)
+        f32 = lambda a: torch.as_tensor(np.asarray(_host(a), np.float32), device=dev)  # noqa: E731
+        self.Pa[:, :D] = f32(P0)
+        self.Qa[:, :D] = f32(Q0)
+        if Qa0 is not None:
+            self.Aa[:, :D] = f32(Qa0)
+        for t, b in ((self.Pa, b_u), (self.Qa, b_i), (self.Aa, b_a)):
+            if b is not None:
+                t[:, D] = f32(b)
+        self.art_np = np.asarray(art, np.int64)
+        self.art = torch.as_tensor(self.art_np.astype(np.int32), device=dev)
+        self.Xu, self.Xi = z(U), z(I)
+        self.t_items = torch.empty(ratings.nnz, dtype=torch.float32, device=dev)
+        self.t_users = torch.empty(ratings.nnz, dtype=torch.float32, device=dev)
+        # artist layout: the records whose item has an artist, keyed by artist,
+        # partner = user, aux = item (records rebuilt from the users layout)
+        lay = ratings.by_user
+        rec_u = torch.repeat_interleave(torch.arange(U, device=dev, dtype=torch.int32),
+                                        lay.degrees())
+        rec_i, rec_s = lay.idx, lay.val
+        a_of = self.art[rec_i.long()]
+        has = a_of >= 0
+        hu, hi, hs, ha = rec_u[has], rec_i[has], rec_s[has], a_of[has]
+        self.by_artist = SideLayout(ha.contiguous(), hu.contiguous(), hs.contiguous(), I,
+                                    keep_perm=True)
+        self.art_item = hi[self.by_artist.perm.long()].contiguous()
+        self.t_art = torch.empty(self.by_artist.nnz, dtype=torch.float32, device=dev)
+        self.cnt_u = lay.degrees().double()
+        self.cnt_i = ratings.by_item.degrees().double()
+        self.cnt_a = self.by_artist.degrees().double()
+        # taxonomy
+        inc_ptr, inc_edge, inc_other = graph.incident_edges(I)
+        self.inc_ptr = torch.as_tensor(inc_ptr, device=dev)
+        self.inc_edge = torch.as_tensor(inc_edge.astype(np.int32), device=dev)
+        self.inc_other = torch.as_tensor(inc_other.astype(np.int32), device=dev)
+        self.w = torch.as_tensor(np.asarray(w, np.float32), device=dev)
+        self.w64 = torch.as_tensor(np.asarray(w, np.float64), device=dev)
+        self.ec = torch.as_tensor(graph.edge_child, device=dev)
+        self.ep = torch.as_tensor(graph.edge_parent, device=dev)
+        self.layers = [torch.as_tensor(L.astype(np.int32), device=dev) for L in graph.layers(I)]
+        self.S = torch.zeros(I, dtype=torch.float32, device=dev)
+        self.T = torch.zeros(I, self.ld, dtype=torch.float32, device=dev)
+        self.tau = hyper.lam3 + hyper.lam4
+        self.solver = LayoutSolver(D + 1, chunk or DEFAULT_CHUNK)
+        self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
+
+    def _bias(self):
+        return (self.D, 0.0, self.hyper.lam1)
+
+    def _fixed(self, main, add, art, n, out):
+        check(_lib.lib().mcf_mfitr_fixed(ptr(main), ptr(add), ptr(art), n, self.D, ptr(out),
+                                         stream_ptr(self.device)), "mcf_mfitr_fixed")
+
+    def _targets(self, mode, lay, aux, out):
+        check(_lib.lib().mcf_mfitr_targets(mode, ptr(lay.ptr), ptr(lay.idx), ptr(lay.val),
+                                           ptr(aux), lay.n_rows, ptr(self.Pa), ptr(self.Qa),
+                                           ptr(self.Aa), ptr(self.art), self.mu, self.D, ptr(out),
+                                           stream_ptr(self.device)), "mcf_mfitr_targets")
+
+    def _item_prep(self):
+        # [p_u | 1] and the item targets depend only on user / artist blocks
+        self._fixed(self.Pa, None, None, self.U, self.Xu)
+        self._targets(1, self.r.by_item, None, self.t_items)
+
+    def item_layers(self):
+        self._item_prep()
+        for k in range(len(self.layers)):
+            self._solve_layer(k)
+
+    def item_layer(self, k: int):
+        """One taxonomy layer on its own (tests / diagnostics)."""
+        self._item_prep()
+        self._solve_layer(k)
+
+    def _solve_layer(self, k: int):
+        L, h = _lib.lib(), self.hyper
+        rows = self.layers[k]
+        if rows.numel():
+            check(L.mcf_taxonomy_terms(ptr(self.inc_ptr), ptr(self.inc_edge), ptr(self.inc_other),
+                                       ptr(self.w), ptr(self.Qa), self.I, self.D + 1, ptr(rows),
+                                       rows.numel(), ptr(self.S), ptr(self.T),
+                                       stream_ptr(self.device)), "mcf_taxonomy_terms")
+            self.solver.solve(self.r.by_item, self.Xu, self.Qa, 0.0, h.lam2, 0.0, self.S, self.T,
+                              self.tau, rows, ("layer", k), None, self.fail, None,
+                              val=self.t_items, bias=self._bias())
+
+    def artists(self):
+        self._fixed(self.Pa, None, None, self.U, self.Xu)
+        self._targets(2, self.by_artist, self.art_item, self.t_art)
+        self.solver.solve(self.by_artist, self.Xu, self.Aa, 0.0, self.hyper.lam2, fail=self.fail,
+                          val=self.t_art, bias=self._bias())
+
+    def users(self):
+        self._fixed(self.Qa, self.Aa, self.art, self.I, self.Xi)
+        self._targets(0, self.r.by_user, None, self.t_users)
+        self.solver.solve(self.r.by_user, self.Xi, self.Pa, 0.0, self.hyper.lam2, fail=self.fail,
+                          val=self.t_users, bias=self._bias())
+
+    def sweep(self):
+        self.item_layers()
+        self.artists()
+        self.users()
+
+    def check(self):
+        row = int(self.fail.item())
+        self.fail.fill_(-1)
+        if row >= 0:
+            from .errors import SingularSystemError
+            raise SingularSystemError(f"singular MFITR block system at row {row}")
+
+    def params(self):
+        """(P, Q, b_u, b_i, b_a, Q_a) device views."""
+        D = self.D
+        return (self.Pa[:, :D], self.Qa[:, :D], self.Pa[:, D], self.Qa[:, D], self.Aa[:, D],
+                self.Aa[:, :D])
+
+    def _predictor(self):
+        pe = getattr(self, "_pe", None)
+        if pe is None:
+            from .device import DeviceRatings
+            z = torch.zeros(0, dtype=torch.int32, device=self.device)
+            pe = self._pe = AlsEngine(DeviceRatings(z, z, z.float(), self.U, self.I, self.device),
+                                      self.D)
+            pe.Qa_t = torch.zeros_like(pe.Q)
+        P, Q, _, _, _, Qa = self.params()
+        pe.P[:, : self.D] = P
+        pe.Q[:, : self.D] = Q
+        pe.Qa_t[:, : self.D] = Qa
+        return pe
+
+    def predict(self, users, items, truth=None, clip=(-3.0e38, 3.0e38)):
+        """(pred, sse) of the full model through mcf_predict_sse."""
+        pe = self._predictor()
+        bu, bi, ba = (x.contiguous() for x in self.params()[2:5])
+        return pe.predict(users, items, truth, want_pred=truth is None, mu=self.mu, b_u=bu, b_i=bi,
+                          art=self.art, b_a=ba, Q_a=pe.Qa_t, clip=clip)
+
+    def loss(self) -> torch.Tensor:
+        """loss_mfitr with time off (mfitr.py:226-242), on device: the data
+        term through mcf_predict_sse, the per-observation regularisers as
+        count-weighted squared norms, the graph term over the edges."""
+        h, D = self.hyper, self.D
+        lay = self.r.by_user
+        P, Q, bu, bi, ba, Qa = self.params()
+        rec_u = getattr(self, "_rec_u", None)
+        if rec_u is None:
+            rec_u = self._rec_u = torch.repeat_interleave(
+                torch.arange(self.U, device=self.device, dtype=torch.int32), lay.degrees())
+        _, sse = self.predict(rec_u, lay.idx, lay.val)
+        d = lambda x: x.double()  # noqa: E731
+        reg1 = ((self.cnt_u * d(bu) ** 2).sum() + (self.cnt_i * d(bi) ** 2).sum()
+                + (self.cnt_a * d(ba) ** 2).sum())
+        reg2 = ((self.cnt_u * (d(P) ** 2).sum(1)).sum() + (self.cnt_i * (d(Q) ** 2).sum(1)).sum()
+                + (self.cnt_a * (d(Qa) ** 2).sum(1)).sum())
+        d2 = ((d(Q)[self.ec] - d(Q)[self.ep]) ** 2).sum(1)
+        return sse + h.lam1 * reg1 + h.lam2 * reg2 + self.tau * (self.w64 * d2).sum()
+
+
 def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
                 graph: TaxonomyGraph, hyper: MfitrHyper, threads: int = 1, seed: int = 0,
                 binner=None, ew: TaxonomyEdgeWeights | None = None,
                 num_users: int | None = None, num_items: int | None = None, *, init=None,
                 device=None, as_torch: bool = False, objective: bool = True,
+                blocks: str = "full",
                 ) -> tuple[MfitrModel, list[EpochStats]]:
-    """hyper.iters ALS-MFITR sweeps (layered item half-step, then users);
-    one EpochStats row per sweep with loss_mfitr and the clipped validation
-    RMSE (mfitr.py:347-371 signature)."""
+    """hyper.iters ALS-MFITR sweeps; one EpochStats row per sweep with
+    loss_mfitr and the clipped validation RMSE (mfitr.py:347-371 signature).
+
+    blocks="full" (default): every parameter of the reference's MFITR model
+    (mfitr.py:92-149) -- [q_i|b_i] per taxonomy layer, [q_a|b_a] per artist,
+    [p_u|b_u] (MfitrFullSolver); blocks="q": factors only, biases and q_a
+    frozen at 0 (MfitrSolver, the benchmark's configs 2 and 4)."""
     if kind == "time-mfitr":
         raise ConfigError("time-mfitr is outside the device path (no time terms)")
+    if blocks not in ("full", "q"):
+        raise ConfigError(f"blocks must be 'full' or 'q', got {blocks!r}")
     hyper = dataclasses.replace(hyper)
     model = init_mfitr(kind, train_data, graph, hyper, seed, num_users=num_users,
                        num_items=num_items)
-    model.q_a = np.zeros_like(model.q_a)      # minimum scope: artist factors frozen at 0
+    if blocks == "q":
+        model.q_a = np.zeros_like(model.q_a)      # artist factors frozen at 0
     base = model.base
     if init is not None:
         base.p, base.q = np.asarray(init[0], np.float64), np.asarray(init[1], np.float64)
     r = _ratings_for(train_data, device, False, base.num_users, base.num_items)
     if ew is None:
         ew = edge_weights(graph, train_data, device=r.device, num_items=base.num_items)
-    eng = AlsEngine(r, base.D)
-    eng.set_factors(base.p, base.q)
-    base.engine = eng
-    solver = MfitrSolver(eng, graph, ew.w, hyper, base.mu)
-    dev = eng.device
+    dev = r.device
     vu = vi = vs = None
     if validation is not None and len(validation):
         vu = torch.as_tensor(validation.users.astype(np.int32), device=dev)
         vi = torch.as_tensor(validation.items.astype(np.int32), device=dev)
         vs = torch.as_tensor(validation.scores.astype(np.float32), device=dev)
-    art = torch.as_tensor(model.artist_of_item.astype(np.int32), device=dev)
+    clip = (train_data.scale.lo, train_data.scale.hi)
     report = []
+    if blocks == "full":
+        solver = MfitrFullSolver(r, graph, ew.w, hyper, base.mu, model.artist_of_item, base.p,
+                                 base.q, model.q_a, base.b_u, base.b_i, model.b_a)
+        for ep in range(hyper.iters):
+            solver.sweep()
+            base.epochs_done += 1
+            obj = solver.loss() if objective else None
+            rm = None
+            if vu is not None:
+                _, sse = solver.predict(vu, vi, vs, clip=clip)
+                rm = torch.sqrt(sse / vu.numel())
+            solver.check()
+            report.append(EpochStats(ep, hyper.gamma,
+                                     float(obj.item()) if obj is not None else float("nan"),
+                                     float(rm.item()) if rm is not None else float("nan")))
+        P, Q, bu, bi, ba, Qa = solver.params()
+        host = (lambda t: t.clone()) if as_torch else (lambda t: t.double().cpu().numpy())
+        base.p, base.q, model.q_a = host(P), host(Q), host(Qa)
+        base.b_u, base.b_i, model.b_a = (t.double().cpu().numpy() for t in (bu, bi, ba))
+        eng = AlsEngine(r, base.D)       # prediction engine of the fitted model
+        eng.set_factors(P, Q)
+        base.engine = eng
+        model.ew = ew
+        return model, report
+    eng = AlsEngine(r, base.D)
+    eng.set_factors(base.p, base.q)
+    base.engine = eng
+    solver = MfitrSolver(eng, graph, ew.w, hyper, base.mu)
+    art = torch.as_tensor(model.artist_of_item.astype(np.int32), device=dev)
     for ep in range(hyper.iters):
         solver.sweep()
         base.epochs_done += 1
@@ -291,8 +511,7 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
         rm = None
         if vu is not None:
             _, sse = eng.predict(vu, vi, vs, want_pred=False, mu=base.mu, art=art,
-                                 Q_a=torch.zeros_like(eng.Q),
-                                 clip=(train_data.scale.lo, train_data.scale.hi))
+                                 Q_a=torch.zeros_like(eng.Q), clip=clip)
             rm = torch.sqrt(sse / vu.numel())
         eng.check()
         report.append(EpochStats(ep, hyper.gamma,

@@ -29,7 +29,8 @@ Fixtures (reference entry point -> file):
   taxonomy.npz       synth.build_taxonomy, taxonomy.load_taxonomy (artist
                      inheritance), taxonomy.build_graph on this repo's MFITR
                      generator: edge lists and artist_array
-  mfitr.npz          mfitr.edge_weights, loss_mfitr, grad_mfitr on a small
+  mfitr.npz          mfitr.edge_weights, loss_mfitr, grad_mfitr (every group:
+                     p, q, b_u, b_i, b_a, q_a) on a small
                      synth.generate_synthetic instance with random parameters
   mfitr_cfg2s.npz    config-2 shaped workload (this repo's generator, scaled):
                      reference edge weights, loss_mfitr, grad_mfitr
@@ -267,7 +268,8 @@ def mfitr_fx():
                         ep=g.edge_parent, w=ew.w, P=m.base.p, Q=m.base.q, Qa=m.q_a, ba=m.b_a,
                         bu=m.base.b_u, bi=m.base.b_i, mu=m.base.mu, art=m.artist_of_item,
                         lam1=h.lam1, lam2=h.lam2, lam3=h.lam3, lam4=h.lam4, loss=loss,
-                        grad_p=grad["p"], grad_q=grad["q"])
+                        grad_p=grad["p"], grad_q=grad["q"], grad_bu=grad["b_u"],
+                        grad_bi=grad["b_i"], grad_ba=grad["b_a"], grad_qa=grad["q_a"])
 
 
 def mfitr_cfg2s():
@@ -347,6 +349,11 @@ def formats():
 
 
 def main():
+    only = sys.argv[1:]
+    if only:   # regenerate just the named fixtures, e.g. `make_golden.py mfitr_fx`
+        for name in only:
+            globals()[name]()
+        return
     with open(os.path.join(HERE, "spec_scalars.json"), "w") as fh:
         json.dump(spec_scalars(), fh, indent=1)
     als_small()

@@ -140,6 +140,107 @@ def test_train_mfitr_drop_in(golden):
     assert np.all(np.isfinite(objs)) and np.all(np.diff(objs) <= 1e-5 * objs[:-1])
     m = tm.model
     pred = tm.predict(g["users"][:500], g["items"][:500])
-    ref = oracle.predict(m.base.p, m.base.q, g["users"][:500], g["items"][:500], mu=m.base.mu)
+    ref = oracle.predict(m.base.p, m.base.q, g["users"][:500], g["items"][:500], mu=m.base.mu,
+                         b_u=m.base.b_u, b_i=m.base.b_i,
+                         arts=m.artist_of_item[g["items"][:500]],   # per query (mf_predict_batch)
+                         b_a=m.b_a, Q_a=m.q_a)
     assert np.abs(pred - ref).max() < 1e-4 * np.abs(ref).max()
     assert np.array_equal(tm.model.ew.w, g["w"])
+    # the full model trains every block (biases and artist offsets move)
+    assert np.abs(m.base.b_u).max() > 0 and np.abs(m.q_a).max() > 0
+    # the reported objective is the oracle's loss_mfitr of the returned model
+    u, i = g["users"].astype(np.int64), g["items"].astype(np.int64)
+    ref_loss = oracle.loss_mfitr(m.base.p, m.base.q, u, i, g["scores"], m.base.mu, m.base.b_u,
+                                 m.base.b_i, m.artist_of_item, m.b_a, m.q_a, g["ec"], g["ep"],
+                                 g["w"], h.lam1, h.lam2, h.lam3, h.lam4)
+    assert abs(objs[-1] - ref_loss) < 1e-4 * ref_loss
+
+
+def test_train_mfitr_q_blocks_only(golden):
+    from paper_1108_2580_b200 import mfitr
+    g = golden("mfitr_cfg2s.npz")
+    h = mfitr.MfitrHyper(D=8, lam1=0.0, lam2=0.065, lam3=0.1, lam4=0.1, iters=3)
+    m, rep = mfitr.train_mfitr("mfitr", _train(g), None, _graph(g), h, blocks="q")
+    assert np.all(m.base.b_u == 0) and np.all(m.q_a == 0)
+    objs = np.array([r.objective for r in rep])
+    assert np.all(np.diff(objs) <= 1e-5 * objs[:-1])
+
+
+def _full_solver(g, D=None):
+    from paper_1108_2580_b200.device import DeviceRatings
+    from paper_1108_2580_b200 import mfitr
+    graph = _graph(g)
+    U, I = int(g["U"]), int(g["I"])
+    D = D or g["P"].shape[1]
+    h = mfitr.MfitrHyper(D=D, lam1=float(g["lam1"]), lam2=float(g["lam2"]),
+                         lam3=float(g["lam3"]), lam4=float(g["lam4"]))
+    r = DeviceRatings(g["users"], g["items"], g["scores"], U, I, dev())
+    return mfitr.MfitrFullSolver(r, graph, g["w"], h, float(g["mu"]), g["art"], g["P"], g["Q"],
+                                 g["Qa"], g["bu"], g["bi"], g["ba"], chunk=64)
+
+
+def _host_params(fs):
+    return [t.double().cpu().numpy() for t in fs.params()]
+
+
+@pytest.mark.parametrize("fixture,D", [("mfitr.npz", None), ("mfitr_cfg2s.npz", None),
+                                       ("mfitr_cfg2s.npz", 24), ("mfitr_cfg2s.npz", 40)])
+def test_full_blocks_zero_gradient_and_monotone(golden, fixture, D):
+    """MFITR full blocks: every block solve is exact, so the
+    reference's own gradient (grad_mfitr, restated in oracle/ and pinned to
+    the reference's values) of the solved block vanishes, and loss_mfitr
+    never increases; the device loss matches the oracle's."""
+    g = golden(fixture)
+    if "Qa" not in g.files:   # cfg2s fixture: start from its factors, biases / q_a at 0
+        g = dict(g)
+        g["Qa"] = np.zeros_like(g["Q"])
+        g["bu"], g["bi"], g["ba"] = np.zeros(int(g["U"])), np.zeros(int(g["I"])), np.zeros(int(g["I"]))
+        g["lam1"] = 0.01
+    if D is not None:   # wider factors: the warp (D+1 <= 28) and tile-warp paths
+        rng = np.random.default_rng(D)
+        g["P"] = rng.normal(0, 0.1, (int(g["U"]), D))
+        g["Q"] = rng.normal(0, 0.1, (int(g["I"]), D))
+        g["Qa"] = np.zeros_like(g["Q"])
+    fs = _full_solver(g)
+    u, i = g["users"].astype(np.int64), g["items"].astype(np.int64)
+    s = g["scores"].astype(np.float64)
+    lam = [float(g[k]) for k in ("lam1", "lam2", "lam3", "lam4")]
+
+    def terms():
+        P, Q, bu, bi, ba, Qa = _host_params(fs)
+        a = (P, Q, u, i, s, float(g["mu"]), bu, bi, g["art"], ba, Qa, g["ec"], g["ep"], g["w"],
+             *lam)
+        return oracle.loss_mfitr(*a), oracle.grad_mfitr(*a)
+
+    loss0, gr0 = terms()
+    scale = {k: max(np.abs(v).max(), 1e-12) for k, v in gr0.items()}
+    dev_loss = float(fs.loss().item())
+    assert abs(dev_loss - loss0) < 1e-4 * abs(loss0), (dev_loss, loss0)
+    prev = loss0
+    arts = np.unique(g["art"][g["art"] >= 0])
+    for k, layer in enumerate(fs.layers):
+        rows = layer.cpu().numpy()
+        if rows.size == 0:
+            continue
+        fs.item_layer(k)
+        fs.check()
+        loss, gr = terms()
+        assert loss <= prev * (1 + 1e-6), ("items layer", loss, prev)
+        prev = loss
+        assert np.abs(gr["q"][rows]).max() < 1e-4 * scale["q"]
+        assert np.abs(gr["b_i"][rows]).max() < 1e-4 * scale["b_i"]
+    fs.artists()
+    fs.check()
+    loss, gr = terms()
+    assert loss <= prev * (1 + 1e-6), ("artists", loss, prev)
+    prev = loss
+    assert np.abs(gr["q_a"][arts]).max() < 1e-4 * scale["q_a"]
+    assert np.abs(gr["b_a"][arts]).max() < 1e-4 * scale["b_a"]
+    fs.users()
+    fs.check()
+    loss, gr = terms()
+    assert loss <= prev * (1 + 1e-6), ("users", loss, prev)
+    assert np.abs(gr["p"]).max() < 1e-4 * scale["p"]
+    assert np.abs(gr["b_u"]).max() < 1e-4 * scale["b_u"]
+    dev_loss = float(fs.loss().item())
+    assert abs(dev_loss - loss) < 1e-4 * abs(loss), (dev_loss, loss)

@@ -128,6 +128,9 @@ def test_mfitr_weights_loss_grad(golden):
     gr = oracle.grad_mfitr(*args)
     np.testing.assert_allclose(gr["p"], g["grad_p"], rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(gr["q"], g["grad_q"], rtol=1e-12, atol=1e-12)
+    # bias and artist groups too (the MFITR full-block solver's optimality oracle)
+    for k, f in (("b_u", "grad_bu"), ("b_i", "grad_bi"), ("b_a", "grad_ba"), ("q_a", "grad_qa")):
+        np.testing.assert_allclose(gr[k], g[f], rtol=1e-12, atol=1e-12)
 
 
 def test_mfitr_cfg2_shape_weights_loss_grad(golden):
