@@ -432,12 +432,18 @@ def run_mfitr(args, cfg, wl, t_gen):
     ew = mfitr.edge_weights(wl.graph, tr, device=dev, num_items=cfg.items)
     torch.cuda.synchronize()
     t_layout = time.perf_counter() - t0
-    eng = AlsEngine(r, cfg.D)
     P0, Q0 = synth.init_factors(cfg.users, cfg.items, cfg.D, seed=1)
-    eng.set_factors(P0, Q0)
-    h = mfitr.MfitrHyper(D=cfg.D, lam1=0.0, lam2=cfg.lam, lam3=cfg.tax_weight,
-                         lam4=cfg.tax_weight, iters=cfg.sweeps)
-    solver = mfitr.MfitrSolver(eng, wl.graph, ew.w, h, r.global_mean)
+    full = args.mfitr_blocks == "full"
+    h = mfitr.MfitrHyper(D=cfg.D, lam1=cfg.lam if full else 0.0, lam2=cfg.lam,
+                         lam3=cfg.tax_weight, lam4=cfg.tax_weight, iters=cfg.sweeps)
+    if full:   # every block: [q|b_i] layers, [q_a|b_a] artists, [p|b_u] users (D+1 solves)
+        art = wl.graph.artist_array(cfg.items)
+        solver = mfitr.MfitrFullSolver(r, wl.graph, ew.w, h, r.global_mean, art, P0, Q0)
+        eng = solver
+    else:
+        eng = AlsEngine(r, cfg.D)
+        eng.set_factors(P0, Q0)
+        solver = mfitr.MfitrSolver(eng, wl.graph, ew.w, h, r.global_mean)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
         solver.sweep()
@@ -463,9 +469,12 @@ def run_mfitr(args, cfg, wl, t_gen):
                         ms / 1000.0, kernel=kernel_name(cfg.D) + " per item layer + users; "
                         "k_tax_terms per layer")
     roof["per"] = "sweep"
-    art = torch.as_tensor(wl.graph.artist_array(cfg.items).astype(np.int32), device=dev)
-    _, sse = eng.predict(wl.valid_users, wl.valid_items, wl.valid_scores, want_pred=False,
-                         mu=r.global_mean, art=art, Q_a=torch.zeros_like(eng.Q))
+    if full:
+        _, sse = solver.predict(wl.valid_users, wl.valid_items, wl.valid_scores)
+    else:
+        art = torch.as_tensor(wl.graph.artist_array(cfg.items).astype(np.int32), device=dev)
+        _, sse = eng.predict(wl.valid_users, wl.valid_items, wl.valid_scores, want_pred=False,
+                             mu=r.global_mean, art=art, Q_a=torch.zeros_like(eng.Q))
     rm = float(torch.sqrt(sse / wl.valid_users.numel()).item())
     line = {"metric": "MFITR ratings/sec per full sweep", "value": nnz / (ms / 1000.0),
             "unit": "ratings/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -473,9 +482,12 @@ def run_mfitr(args, cfg, wl, t_gen):
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator, BASELINE config shapes)",
             "config": {"workload": cfg.name, "users": cfg.users, "items": cfg.items,
-                       "nnz_train": nnz, "D": cfg.D, "lambda2": cfg.lam,
+                       "nnz_train": nnz, "D": cfg.D, "lambda1": h.lam1, "lambda2": cfg.lam,
                        "lambda3": cfg.tax_weight, "lambda4": cfg.tax_weight,
-                       "edges": E, "step": "one ALS-MFITR sweep: 4 item layers + users"},
+                       "edges": E, "blocks": args.mfitr_blocks,
+                       "step": "one ALS-MFITR sweep: 4 item layers + users" + (
+                           " + artists; [f|b] blocks, D+1 unknowns" if full else
+                           "; factors only (biases, q_a frozen at 0)")},
             "roofline": roof,
             "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clk.summary(),
             "valid_rmse_after": rm, "layout_build_s": t_layout, "datagen_s": t_gen}
@@ -563,6 +575,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--mfitr-blocks", choices=["q", "full"], default="q",
+                    help="configs 2/4: factor blocks only (default) or every MFITR block")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

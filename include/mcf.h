@@ -137,7 +137,7 @@ int mcf_als_half_step_bias(const int64_t *ptr, const int32_t *idx, const float *
  * (users step: main = Q, add = artist table; items / artists steps: main = P).
  * mcf_mfitr_targets: per-rating targets of one layout in CSR order,
  *   mode 0 (users layout, partner = item i):  r - mu - b_i - b_a[art(i)]
- *   mode 1 (items layout, row = item i, partner = user u):
+ *   mode 1 (items layout, row = item i, partner = user u, aux = i per rating):
  *                       r - mu - b_u - [art(i) >= 0] (b_a + q_a . p_u)
  *   mode 2 (artists layout, row = artist, partner = user u, aux = item i):
  *                       r - mu - b_u - b_i - q_i . p_u

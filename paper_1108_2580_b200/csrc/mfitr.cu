@@ -42,45 +42,61 @@ __global__ void k_mfitr_fixed(const float *main_t, const float *add_t, const int
     }
 }
 
-// per-rating targets of one layout, warp per row, ratings in CSR order.
-// mode 0 users (row u, partner i), 1 items (row i, partner u),
-// 2 artists (row a, partner u, item = aux[k]).
+// dot of the first D floats of two 16-byte aligned rows (column D onwards
+// holds the bias / padding and is excluded), float4 loads
+__device__ __forceinline__ float dot_d(const float *a, const float *b, int D) {
+    const float4 *a4 = reinterpret_cast<const float4 *>(a);
+    const float4 *b4 = reinterpret_cast<const float4 *>(b);
+    float d = 0.f;
+    const int nf = D >> 2;
+    for (int c = 0; c < nf; ++c) {
+        const float4 x = a4[c], y = b4[c];
+        d = fmaf(x.x, y.x, d);
+        d = fmaf(x.y, y.y, d);
+        d = fmaf(x.z, y.z, d);
+        d = fmaf(x.w, y.w, d);
+    }
+    const int rem = D & 3;
+    if (rem) {
+        const float4 x = a4[nf], y = b4[nf];
+        d = fmaf(x.x, y.x, d);
+        if (rem > 1) d = fmaf(x.y, y.y, d);
+        if (rem > 2) d = fmaf(x.z, y.z, d);
+    }
+    return d;
+}
+
+// per-rating targets of one layout, thread per rating (a warp per row
+// serialised the Zipf-hot rows), ratings in CSR order.
+// mode 0 users (partner i), 1 items (partner u, aux = row item),
+// 2 artists (partner u, aux = item).
 __global__ void k_mfitr_targets(int mode, const int64_t *ptr, const int32_t *idx,
                                 const float *val, const int32_t *aux, int32_t n_rows,
                                 const float *Pa, const float *Qa, const float *Aa,
                                 const int32_t *art, float mu, int D, int ld, float *out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows;
-         r += warps) {
-        const int64_t a = ptr[r], b = ptr[r + 1];
-        const int ar = mode == 1 ? art[r] : -1;   // items: the row's artist
-        for (int64_t k = a + lane; k < b; k += 32) {
-            const int j = idx[k];
-            float t = val[k] - mu;
-            if (mode == 0) {            // j = item
-                t -= Qa[(size_t)j * ld + D];
-                const int aj = art[j];
-                if (aj >= 0) t -= Aa[(size_t)aj * ld + D];
-            } else if (mode == 1) {     // j = user, row = item
-                t -= Pa[(size_t)j * ld + D];
-                if (ar >= 0) {
-                    const float *qa = Aa + (size_t)ar * ld;
-                    const float *pu = Pa + (size_t)j * ld;
-                    float d = qa[D];
-                    for (int c = 0; c < D; ++c) d = fmaf(qa[c], pu[c], d);
-                    t -= d;
-                }
-            } else {                    // j = user, row = artist, aux = item
-                const int i = aux[k];
-                const float *qi = Qa + (size_t)i * ld;
-                const float *pu = Pa + (size_t)j * ld;
-                float d = pu[D] + qi[D];
-                for (int c = 0; c < D; ++c) d = fmaf(qi[c], pu[c], d);
-                t -= d;
+    const int64_t nnz = ptr[n_rows];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int j = idx[k];
+        float t = val[k] - mu;
+        if (mode == 0) {            // j = item
+            t -= Qa[(size_t)j * ld + D];
+            const int aj = art[j];
+            if (aj >= 0) t -= Aa[(size_t)aj * ld + D];
+        } else if (mode == 1) {     // j = user, aux = the row's item
+            const float *pu = Pa + (size_t)j * ld;
+            t -= pu[D];
+            const int ar = art[aux[k]];
+            if (ar >= 0) {
+                const float *qa = Aa + (size_t)ar * ld;
+                t -= qa[D] + dot_d(qa, pu, D);
             }
-            out[k] = t;
+        } else {                    // j = user, aux = item
+            const float *qi = Qa + (size_t)aux[k] * ld;
+            const float *pu = Pa + (size_t)j * ld;
+            t -= pu[D] + qi[D] + dot_d(qi, pu, D);
         }
+        out[k] = t;
     }
 }
 
@@ -110,14 +126,14 @@ extern "C" int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t
                                  const int32_t *art, float mu, int32_t D, float *out,
                                  void *stream) {
     if (mode < 0 || mode > 2 || !ptr || !out || n_rows < 0 || D < 1 || D + 1 > 128 ||
-        (mode == 0 && (!Qa || !Aa || !art)) || (mode == 1 && (!Pa || !Aa || !art)) ||
+        (mode == 0 && (!Qa || !Aa || !art)) || (mode == 1 && (!Pa || !Aa || !art || !aux)) ||
         (mode == 2 && (!Pa || !Qa || !aux))) {
         set_error("mcf_mfitr_targets: invalid arguments");
         return MCF_E_ARG;
     }
     if (n_rows == 0) return MCF_OK;
     const int ld = mcf_factor_ld(D + 1);
-    const int grid = (int)std::min<int64_t>(ceil_div((int64_t)n_rows, 8), 148 * 16);
+    const int grid = 148 * 16;   // grid-stride over the layout's ratings
     k_mfitr_targets<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         mode, ptr, idx, val, aux, n_rows, Pa, Qa, Aa, art, mu, D, ld, out);
     return check_launch("mcf_mfitr_targets");

@@ -293,6 +293,10 @@ class MfitrFullSolver:
         self.art = torch.as_tensor(self.art_np.astype(np.int32), device=dev)
         self.Xu, self.Xi = z(U), z(I)
         self.t_items = torch.empty(ratings.nnz, dtype=torch.float32, device=dev)
+        # item id of every rating of the items layout (the targets kernel runs
+        # thread per rating)
+        self.item_rows = torch.repeat_interleave(torch.arange(I, device=dev, dtype=torch.int32),
+                                                 ratings.by_item.degrees())
         self.t_users = torch.empty(ratings.nnz, dtype=torch.float32, device=dev)
         # artist layout: the records whose item has an artist, keyed by artist,
         # partner = user, aux = item (records rebuilt from the users layout)
@@ -342,7 +346,7 @@ class MfitrFullSolver:
     def _item_prep(self):
         # [p_u | 1] and the item targets depend only on user / artist blocks
         self._fixed(self.Pa, None, None, self.U, self.Xu)
-        self._targets(1, self.r.by_item, None, self.t_items)
+        self._targets(1, self.r.by_item, self.item_rows, self.t_items)
 
     def item_layers(self):
         self._item_prep()
