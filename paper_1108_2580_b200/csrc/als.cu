@@ -976,15 +976,22 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
     // staged row layout, "split halves": the low 4 floats of 8-block I sit
     // in 16-byte unit I, the high 4 in unit NB8 + I, so the a-side loads of
     // 8 lanes holding consecutive block rows I hit 8 distinct bank groups
+    // lane pair (2 rr, 2 rr + 1) copies row rr: lane h takes the 16-byte
+    // parts h, h+2, ... (adjacent parts in one instruction -> one 32-byte
+    // sector), i.e. unit j (h = 0) or NB8 + j (h = 1) of the split halves
+    static_assert(BT == 16, "one lane pair per staged row");
     auto issue = [&](int id, float y, float w, float *stage) {
         float *ys = stage + BT * C::ROWS;
-        for (int e = lane; e < BT * (LDK / 4); e += 32) {
-            const int rr = e / (LDK / 4), part = e - rr * (LDK / 4);
+        {
+            const int rr = lane >> 1, h = lane & 1;
             const int rid = __shfl_sync(FULL, id, rr);
-            const bool ok = rid >= 0 && part < nb4_real;
-            const float *g = ok ? p.fixed + (size_t)rid * p.ld + part * 4 : p.fixed;
-            const int unit = (part & 1) ? NB8 + (part >> 1) : (part >> 1);
-            cp_async16(stage + rr * C::ROWS + unit * 4, g, ok ? 16 : 0);
+            const float *g = p.fixed + (size_t)(rid >= 0 ? rid : 0) * p.ld + 4 * h;
+            float *dst = stage + rr * C::ROWS + 4 * NB8 * h;
+#pragma unroll
+            for (int j = 0; j < NB8; ++j) {
+                const bool ok = rid >= 0 && 2 * j + h < nb4_real;
+                cp_async16(dst + 4 * j, g + 8 * j, ok ? 16 : 0);
+            }
         }
         if (lane < BT) {
             ys[lane] = id >= 0 ? y - p.y_shift : 0.f;
