@@ -44,6 +44,16 @@ def test_host_only_queries():
     assert L.mcf_als_half_step(None, None, None, None, None, 0, None, 0, 0, 0, 0, None, None, 0,
                                None, 0, 0, 32, None, None, None, None, None, 0, None) == -5
     assert b"D must be" in L.mcf_last_error()
+    # the bias-coordinate variant rejects a negative bias dimension, and the
+    # MFITR block helpers reject missing tables, before touching the device
+    assert L.mcf_als_half_step_bias(None, None, None, None, None, 0, None, 21, 0, 0, 0, None,
+                                    None, 0, None, 0, 0, 32, None, None, None, None, 0, -1, 0,
+                                    0, None) != 0
+    assert b"bias_dim" in L.mcf_last_error()
+    assert L.mcf_mfitr_fixed(None, None, None, 10, 20, None, None) != 0
+    assert L.mcf_mfitr_targets(1, None, None, None, None, 10, None, None, None, None, 0.0, 20,
+                               None, None) != 0
+    assert b"mcf_mfitr_targets" in L.mcf_last_error()
 
 
 def test_no_cuda_means_loud_failure():
