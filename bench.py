@@ -290,7 +290,9 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     nnz = wl.nnz
-    if world > 1:
+    if world > 1 or args.force_sharded:
+        if cfg.taxonomy is not None:
+            return run_sharded_mfitr(args, rank, world, cfg, wl, t_gen)
         return run_sharded(args, rank, world, cfg, wl, t_gen)
     if cfg.taxonomy is not None:
         return run_mfitr(args, cfg, wl, t_gen)
@@ -494,6 +496,78 @@ def run_mfitr(args, cfg, wl, t_gen):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded_mfitr(args, rank, world, cfg, wl, t_gen):
+    """Configs 2 / 4 at N > 1: users cut at nnz quantiles, items assigned by
+    whole taxonomy subtree (no exchange inside the layered item half-step),
+    one in-place NCCL all-gather per half-step (parallel.ShardedMfitr).
+    Strong scaling: the same workload for every N."""
+    from paper_1108_2580_b200 import mfitr
+    from paper_1108_2580_b200.device import DeviceRatings
+    from paper_1108_2580_b200.parallel import ShardedMfitr
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    # edge weights from the full ratings (every rank computes the same, bit-exact)
+    r = DeviceRatings(wl.train_users, wl.train_items, wl.train_scores, cfg.users, cfg.items, dev)
+    tr = wl.train_dataset()
+    tr.__dict__["_device_cache"] = {(str(dev), cfg.users, cfg.items): r}
+    ew = mfitr.edge_weights(wl.graph, tr, device=dev, num_items=cfg.items)
+    mu = r.global_mean
+    del r, tr
+    torch.cuda.empty_cache()
+    run = ShardedMfitr(wl.train_users, wl.train_items, wl.train_scores, cfg.users, cfg.items,
+                       cfg.D, wl.graph, ew.w, cfg.lam, 2 * cfg.tax_weight, mu, device=dev)
+    torch.cuda.synchronize()
+    t_layout = time.perf_counter() - t0
+    P0, Q0 = synth.init_factors(cfg.users, cfg.items, cfg.D, seed=1)
+    run.set_factors(P0, Q0)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        run.sweep()
+    run.check()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(dev.index) as clk:
+        time.sleep(0.2)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev[0].record(stream)
+        for s in range(args.steps):
+            run.sweep()
+            ev[s + 1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    run.check()
+    ms = max_over_ranks(ev[0].elapsed_time(ev[-1]) / args.steps, world)
+    nnz = wl.nnz
+    D = cfg.D
+    local = run.nnz_local["items"] + run.nnz_local["users"]
+    roof = roofline_for(D, local * (4 * D + 8), local * (D * D + 3 * D), ms / 1000.0,
+                        kernel=kernel_name(D) + " per rank: 4 item layers + users; "
+                        "k_tax_terms; all-gather")
+    roof["per"] = "sweep (this rank's ratings)"
+    if rank == 0:
+        line = {"metric": "MFITR ratings/sec per full sweep", "value": nnz / (ms / 1000.0),
+                "unit": "ratings/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded generator, BASELINE config shapes)",
+                "config": {"workload": cfg.name, "users": cfg.users, "items": cfg.items,
+                           "nnz_train": nnz, "D": D, "lambda2": cfg.lam,
+                           "lambda3": cfg.tax_weight, "lambda4": cfg.tax_weight,
+                           "edges": wl.graph.num_edges, "blocks": "q",
+                           "step": "one ALS-MFITR sweep incl. the all-gather after each half-step",
+                           "parallelism": f"users nnz-balanced, items by taxonomy subtree (LPT) "
+                                          f"over {world} GPU(s)"},
+                "roofline": roof, "cpu_baseline": None, "e2e": None,
+                "gpu_launches": None, "clocks": clk.summary(), "layout_build_s": t_layout,
+                "datagen_s": t_gen, "nnz_local_rank0": run.nnz_local}
+        print(json.dumps(line), flush=True)
+
+
 def run_sharded(args, rank, world, cfg, wl, t_gen):
     """N > 1: users and items sharded at nnz quantiles, opposite factor
     replicated, in-place NCCL all-gather of the solved shard after every
@@ -514,12 +588,14 @@ def run_sharded(args, rank, world, cfg, wl, t_gen):
         run.sweep(0.0, lam)
     run.check()
     torch.cuda.synchronize()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
     with ClockSampler(dev.index) as clk:
         time.sleep(0.2)
         torch.cuda.synchronize()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
         ev[0].record(stream)
         for s in range(args.steps):
             run.half_step("items", 0.0, lam)
@@ -527,7 +603,8 @@ def run_sharded(args, rank, world, cfg, wl, t_gen):
             run.half_step("users", 0.0, lam)
             ev[2 * s + 2].record(stream)
         torch.cuda.synchronize()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
     run.check()
     total_ms = ev[0].elapsed_time(ev[-1])
     ms_per_step = max_over_ranks(total_ms / args.steps, world)
@@ -575,6 +652,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the multi-GPU runner even at N = 1 (exercises its host logic)")
     ap.add_argument("--mfitr-blocks", choices=["q", "full"], default="q",
                     help="configs 2/4: factor blocks only (default) or every MFITR block")
     args = ap.parse_args()

@@ -173,3 +173,188 @@ class _HostLayout:
         self.idx = cols[order]
         self.val = vals[order]
         self.nnz = int(keys.numel())
+
+
+# ---------------------------------------------------------------------------
+# ALS-MFITR sharding: items cut at taxonomy-subtree boundaries
+
+def subtree_components(graph, num_items: int) -> np.ndarray:
+    """Component label per item of the taxonomy forest (an artist with its
+    albums and tracks; items off the graph are singletons).  Every edge of
+    the graph term (taxonomy.py:106-118) stays inside one component, so a
+    rank that owns whole components solves its layered item half-step
+    without any cross-rank exchange."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    E = int(graph.edge_child.size)
+    A = coo_matrix((np.ones(E, dtype=np.int8), (graph.edge_child, graph.edge_parent)),
+                   shape=(num_items, num_items))
+    _, lab = connected_components(A, directed=False)
+    return lab.astype(np.int64)
+
+
+def lpt_owner(weights: np.ndarray, world: int) -> np.ndarray:
+    """Longest-processing-time assignment of weighted units to `world`
+    ranks (heaviest first onto the least-loaded rank; ties by unit id and
+    rank id), deterministic."""
+    import heapq
+    n = int(weights.size)
+    order = np.lexsort((np.arange(n), -weights))
+    heap = [(0, r) for r in range(world)]
+    owner = np.empty(n, dtype=np.int64)
+    for c in order:
+        load, r = heapq.heappop(heap)
+        owner[c] = r
+        heapq.heappush(heap, (load + int(weights[c]), r))
+    return owner
+
+
+class PermMap:
+    """Padded shard numbering for an arbitrary row -> rank assignment: rank
+    r's rows (ascending id) occupy [r*S, r*S + n_r) of a [world*S] table."""
+
+    def __init__(self, owner: np.ndarray, world: int, device):
+        owner = np.asarray(owner, np.int64)
+        self.world, self.n = int(world), int(owner.size)
+        counts = np.bincount(owner, minlength=world)
+        self.counts = counts
+        self.S = max(1, int(counts.max())) if self.n else 1
+        self.rows = self.world * self.S
+        order = np.lexsort((np.arange(self.n), owner))           # by rank, then id
+        local = np.empty(self.n, dtype=np.int64)
+        starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
+        local[order] = np.arange(self.n) - np.repeat(starts, counts)
+        self.owner, self.local = owner, local
+        self.padded_np = owner * self.S + local
+        self.padded = torch.as_tensor(self.padded_np, device=device)
+
+    def to_padded(self, ids: torch.Tensor) -> torch.Tensor:
+        return self.padded[ids.to(torch.int64)].to(torch.int32)
+
+    def padded_index(self) -> torch.Tensor:
+        return self.padded
+
+
+class ShardedMfitr:
+    """One rank's part of a sharded ALS-MFITR fit (factor blocks; biases and
+    q_a at 0, as MfitrSolver): users cut at nnz quantiles, items assigned by
+    whole taxonomy subtree (LPT on their ratings), the layered item
+    half-step solved locally with S/T from the local subtrees, one in-place
+    all-gather per half-step.  Results are identical for any world size."""
+
+    def __init__(self, users, items, scores, num_users: int, num_items: int, D: int, graph,
+                 w, lam2: float, tau: float, mu: float, *, group=None, solver="device",
+                 device=None, chunk: int | None = None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.D, self.ld = int(D), _lib.factor_ld(D)
+        self.lam2, self.tau, self.mu = float(lam2), float(tau), float(mu)
+        if solver == "device":
+            from .device import DEFAULT_CHUNK, LayoutSolver, cuda_device
+            dev = cuda_device(device)
+            self._solver = LayoutSolver(D, chunk or DEFAULT_CHUNK)
+        else:
+            dev = torch.device(device or "cpu")
+            self._solver = solver
+        self.device = dev
+        u = torch.as_tensor(users).to(dev, torch.int64)
+        it = torch.as_tensor(items).to(dev, torch.int64)
+        s = torch.as_tensor(scores).to(dev, torch.float32)
+        self.num_users, self.num_items = int(num_users), int(num_items)
+        self.umap = ShardMap(nnz_balanced_cuts(torch.bincount(u, minlength=num_users), self.world))
+        comp = subtree_components(graph, num_items)
+        deg = torch.bincount(it, minlength=num_items).cpu().numpy()
+        cw = np.bincount(comp, weights=deg, minlength=int(comp.max()) + 1 if comp.size else 0)
+        self.imap = PermMap(lpt_owner(cw.astype(np.int64), self.world)[comp], self.world, dev)
+        self.P = torch.zeros(self.umap.rows, self.ld, dtype=torch.float32, device=dev)
+        self.Q = torch.zeros(self.imap.rows, self.ld, dtype=torch.float32, device=dev)
+        lo, hi = self.umap.range(self.rank)
+        m = (u >= lo) & (u < hi)
+        mk = ShardedAls._make_layout
+        self.local = {"users": mk(self, (u[m] - lo).to(torch.int32), self.imap.to_padded(it[m]),
+                                  s[m], hi - lo)}
+        own = torch.as_tensor(self.imap.owner, device=dev)[it] == self.rank
+        loc = torch.as_tensor(self.imap.local, device=dev)
+        n_mine = int(self.imap.counts[self.rank])
+        self.local["items"] = mk(self, loc[it[own]].to(torch.int32), self.umap.to_padded(u[own]),
+                                 s[own], n_mine)
+        self.nnz_local = {k: int(v.nnz) for k, v in self.local.items()}
+        # taxonomy in padded item ids: incident-edge CSR (edge-list order per
+        # item, as TaxonomyGraph.incident_edges), edge weights
+        pc, pp = self.imap.padded_np[graph.edge_child], self.imap.padded_np[graph.edge_parent]
+        E = int(pc.size)
+        ends, other = np.concatenate([pc, pp]), np.concatenate([pp, pc])
+        eid = np.concatenate([np.arange(E), np.arange(E)])
+        order = np.argsort(ends, kind="stable")
+        inc_ptr = np.zeros(self.imap.rows + 1, dtype=np.int64)
+        np.cumsum(np.bincount(ends, minlength=self.imap.rows), out=inc_ptr[1:])
+        self.inc = (torch.as_tensor(inc_ptr, device=dev),
+                    torch.as_tensor(eid[order].astype(np.int32), device=dev),
+                    torch.as_tensor(other[order].astype(np.int32), device=dev))
+        self.w = torch.as_tensor(np.asarray(w, np.float32), device=dev)
+        self.edges_padded = (pc, pp, np.asarray(w, np.float64))
+        # my rows of each layer: local and padded indices
+        mine = self.imap.owner == self.rank
+        self.layers = []
+        for L in graph.layers(num_items):
+            Lm = L[mine[L]]
+            loc_rows = np.sort(self.imap.local[Lm])
+            self.layers.append((torch.as_tensor(loc_rows.astype(np.int32), device=dev),
+                                torch.as_tensor((self.rank * self.imap.S + loc_rows)
+                                                .astype(np.int32), device=dev)))
+        self.S_t = torch.zeros(self.imap.rows, dtype=torch.float32, device=dev)
+        self.T_t = torch.zeros(self.imap.rows, self.ld, dtype=torch.float32, device=dev)
+
+    # -- factors -------------------------------------------------------------
+    def set_factors(self, P=None, Q=None):
+        for dst, src, idx in ((self.P, P, self.umap.padded_index()),
+                              (self.Q, Q, self.imap.padded_index())):
+            if src is None:
+                continue
+            t = torch.as_tensor(np.asarray(src) if not isinstance(src, torch.Tensor) else src)
+            dst.zero_()
+            dst[idx, : self.D] = t.to(self.device, torch.float32)
+
+    def factors(self):
+        return (self.P[self.umap.padded_index(), : self.D],
+                self.Q[self.imap.padded_index(), : self.D])
+
+    # -- sweep ---------------------------------------------------------------
+    def _terms(self, padded_rows):
+        if self._solver.__class__.__name__ == "LayoutSolver":
+            from ._lib import check, ptr
+            from .device import stream_ptr
+            ip, ie, io = self.inc
+            check(_lib.lib().mcf_taxonomy_terms(ptr(ip), ptr(ie), ptr(io), ptr(self.w),
+                                                ptr(self.Q), self.imap.rows, self.D,
+                                                ptr(padded_rows), padded_rows.numel(),
+                                                ptr(self.S_t), ptr(self.T_t),
+                                                stream_ptr(self.device)), "mcf_taxonomy_terms")
+        else:   # host stand-in (tests): the same sums, float32 tables
+            self._solver.terms(self, padded_rows)
+
+    def item_layers(self):
+        S0 = self.rank * self.imap.S
+        mine = self.Q[S0:S0 + self.imap.S]
+        for k, (rows_loc, rows_pad) in enumerate(self.layers):
+            if rows_loc.numel():
+                self._terms(rows_pad)
+                self._solver.solve(self.local["items"], self.P, mine, 0.0, self.lam2, self.mu,
+                                   self.S_t[S0:], self.T_t[S0:], self.tau, rows_loc,
+                                   ("layer", k))
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.Q, mine, group=self.group)
+
+    def users(self):
+        S0 = self.rank * self.umap.S
+        mine = self.P[S0:S0 + self.umap.S]
+        self._solver.solve(self.local["users"], self.Q, mine, 0.0, self.lam2, self.mu)
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.P, mine, group=self.group)
+
+    def sweep(self):
+        self.item_layers()
+        self.users()
+
+    check = ShardedAls.check

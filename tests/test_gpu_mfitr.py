@@ -244,3 +244,33 @@ def test_full_blocks_zero_gradient_and_monotone(golden, fixture, D):
     assert np.abs(gr["b_u"]).max() < 1e-4 * scale["b_u"]
     dev_loss = float(fs.loss().item())
     assert abs(dev_loss - loss) < 1e-4 * abs(loss), (dev_loss, loss)
+
+
+def test_sharded_mfitr_device_world1_matches_solver(golden):
+    """The subtree-sharded runner on one GPU (no process group) reproduces
+    MfitrSolver bit for bit (same layouts, plans, kernels)."""
+    from paper_1108_2580_b200 import mfitr
+    from paper_1108_2580_b200.device import AlsEngine, DeviceRatings
+    from paper_1108_2580_b200.parallel import ShardedMfitr
+    g = golden("mfitr_cfg2s.npz")
+    graph = _graph(g)
+    U, I, D = int(g["U"]), int(g["I"]), 8
+    rng = np.random.default_rng(5)
+    P0, Q0 = rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D))
+    lam2, tau, mu = float(g["lam2"]), float(g["lam3"]) + float(g["lam4"]), float(g["mu"])
+    run = ShardedMfitr(g["users"], g["items"], g["scores"], U, I, D, graph, g["w"], lam2, tau,
+                       mu, chunk=64)
+    run.set_factors(P0, Q0)
+    r = DeviceRatings(g["users"], g["items"], g["scores"], U, I, dev())
+    eng = AlsEngine(r, D, chunk=64)
+    eng.set_factors(P0, Q0)
+    h = mfitr.MfitrHyper(D=D, lam1=0.0, lam2=lam2, lam3=float(g["lam3"]), lam4=float(g["lam4"]))
+    solver = mfitr.MfitrSolver(eng, graph, g["w"], h, mu)
+    for _ in range(2):
+        run.sweep()
+        solver.sweep()
+    run.check()
+    eng.check()
+    P1, Q1 = run.factors()
+    P2, Q2 = eng.factors()
+    assert torch.equal(P1, P2) and torch.equal(Q1, Q2)
