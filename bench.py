@@ -578,7 +578,7 @@ def run_sharded(args, rank, world, cfg, wl, t_gen):
     lam = cfg.lam
     t0 = time.perf_counter()
     run = ShardedAls(wl.train_users, wl.train_items, wl.train_scores, cfg.users, cfg.items,
-                     cfg.D, device=dev)
+                     cfg.D, device=dev, collective=args.collective)
     torch.cuda.synchronize()
     t_layout = time.perf_counter() - t0
     P0, Q0 = synth.init_factors(cfg.users, cfg.items, cfg.D, seed=1)
@@ -633,7 +633,8 @@ def run_sharded(args, rank, world, cfg, wl, t_gen):
                            "step": "one full sweep incl. the NCCL all-gather after each half-step",
                            "l2": "inputs > L2; no flush",
                            "parallelism": f"rows sharded over {world} GPUs (nnz-balanced), "
-                                          "opposite factor replicated"},
+                                          "opposite factor replicated",
+                           "collective": args.collective},
                 "roofline": roof,
                 "cpu_baseline": None, "e2e": None, "gpu_launches": 4 * args.steps,
                 "clocks": clk.summary(), "valid_rmse_after": rm, "layout_build_s": t_layout,
@@ -652,6 +653,9 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--collective", choices=["nccl", "peer"], default="nccl",
+                    help="N > 1 ALS: NCCL all-gather after each half-step, or the fused "
+                         "peer stores from the solve kernel (symmetric memory)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the multi-GPU runner even at N = 1 (exercises its host logic)")
     ap.add_argument("--mfitr-blocks", choices=["q", "full"], default="q",

@@ -27,6 +27,8 @@
  *   mcf_sq_norms       the regulariser of factor.als_objective factor.py:541-547
  *                      / factor.loss_mf (factor.py:270-278)
  *   mcf_add_gathered   q_i + q_a[artist(i)] of mfitr._rating_terms mfitr.py:203-216
+ *   mcf_als_half_step_peers the half-step + the replica all-gather of the
+ *                      multi-GPU sweep (the reference is single-process)
  *   mcf_als_half_step_bias  the lam1 (bias) / lam2 (factor) regularisers of
  *                      mfitr.loss_mfitr for augmented [f | b] blocks  mfitr.py:226-242
  *   mcf_mfitr_fixed, mcf_mfitr_targets  the block terms of mfitr._rating_terms
@@ -128,6 +130,23 @@ int mcf_als_half_step_bias(const int64_t *ptr, const int32_t *idx, const float *
                            int32_t chunk, const void *plan, const int64_t *plan_info,
                            int64_t *fail_row, void *ws, size_t ws_bytes, int32_t bias_dim,
                            float bias_lam_c, float bias_lam_n, void *stream);
+
+/* mcf_als_half_step fused with the all-gather of the row-sharded multi-GPU
+ * sweep: every solved row of `out` (this rank's shard) is also
+ * stored, by the solve kernel itself, at the same row offset of each of the
+ * n_peers replicas in peer_out (a DEVICE array of n_peers float* -- NVLink
+ * peer / symmetric-memory pointers to the peers' tables, already offset to
+ * this rank's shard).  The caller orders the next half-step after every
+ * rank's stores (a device barrier over the peers).  Other arguments as
+ * mcf_als_half_step. */
+int mcf_als_half_step_peers(const int64_t *ptr, const int32_t *idx, const float *val,
+                            const float *wts, const float *fixed, int64_t n_fixed, float *out,
+                            int32_t D, float lam_c, float lam_n, float y_shift,
+                            const float *tax_S, const float *tax_T, float tau,
+                            const int32_t *row_list, int32_t n_list, int32_t row_lo,
+                            int32_t chunk, const void *plan, const int64_t *plan_info,
+                            int64_t *fail_row, double *obj_out, void *ws, size_t ws_bytes,
+                            float *const *peer_out, int32_t n_peers, void *stream);
 
 /* ---- MFITR full-model blocks (mfitr.py:203-216 prediction) -----------------
  * Tables are [rows][mcf_factor_ld(D + 1)] with the factor in columns 0..D-1

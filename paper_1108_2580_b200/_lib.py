@@ -37,6 +37,10 @@ SIGNATURES = {
                                        vp, c_f32, vp, c_i32, c_i32, c_i32, vp,
                                        ctypes.POINTER(c_i64), vp, vp, c_size, c_i32, c_f32, c_f32,
                                        vp]),
+    "mcf_als_half_step_peers": (c_int, [vp, vp, vp, vp, vp, c_i64, vp, c_i32, c_f32, c_f32, c_f32,
+                                        vp, vp, c_f32, vp, c_i32, c_i32, c_i32, vp,
+                                        ctypes.POINTER(c_i64), vp, vp, vp, c_size, vp, c_i32,
+                                        vp]),
     "mcf_mfitr_fixed": (c_int, [vp, vp, vp, c_i64, c_i32, vp, vp]),
     "mcf_mfitr_targets": (c_int, [c_i32, vp, vp, vp, vp, c_i32, vp, vp, vp, vp, c_f32, c_i32, vp,
                                   vp]),

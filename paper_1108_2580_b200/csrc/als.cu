@@ -72,7 +72,18 @@ struct AlsParams {
     // bias_lam_c + bias_lam_n * n, no taxonomy terms; -1 = none
     int bias_dim;
     float bias_lam_c, bias_lam_n;
+    // fused all-gather (multi-GPU): every solved row is also stored into
+    // n_peers peer replicas (NVLink peer pointers, same row offsets as out)
+    float *const *peer_out;
+    int n_peers;
 };
+
+// one element of row r of the solved shard: local table + every peer replica
+__device__ __forceinline__ void put_out(const AlsParams &p, int r, int i, float v) {
+    const size_t off = (size_t)r * p.ld + i;
+    p.out[off] = v;
+    for (int k = 0; k < p.n_peers; ++k) p.peer_out[k][off] = v;
+}
 
 // diagonal regulariser of coordinate i of row system with n ratings.  A
 // bias of a row without ratings (an item only the taxonomy touches) has a
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(256) k_als_warp(AlsParams p) {
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     if (it.n == 0 && S == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
-            if (lane < p.ld) p.out[(size_t)r * p.ld + lane] = 0.f;
+            if (lane < p.ld) put_out(p, r, lane, 0.f);
         } else if (lane == 0) {
             report_fail(p.fail, r);
         }
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(256) k_als_warp(AlsParams p) {
         const float xj = __shfl_sync(FULL, b, j2);
         if (lane < j2) b = fmaf(-M[j2 * MS + lane], xj, b);
     }
-    if (lane < p.ld) p.out[(size_t)r * p.ld + lane] = lane < D ? b : 0.f;
+    if (lane < p.ld) put_out(p, r, lane, lane < D ? b : 0.f);
 }
 
 // Paired FP32 FMA (sm_100 FFMA2): acc.{x,y} += a * b.{x,y}; the scalar a is
@@ -639,7 +650,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     if (it.n == 0 && S == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
-            for (int i = tid; i < p.ld; i += CTA_THREADS) p.out[(size_t)r * p.ld + i] = 0.f;
+            for (int i = tid; i < p.ld; i += CTA_THREADS) put_out(p, r, i, 0.f);
         } else if (tid == 0) {
             report_fail(p.fail, r);
         }
@@ -847,7 +858,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_als_cta(AlsParams p) {
             for (int i = tid; i < j; i += 32) vb[i] = fmaf(-Lat(j, i), xj, vb[i]);
             __syncwarp();
         }
-        for (int i = tid; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? vb[i] : 0.f;
+        for (int i = tid; i < p.ld; i += 32) put_out(p, r, i, i < D ? vb[i] : 0.f);
     }
 }
 
@@ -1098,7 +1109,7 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
     const float Sr = p.tax_S ? p.tax_S[r] : 0.f;
     if (it.n == 0 && Sr == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
-            for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = 0.f;
+            for (int i = lane; i < p.ld; i += 32) put_out(p, r, i, 0.f);
         } else if (lane == 0) {
             report_fail(p.fail, r);
         }
@@ -1307,7 +1318,7 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
         }
         __syncwarp();
     }
-    for (int i = lane; i < p.ld; i += 32) p.out[(size_t)r * p.ld + i] = i < D ? bv[i] : 0.f;
+    for (int i = lane; i < p.ld; i += 32) put_out(p, r, i, i < D ? bv[i] : 0.f);
 }
 
 // persistent: every warp pulls work items from an atomic counter (no CTA
@@ -1483,10 +1494,9 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     const int D = p.D;
     sse = reg = 0.0;
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
-    float *orow = p.out + (size_t)r * p.ld;
     if (n == 0 && S == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
-            for (int i = 0; i < p.ld; ++i) orow[i] = 0.f;
+            for (int i = 0; i < p.ld; ++i) put_out(p, r, i, 0.f);
         } else {
             report_fail(p.fail, r);
         }
@@ -1514,7 +1524,7 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     }
     sse = (double)yy - (double)bx - (double)diag * (double)xx;
     reg = (double)lam_row * (double)xx;
-    for (int i = 0; i < p.ld; ++i) orow[i] = i < D ? g[RHS0 + i] : 0.f;
+    for (int i = 0; i < p.ld; ++i) put_out(p, r, i, i < D ? g[RHS0 + i] : 0.f);
 }
 
 __global__ void k_obj_sum(const double *part, int64_t n, double *out) {
@@ -1939,7 +1949,6 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
     const int D = p.D;
     const int64_t n = p.ptr[r + 1] - p.ptr[r];
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
-    float *orow = p.out + (size_t)r * p.ld;
     const float lam_row = p.lam_c + p.lam_n * (float)n;
     const float diag = lam_row + p.tau * S;
     float a[LDK];
@@ -1993,7 +2002,7 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
         const float xj = __shfl_sync(FULL, b, j2);
         if (lane < j2) b = fmaf(-G[pidx(j2, lane)], xj, b);
     }
-    if (lane < p.ld) orow[lane] = lane < D ? b : 0.f;
+    if (lane < p.ld) put_out(p, r, lane, lane < D ? b : 0.f);
     if (p.obj_partial) {
         float bx = lane < D ? b0 * b : 0.f, xx = lane < D ? b * b : 0.f;
 #pragma unroll
@@ -2328,7 +2337,8 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
                           int32_t row_lo, int32_t chunk, const void *plan,
                           const int64_t *plan_info, int64_t *fail_row, double *obj_out, void *ws,
                           size_t ws_bytes, void *stream, int32_t bias_dim, float bias_lam_c,
-                          float bias_lam_n) {
+                          float bias_lam_n, float *const *peer_out = nullptr,
+                          int32_t n_peers = 0) {
     if (D < 1 || D > 128) {
         set_error("mcf_als_half_step: D must be in [1, 128]");
         return MCF_E_UNSUPPORTED;
@@ -2360,6 +2370,12 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
     p.total_items = total_items;
     p.fail = reinterpret_cast<unsigned long long *>(fail_row);
     p.bias_dim = bias_dim;
+    p.peer_out = peer_out;
+    p.n_peers = peer_out ? n_peers : 0;
+    if (n_peers < 0 || (n_peers > 0 && !peer_out)) {
+        set_error("mcf_als_half_step: peer_out must hold n_peers >= 0 device pointers");
+        return MCF_E_ARG;
+    }
     p.bias_lam_c = bias_lam_c;
     p.bias_lam_n = bias_lam_n;
     if (bias_dim >= D || (bias_dim >= 0 && obj_out)) {
@@ -2437,4 +2453,18 @@ extern "C" int mcf_als_half_step_bias(const int64_t *ptr, const int32_t *idx, co
     return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
                           tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
                           nullptr, ws, ws_bytes, stream, bias_dim, bias_lam_c, bias_lam_n);
+}
+
+extern "C" int mcf_als_half_step_peers(const int64_t *ptr, const int32_t *idx, const float *val,
+                                       const float *wts, const float *fixed, int64_t n_fixed,
+                                       float *out, int32_t D, float lam_c, float lam_n,
+                                       float y_shift, const float *tax_S, const float *tax_T,
+                                       float tau, const int32_t *row_list, int32_t n_list,
+                                       int32_t row_lo, int32_t chunk, const void *plan,
+                                       const int64_t *plan_info, int64_t *fail_row,
+                                       double *obj_out, void *ws, size_t ws_bytes,
+                                       float *const *peer_out, int32_t n_peers, void *stream) {
+    return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
+                          tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
+                          obj_out, ws, ws_bytes, stream, -1, 0.f, 0.f, peer_out, n_peers);
 }

@@ -127,10 +127,12 @@ class LayoutSolver:
     def solve(self, lay: SideLayout, fixed: torch.Tensor, out: torch.Tensor, lam_c=0.0, lam_n=0.0,
               y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
               fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None,
-              val: torch.Tensor | None = None, bias=None):
+              val: torch.Tensor | None = None, bias=None, peers: torch.Tensor | None = None):
         """bias = (dim, lam_c, lam_n): coordinate `dim` is a bias with its own
         regulariser (mcf_als_half_step_bias); val: per-rating targets in the
-        layout's CSR order instead of the ratings."""
+        layout's CSR order instead of the ratings; peers: device int64 tensor
+        of peer replica pointers -- the kernel stores every solved row there
+        too (mcf_als_half_step_peers, the fused all-gather)."""
         dev = lay.device
         if fail is None:
             if self.fail is None:
@@ -144,6 +146,16 @@ class LayoutSolver:
             self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = self._ws[k]
         vals = lay.val if val is None else val
+        if peers is not None:
+            if bias is not None:
+                raise ConfigError("bias blocks and peer stores are not combined")
+            check(_lib.lib().mcf_als_half_step_peers(
+                ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
+                ptr(out), self.D, float(lam_c), float(lam_n), float(y_shift), ptr(tax_S),
+                ptr(tax_T), float(tau), ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail),
+                ptr(obj_out), ptr(ws), ws.numel(), ptr(peers), int(peers.numel()),
+                stream_ptr(dev)), "mcf_als_half_step_peers")
+            return fail
         if bias is not None:
             check(_lib.lib().mcf_als_half_step_bias(
                 ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],

@@ -81,7 +81,16 @@ class ShardedAls:
     """One rank's part of a row-sharded ALS fit."""
 
     def __init__(self, users, items, scores, num_users: int, num_items: int, D: int, *,
-                 group=None, solver="device", device=None, chunk: int | None = None):
+                 group=None, solver="device", device=None, chunk: int | None = None,
+                 collective: str = "nccl"):
+        """collective: "nccl" -- in-place ncclAllGather after each half-step;
+        "peer" -- the fused form: P and Q live in symmetric memory
+        (torch.distributed._symmetric_memory, NVLink peer mappings) and the
+        solve kernel itself stores every row into each peer's replica
+        (mcf_als_half_step_peers), followed by a device barrier."""
+        if collective not in ("nccl", "peer"):
+            raise ConfigError(f"collective must be 'nccl' or 'peer', got {collective!r}")
+        self.collective = collective
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -100,8 +109,12 @@ class ShardedAls:
         self.num_users, self.num_items = int(num_users), int(num_items)
         self.umap = ShardMap(nnz_balanced_cuts(torch.bincount(u, minlength=num_users), self.world))
         self.imap = ShardMap(nnz_balanced_cuts(torch.bincount(it, minlength=num_items), self.world))
-        self.P = torch.zeros(self.umap.rows, self.ld, dtype=torch.float32, device=dev)
-        self.Q = torch.zeros(self.imap.rows, self.ld, dtype=torch.float32, device=dev)
+        self._peers, self._handles = {}, {}
+        if collective == "peer":
+            self.P, self.Q = self._symmetric_tables(dev)
+        else:
+            self.P = torch.zeros(self.umap.rows, self.ld, dtype=torch.float32, device=dev)
+            self.Q = torch.zeros(self.imap.rows, self.ld, dtype=torch.float32, device=dev)
         # local layouts: my users (partners = padded item ids), my items
         self.local = {}
         for side, keys, cols, kmap, cmap in (("users", u, it, self.umap, self.imap),
@@ -112,6 +125,26 @@ class ShardedAls:
             c_pad = cmap.to_padded(cols[m])
             self.local[side] = self._make_layout(k_loc, c_pad, s[m], hi - lo)
         self.nnz_local = {k: int(v.nnz) for k, v in self.local.items()}
+
+    def _symmetric_tables(self, dev):
+        """P, Q in symmetric memory; per side the device array of the peers'
+        replica pointers, offset to this rank's shard."""
+        import torch.distributed._symmetric_memory as symm_mem
+        group = self.group if self.group is not None else dist.group.WORLD
+        name = group.group_name
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            symm_mem.enable_symm_mem_for_group(name)
+        tabs = []
+        for side, mp in (("users", self.umap), ("items", self.imap)):
+            t = symm_mem.empty(mp.rows, self.ld, dtype=torch.float32, device=dev)
+            t.zero_()
+            h = symm_mem.rendezvous(t, name)
+            off = self.rank * mp.S * self.ld * 4
+            ptrs = [int(h.buffer_ptrs[k]) + off for k in range(self.world) if k != self.rank]
+            self._peers[side] = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+            self._handles[side] = h
+            tabs.append(t)
+        return tabs
 
     def _make_layout(self, keys, cols, vals, n_rows):
         if self._solver.__class__.__name__ == "LayoutSolver":
@@ -142,6 +175,14 @@ class ShardedAls:
                                else (self.Q, self.P, self.imap))
         S = mp.S
         mine = out_full[self.rank * S:(self.rank + 1) * S]
+        if self.collective == "peer":
+            # fused: the kernel also stores each solved row into every peer's
+            # replica; the barrier orders the next half-step after all stores
+            self._solver.solve(self.local[side], fixed, mine, lam_c, lam_n,
+                               peers=self._peers[side])
+            if gather and self.world > 1:
+                self._handles[side].barrier(channel=0)
+            return out_full
         self._solver.solve(self.local[side], fixed, mine, lam_c, lam_n)
         if gather and self.world > 1:
             # in place: my shard already sits at rank*S inside out_full

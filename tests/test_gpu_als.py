@@ -359,3 +359,61 @@ def test_fused_objective_matches_explicit(golden, reg, D):
         ref = oracle.weighted_objective(P, Q, u.astype(np.int64), i.astype(np.int64), s, lam)
     assert abs(explicit - ref) < 1e-5 * ref
     assert abs(fused - ref) < 1e-4 * ref, (fused, explicit, ref)
+
+
+def test_fused_peer_stores_replicate_every_row():
+    """mcf_als_half_step_peers: the solve kernel writes every solved row into
+    each peer replica too (the fused all-gather of the sharded sweep) -- two
+    'peers' on this GPU receive exactly the local result, for the pair
+    (D = 20, hot rows) and tile-warp (D = 50) paths."""
+    from paper_1108_2580_b200.device import LayoutSolver
+    for D in (20, 50):
+        U, I = 3000, 400
+        u, i, s = _random_split(U, I, 120_000, 11, hot=5)
+        eng = _engine(u, i, s, U, I, D, chunk=256)
+        rng = np.random.default_rng(1)
+        eng.set_factors(rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D)))
+        ref = eng.half_step("items", 0.0, 0.065).clone()
+        peers = [torch.full_like(eng.Q, float("nan")) for _ in range(2)]
+        ptrs = torch.tensor([t.data_ptr() for t in peers], dtype=torch.int64, device=eng.device)
+        out = torch.zeros_like(eng.Q)
+        LayoutSolver(D, 256).solve(eng.r.by_item, eng.P, out, 0.0, 0.065, peers=ptrs)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        for t in peers:
+            assert torch.equal(t, ref)
+
+
+def test_sharded_peer_collective_single_rank():
+    """ShardedAls(collective="peer") on a one-rank NCCL group: tables in
+    symmetric memory, the fused peer-store path (no peers at world 1) and the
+    device barrier; identical to the NCCL-collective runner."""
+    import socket
+    import torch.distributed as dist
+    from paper_1108_2580_b200.parallel import ShardedAls
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        U, I, D = 2000, 300, 20
+        u, i, s = _random_split(U, I, 60_000, 4)
+        rng = np.random.default_rng(0)
+        P0, Q0 = rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D))
+        outs = []
+        for coll in ("nccl", "peer"):
+            try:
+                run = ShardedAls(u, i, s, U, I, D, collective=coll)
+            except Exception as e:   # pragma: no cover - symmetric memory unavailable
+                if coll == "peer":
+                    pytest.skip(f"torch symmetric memory unavailable: {e}")
+                raise
+            run.set_factors(P0, Q0)
+            for _ in range(2):
+                run.sweep(0.0, 0.065)
+            run.check()
+            outs.append([t.clone() for t in run.factors()])
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    finally:
+        dist.destroy_process_group()
