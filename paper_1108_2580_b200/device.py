@@ -22,6 +22,12 @@ from ._lib import check, ptr
 from .errors import ConfigError, DeviceError, SingularSystemError
 
 DEFAULT_CHUNK = 2048
+TASKS_IN_FLIGHT = 2 * 148 * 8 * 16   # 2 x (SMs x pair-kernel warps x lane pairs)
+
+
+def adaptive_chunk(nnz_rows: int, cap: int = DEFAULT_CHUNK) -> int:
+    """Task length for a row subset with nnz_rows ratings (see SideLayout.plan)."""
+    return max(64, min(cap, nnz_rows // TASKS_IN_FLIGHT // 32 * 32))
 PLAN_INFO_LEN = 6   # MCF_PLAN_INFO_LEN
 
 
@@ -62,19 +68,25 @@ class SideLayout:
     def degrees(self) -> torch.Tensor:
         return self.ptr[1:] - self.ptr[:-1]
 
-    def plan(self, rows: torch.Tensor | None = None, key=None, chunk: int = DEFAULT_CHUNK):
-        """(plan buffer, plan_info, row list, n_list) for all rows, or for the
-        int32 row list `rows` (cached under `key`)."""
+    def plan(self, rows: torch.Tensor | None = None, key=None, chunk: int = DEFAULT_CHUNK,
+             adaptive: bool = True):
+        """(plan buffer, plan_info, row list, n_list, chunk) for all rows, or
+        for the int32 row list `rows` (cached under `key`).  For a row list
+        (adaptive=True, the pair path) the chunk shrinks with its rating count (at least ~2 tasks per lane
+        pair in flight, multiples of 32, >= 64): a small taxonomy layer with a
+        few Zipf-hot items would otherwise end on one 2048-rating task."""
         k = (key, chunk) if rows is not None else ("all", chunk)
         if k not in self._plans:
             L = _lib.lib()
             n_list = self.n_rows if rows is None else int(rows.numel())
+            if adaptive and rows is not None and n_list:
+                chunk = adaptive_chunk(int(self.degrees()[rows.long()].sum()), chunk)
             buf = torch.empty(int(L.mcf_als_plan_bytes(n_list, self.nnz, chunk)), dtype=torch.uint8,
                               device=self.device)
             info = (_lib.c_i64 * PLAN_INFO_LEN)()
             check(L.mcf_als_plan(ptr(self.ptr), ptr(rows), n_list, 0, chunk, self.nnz, ptr(buf),
                                  buf.numel(), info, stream_ptr(self.device)), "mcf_als_plan")
-            self._plans[k] = (buf, info, rows, n_list)
+            self._plans[k] = (buf, info, rows, n_list, chunk)
         return self._plans[k]
 
 
@@ -127,7 +139,8 @@ class LayoutSolver:
     def solve(self, lay: SideLayout, fixed: torch.Tensor, out: torch.Tensor, lam_c=0.0, lam_n=0.0,
               y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
               fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None,
-              val: torch.Tensor | None = None, bias=None, peers: torch.Tensor | None = None):
+              val: torch.Tensor | None = None, bias=None, peers: torch.Tensor | None = None,
+              chunk: int | None = None):
         """bias = (dim, lam_c, lam_n): coordinate `dim` is a bias with its own
         regulariser (mcf_als_half_step_bias); val: per-rating targets in the
         layout's CSR order instead of the ratings; peers: device int64 tensor
@@ -138,7 +151,11 @@ class LayoutSolver:
             if self.fail is None:
                 self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
             fail = self.fail
-        buf, info, rl, n_list = lay.plan(rows, rows_key, self.chunk)
+        if chunk is None:   # adaptive task length on the pair path (D <= 20) only
+            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, self.chunk,
+                                                    adaptive=self.D <= 20)
+        else:   # fixed task length (G-invariant sharded runs)
+            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, chunk, adaptive=False)
         slots = info[3] if self.D <= 20 else info[1]
         k = (id(lay), rows_key)
         need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
@@ -152,7 +169,7 @@ class LayoutSolver:
             check(_lib.lib().mcf_als_half_step_peers(
                 ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
                 ptr(out), self.D, float(lam_c), float(lam_n), float(y_shift), ptr(tax_S),
-                ptr(tax_T), float(tau), ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail),
+                ptr(tax_T), float(tau), ptr(rl), n_list, 0, chunk, ptr(buf), info, ptr(fail),
                 ptr(obj_out), ptr(ws), ws.numel(), ptr(peers), int(peers.numel()),
                 stream_ptr(dev)), "mcf_als_half_step_peers")
             return fail
@@ -160,7 +177,7 @@ class LayoutSolver:
             check(_lib.lib().mcf_als_half_step_bias(
                 ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
                 ptr(out), self.D, float(lam_c), float(lam_n), float(y_shift), ptr(tax_S),
-                ptr(tax_T), float(tau), ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail),
+                ptr(tax_T), float(tau), ptr(rl), n_list, 0, chunk, ptr(buf), info, ptr(fail),
                 ptr(ws), ws.numel(), int(bias[0]), float(bias[1]), float(bias[2]),
                 stream_ptr(dev)), "mcf_als_half_step_bias")
             return fail
@@ -168,7 +185,7 @@ class LayoutSolver:
             ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
             ptr(out), self.D,
             float(lam_c), float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau),
-            ptr(rl), n_list, 0, self.chunk, ptr(buf), info, ptr(fail), ptr(obj_out), ptr(ws),
+            ptr(rl), n_list, 0, chunk, ptr(buf), info, ptr(fail), ptr(obj_out), ptr(ws),
             ws.numel(), stream_ptr(dev)), "mcf_als_half_step")
         return fail
 

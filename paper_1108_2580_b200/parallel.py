@@ -337,8 +337,13 @@ class ShardedMfitr:
         self.edges_padded = (pc, pp, np.asarray(w, np.float64))
         # my rows of each layer: local and padded indices
         mine = self.imap.owner == self.rank
-        self.layers = []
+        self.layers, self.layer_chunk = [], []
+        from .device import DEFAULT_CHUNK, adaptive_chunk
         for L in graph.layers(num_items):
+            # task length from the GLOBAL layer size: identical on every rank,
+            # so hot-row chunk sums (and results) do not depend on world size
+            cap = chunk or DEFAULT_CHUNK
+            self.layer_chunk.append(adaptive_chunk(int(deg[L].sum()), cap) if D <= 20 else cap)
             Lm = L[mine[L]]
             loc_rows = np.sort(self.imap.local[Lm])
             self.layers.append((torch.as_tensor(loc_rows.astype(np.int32), device=dev),
@@ -381,9 +386,11 @@ class ShardedMfitr:
         for k, (rows_loc, rows_pad) in enumerate(self.layers):
             if rows_loc.numel():
                 self._terms(rows_pad)
+                kw = ({"chunk": self.layer_chunk[k]}
+                      if self._solver.__class__.__name__ == "LayoutSolver" else {})
                 self._solver.solve(self.local["items"], self.P, mine, 0.0, self.lam2, self.mu,
                                    self.S_t[S0:], self.T_t[S0:], self.tau, rows_loc,
-                                   ("layer", k))
+                                   ("layer", k), **kw)
         if self.world > 1:
             dist.all_gather_into_tensor(self.Q, mine, group=self.group)
 
