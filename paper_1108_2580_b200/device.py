@@ -22,11 +22,14 @@ from ._lib import check, ptr
 from .errors import ConfigError, DeviceError, SingularSystemError
 
 DEFAULT_CHUNK = 2048
+PAIR_CHUNK_CAP = 8192                # pair path: longest task (config 1: 11.5 -> 11.3 ms)
 TASKS_IN_FLIGHT = 2 * 148 * 8 * 16   # 2 x (SMs x pair-kernel warps x lane pairs)
 
 
-def adaptive_chunk(nnz_rows: int, cap: int = DEFAULT_CHUNK) -> int:
-    """Task length for a row subset with nnz_rows ratings (see SideLayout.plan)."""
+def adaptive_chunk(nnz_rows: int, cap: int = PAIR_CHUNK_CAP) -> int:
+    """Task length of the pair path for rows holding nnz_rows ratings: long
+    tasks (fewer hot-row chunk partials, fewer group boundaries) but at
+    least ~2 tasks per lane pair in flight, multiples of 32, 64..cap."""
     return max(64, min(cap, nnz_rows // TASKS_IN_FLIGHT // 32 * 32))
 PLAN_INFO_LEN = 6   # MCF_PLAN_INFO_LEN
 
@@ -69,18 +72,20 @@ class SideLayout:
         return self.ptr[1:] - self.ptr[:-1]
 
     def plan(self, rows: torch.Tensor | None = None, key=None, chunk: int = DEFAULT_CHUNK,
-             adaptive: bool = True):
+             adaptive: bool = False):
         """(plan buffer, plan_info, row list, n_list, chunk) for all rows, or
-        for the int32 row list `rows` (cached under `key`).  For a row list
-        (adaptive=True, the pair path) the chunk shrinks with its rating count (at least ~2 tasks per lane
-        pair in flight, multiples of 32, >= 64): a small taxonomy layer with a
-        few Zipf-hot items would otherwise end on one 2048-rating task."""
-        k = (key, chunk) if rows is not None else ("all", chunk)
+        for the int32 row list `rows` (cached under `key`).  adaptive=True (the
+        pair path): `chunk` is a cap and the task length follows the rows'
+        rating count (adaptive_chunk) -- e.g. a small taxonomy layer with a
+        few Zipf-hot items would otherwise end on one long task."""
+        k = (key if rows is not None else "all", chunk, adaptive)
         if k not in self._plans:
             L = _lib.lib()
             n_list = self.n_rows if rows is None else int(rows.numel())
-            if adaptive and rows is not None and n_list:
-                chunk = adaptive_chunk(int(self.degrees()[rows.long()].sum()), chunk)
+            if adaptive:
+                nnz_rows = self.nnz if rows is None else (
+                    int(self.degrees()[rows.long()].sum()) if n_list else 0)
+                chunk = adaptive_chunk(nnz_rows, chunk)
             buf = torch.empty(int(L.mcf_als_plan_bytes(n_list, self.nnz, chunk)), dtype=torch.uint8,
                               device=self.device)
             info = (_lib.c_i64 * PLAN_INFO_LEN)()
@@ -131,8 +136,10 @@ class LayoutSolver:
     """mcf_als_half_step over one SideLayout with caller-chosen fixed / out
     tables (used by AlsEngine and by the row-sharded multi-GPU runner)."""
 
-    def __init__(self, D: int, chunk: int = DEFAULT_CHUNK):
-        self.D, self.chunk = int(D), int(chunk)
+    def __init__(self, D: int, chunk: int | None = None):
+        """chunk: fixed task length, or None -- adaptive up to PAIR_CHUNK_CAP
+        on the pair path (D <= 20), DEFAULT_CHUNK on the wide paths."""
+        self.D, self.chunk = int(D), (None if chunk is None else int(chunk))
         self._ws = {}
         self.fail = None
 
@@ -151,11 +158,14 @@ class LayoutSolver:
             if self.fail is None:
                 self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
             fail = self.fail
-        if chunk is None:   # adaptive task length on the pair path (D <= 20) only
-            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, self.chunk,
-                                                    adaptive=self.D <= 20)
-        else:   # fixed task length (G-invariant sharded runs)
-            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, chunk, adaptive=False)
+        if chunk is None:
+            chunk = self.chunk
+        if chunk is not None:       # fixed task length (tests, G-invariant sharded runs)
+            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, chunk)
+        elif self.D <= 20:          # pair path: adaptive task length
+            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, PAIR_CHUNK_CAP, adaptive=True)
+        else:
+            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, DEFAULT_CHUNK)
         slots = info[3] if self.D <= 20 else info[1]
         k = (id(lay), rows_key)
         need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
@@ -195,10 +205,10 @@ class AlsEngine:
     ratings split.  All calls are asynchronous on the current stream; row
     failures accumulate in a device scalar read by `check()`."""
 
-    def __init__(self, ratings: DeviceRatings, D: int, chunk: int = DEFAULT_CHUNK):
+    def __init__(self, ratings: DeviceRatings, D: int, chunk: int | None = None):
         if not 1 <= D <= 128:
             raise ConfigError("D must be in [1, 128] on the device path")
-        self.r, self.D, self.ld, self.chunk = ratings, int(D), _lib.factor_ld(D), int(chunk)
+        self.r, self.D, self.ld, self.chunk = ratings, int(D), _lib.factor_ld(D), chunk
         dev = ratings.device
         self.device = dev
         self.P = torch.zeros(ratings.num_users, self.ld, dtype=torch.float32, device=dev)

@@ -273,7 +273,7 @@ class MfitrFullSolver:
     def __init__(self, ratings, graph: TaxonomyGraph, w: np.ndarray, hyper: MfitrHyper, mu: float,
                  art: np.ndarray, P0, Q0, Qa0=None, b_u=None, b_i=None, b_a=None,
                  chunk: int | None = None):
-        from .device import DEFAULT_CHUNK, LayoutSolver, SideLayout
+        from .device import LayoutSolver, SideLayout
         dev = ratings.device
         self.r, self.hyper, self.mu, self.device = ratings, hyper, float(mu), dev
         U, I, D = ratings.num_users, ratings.num_items, int(hyper.D)
@@ -327,7 +327,7 @@ class MfitrFullSolver:
         self.S = torch.zeros(I, dtype=torch.float32, device=dev)
         self.T = torch.zeros(I, self.ld, dtype=torch.float32, device=dev)
         self.tau = hyper.lam3 + hyper.lam4
-        self.solver = LayoutSolver(D + 1, chunk or DEFAULT_CHUNK)
+        self.solver = LayoutSolver(D + 1, chunk)
         self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
 
     def _bias(self):

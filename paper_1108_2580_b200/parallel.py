@@ -52,6 +52,16 @@ def nnz_balanced_cuts(degrees: torch.Tensor, world: int) -> torch.Tensor:
     return torch.cummax(cuts, 0).values
 
 
+def global_chunk(nnz_total: int, D: int, chunk: int | None) -> int:
+    """Task length of a sharded run, from the GLOBAL rating count: every rank
+    and every world size chunks the hot rows identically, so the chunk-order
+    sums -- and the factors -- do not depend on the world size."""
+    from .device import DEFAULT_CHUNK, adaptive_chunk
+    if chunk is not None:
+        return int(chunk)
+    return adaptive_chunk(nnz_total) if D <= 20 else DEFAULT_CHUNK
+
+
 class ShardMap:
     """Global row id <-> padded shard numbering."""
 
@@ -96,9 +106,9 @@ class ShardedAls:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.D, self.ld = int(D), _lib.factor_ld(D)
         if solver == "device":
-            from .device import DEFAULT_CHUNK, LayoutSolver, cuda_device
+            from .device import LayoutSolver, cuda_device
             dev = cuda_device(device)
-            self._solver = LayoutSolver(D, chunk or DEFAULT_CHUNK)
+            self._solver = LayoutSolver(D, chunk)
         else:
             dev = torch.device(device or "cpu")
             self._solver = solver
@@ -125,6 +135,7 @@ class ShardedAls:
             c_pad = cmap.to_padded(cols[m])
             self.local[side] = self._make_layout(k_loc, c_pad, s[m], hi - lo)
         self.nnz_local = {k: int(v.nnz) for k, v in self.local.items()}
+        self.fixed_chunk = global_chunk(int(u.numel()), self.D, chunk)
 
     def _symmetric_tables(self, dev):
         """P, Q in symmetric memory; per side the device array of the peers'
@@ -145,6 +156,9 @@ class ShardedAls:
             self._handles[side] = h
             tabs.append(t)
         return tabs
+
+    def _is_device(self):
+        return self._solver.__class__.__name__ == "LayoutSolver"
 
     def _make_layout(self, keys, cols, vals, n_rows):
         if self._solver.__class__.__name__ == "LayoutSolver":
@@ -179,11 +193,12 @@ class ShardedAls:
             # fused: the kernel also stores each solved row into every peer's
             # replica; the barrier orders the next half-step after all stores
             self._solver.solve(self.local[side], fixed, mine, lam_c, lam_n,
-                               peers=self._peers[side])
+                               peers=self._peers[side], chunk=self.fixed_chunk)
             if gather and self.world > 1:
                 self._handles[side].barrier(channel=0)
             return out_full
-        self._solver.solve(self.local[side], fixed, mine, lam_c, lam_n)
+        kw = {"chunk": self.fixed_chunk} if self._is_device() else {}
+        self._solver.solve(self.local[side], fixed, mine, lam_c, lam_n, **kw)
         if gather and self.world > 1:
             # in place: my shard already sits at rank*S inside out_full
             dist.all_gather_into_tensor(out_full, mine, group=self.group)
@@ -292,9 +307,9 @@ class ShardedMfitr:
         self.D, self.ld = int(D), _lib.factor_ld(D)
         self.lam2, self.tau, self.mu = float(lam2), float(tau), float(mu)
         if solver == "device":
-            from .device import DEFAULT_CHUNK, LayoutSolver, cuda_device
+            from .device import LayoutSolver, cuda_device
             dev = cuda_device(device)
-            self._solver = LayoutSolver(D, chunk or DEFAULT_CHUNK)
+            self._solver = LayoutSolver(D, chunk)
         else:
             dev = torch.device(device or "cpu")
             self._solver = solver
@@ -338,12 +353,11 @@ class ShardedMfitr:
         # my rows of each layer: local and padded indices
         mine = self.imap.owner == self.rank
         self.layers, self.layer_chunk = [], []
-        from .device import DEFAULT_CHUNK, adaptive_chunk
+        self.users_chunk = global_chunk(int(u.numel()), self.D, chunk)
         for L in graph.layers(num_items):
             # task length from the GLOBAL layer size: identical on every rank,
             # so hot-row chunk sums (and results) do not depend on world size
-            cap = chunk or DEFAULT_CHUNK
-            self.layer_chunk.append(adaptive_chunk(int(deg[L].sum()), cap) if D <= 20 else cap)
+            self.layer_chunk.append(global_chunk(int(deg[L].sum()), self.D, chunk))
             Lm = L[mine[L]]
             loc_rows = np.sort(self.imap.local[Lm])
             self.layers.append((torch.as_tensor(loc_rows.astype(np.int32), device=dev),
@@ -386,8 +400,7 @@ class ShardedMfitr:
         for k, (rows_loc, rows_pad) in enumerate(self.layers):
             if rows_loc.numel():
                 self._terms(rows_pad)
-                kw = ({"chunk": self.layer_chunk[k]}
-                      if self._solver.__class__.__name__ == "LayoutSolver" else {})
+                kw = {"chunk": self.layer_chunk[k]} if self._is_device() else {}
                 self._solver.solve(self.local["items"], self.P, mine, 0.0, self.lam2, self.mu,
                                    self.S_t[S0:], self.T_t[S0:], self.tau, rows_loc,
                                    ("layer", k), **kw)
@@ -397,7 +410,8 @@ class ShardedMfitr:
     def users(self):
         S0 = self.rank * self.umap.S
         mine = self.P[S0:S0 + self.umap.S]
-        self._solver.solve(self.local["users"], self.Q, mine, 0.0, self.lam2, self.mu)
+        kw = {"chunk": self.users_chunk} if self._is_device() else {}
+        self._solver.solve(self.local["users"], self.Q, mine, 0.0, self.lam2, self.mu, **kw)
         if self.world > 1:
             dist.all_gather_into_tensor(self.P, mine, group=self.group)
 
@@ -406,3 +420,4 @@ class ShardedMfitr:
         self.users()
 
     check = ShardedAls.check
+    _is_device = ShardedAls._is_device
