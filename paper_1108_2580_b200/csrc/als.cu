@@ -76,6 +76,11 @@ struct AlsParams {
     // n_peers peer replicas (NVLink peer pointers, same row offsets as out)
     float *const *peer_out;
     int n_peers;
+    // Schur bias (pair path): the rows are [f | b] with f in columns 0..D-1
+    // and b in column D; the kernel accumulates u = sum x, d = sum y beside
+    // the Gram and eliminates b exactly: (A - u u^T/s) f = c - u d/s,
+    // b = (d - u.f)/s, s = n + bias regulariser
+    int schur;
 };
 
 // one element of row r of the solved shard: local table + every peer replica
@@ -1373,6 +1378,11 @@ struct PairGeom {
     static constexpr int GRAM = RHS0 + LDK;        // packed lower + rhs
     static constexpr int PSTR = GRAM + 1;          // partial slot: + sum w y^2
     static constexpr int GSTRIDE = GRAM | 1;       // odd stride: conflict-free per-lane rows
+    // Schur-bias variant: packed system + u (LDK) + d; partial + u + d
+    static constexpr int UOFF = GRAM, DOFF = GRAM + LDK;
+    static constexpr int GSTRIDE_S = (GRAM + LDK + 1) | 1;
+    static constexpr int PSTR_S = GRAM + 1 + LDK + 1;
+    static constexpr int PU = GRAM + 1, PD = GRAM + 1 + LDK;   // u, d in a partial slot
 };
 
 // smallest 16-byte unit count >= u that is 2 or 6 mod 8: the 4 pairs of a
@@ -1396,7 +1406,7 @@ struct PairCfg : PairGeom<NBK> {
     static constexpr int STAGE_BYTES = PAIRS * SLOT * 4;
     static constexpr int NS = R == 2 ? 7 : 4;      // pipeline stages (lead = (NS-1)*R ratings)
     static constexpr int RING_BYTES = NS * STAGE_BYTES;
-    static constexpr int SOLVE_BYTES = PAIRS * G::GSTRIDE * 4;
+    static constexpr int SOLVE_BYTES = PAIRS * G::GSTRIDE_S * 4;
     // the gather ring and the solve buffer are never live at the same time
     static constexpr int RING_AREA =
         ((RING_BYTES > SOLVE_BYTES ? RING_BYTES : SOLVE_BYTES) + 127) / 128 * 128;
@@ -1487,10 +1497,11 @@ struct PairPlan {
 //   sum_k w_k (y_k - x_k^T x)^2 = sum w y^2 - b^T x - lam |x|^2   (sse)
 //   (lam_c + lam_n n) |x|^2                                        (reg)
 // (yy = sum w y^2 accumulated with the Gram; exact for tau = 0).
-template <int LDK>
+template <int LDK, bool SCHUR = false>
 __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float yy,
                            double &sse, double &reg) {
     constexpr int RHS0 = LDK * (LDK + 1) / 2;
+    constexpr int UOFF = RHS0 + LDK, DOFF = UOFF + LDK;
     const int D = p.D;
     sse = reg = 0.0;
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
@@ -1506,12 +1517,29 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     const float diag = lam_row + p.tau * S;
     if (p.tax_T)
         for (int i = 0; i < D; ++i) g[RHS0 + i] = tax_rhs(p, r, i, g[RHS0 + i]);
+    float sb = 1.f, db = 0.f;
+    if constexpr (SCHUR) {   // eliminate the bias: A -= u u^T / s, c -= u d / s
+        sb = (float)n + (n > 0 ? fmaf(p.bias_lam_n, (float)n, p.bias_lam_c) : 1.f);
+        db = g[DOFF];
+        const float is = 1.f / sb;
+        for (int i = 0; i < D; ++i) {
+            const float ui = g[UOFF + i] * is;
+            for (int j = 0; j <= i; ++j) g[pidx(i, j)] = fmaf(-ui, g[UOFF + j], g[pidx(i, j)]);
+            g[RHS0 + i] = fmaf(-ui, db, g[RHS0 + i]);
+        }
+    }
     float b[LDK];
 #pragma unroll
     for (int i = 0; i < LDK; ++i) b[i] = i < D ? g[RHS0 + i] : 0.f;
     if (!thread_solve<LDK>(g, D, diag, p.bias_dim, diag_at(p, p.bias_dim, diag, (float)n))) {
         report_fail(p.fail, r);
         return;
+    }
+    float bias = 0.f;
+    if constexpr (SCHUR) {   // b = (d - u.f) / s
+        float uf = 0.f;
+        for (int i = 0; i < D; ++i) uf = fmaf(g[UOFF + i], g[RHS0 + i], uf);
+        bias = (db - uf) / sb;
     }
     float bx = 0.f, xx = 0.f;
 #pragma unroll
@@ -1524,7 +1552,8 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     }
     sse = (double)yy - (double)bx - (double)diag * (double)xx;
     reg = (double)lam_row * (double)xx;
-    for (int i = 0; i < p.ld; ++i) put_out(p, r, i, i < D ? g[RHS0 + i] : 0.f);
+    for (int i = 0; i < p.ld; ++i)
+        put_out(p, r, i, i < D ? g[RHS0 + i] : (SCHUR && i == D) ? bias : 0.f);
 }
 
 __global__ void k_obj_sum(const double *part, int64_t n, double *out) {
@@ -1583,7 +1612,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 // diagonal blocks the lower 4x4 triangle (m=0: 1 scalar; m=1: a pair; m=2: a
 // pair + a scalar; m=3: two pairs), for each of NOFF off-diagonal blocks
 // 4 rows x 2 pairs, for each of HALF rhs blocks 2 pairs.
-template <int NBK>
+template <int NBK, bool SCHUR = false>
 struct PairAcc {
     static constexpr int HALF = (NBK + 1) / 2;
     static constexpr int NOFF = ((NBK - 1) / 2) * HALF;
@@ -1592,8 +1621,15 @@ struct PairAcc {
     float2 off[NOFF > 0 ? NOFF : 1][4][2];
     float2 rhs[HALF][2];
     float yy;   // sum w y^2 (fused objective)
+    float2 ux[HALF][2];   // Schur: sum x of the lane's register blocks
+    float dd;             // Schur: sum y
     __device__ __forceinline__ void zero() {
         yy = 0.f;
+        if constexpr (SCHUR) {
+            dd = 0.f;
+#pragma unroll
+            for (int i = 0; i < HALF; ++i) ux[i][0] = ux[i][1] = make_float2(0.f, 0.f);
+        }
 #pragma unroll
         for (int i = 0; i < HALF; ++i) {
             dsc[i][0] = dsc[i][1] = 0.f;
@@ -1610,6 +1646,14 @@ struct PairAcc {
     __device__ __forceinline__ void add(const float4 (&xa)[NBK], const float4 (&xr)[NBK], float y,
                                         float wy) {
         yy = fmaf(wy, y, yy);
+        if constexpr (SCHUR) {
+            dd += wy;
+#pragma unroll
+            for (int i = 0; i < HALF; ++i) {
+                ffma2(ux[i][0], 1.f, xa[2 * i].x, xa[2 * i].y);
+                ffma2(ux[i][1], 1.f, xa[2 * i].z, xa[2 * i].w);
+            }
+        }
 #pragma unroll
         for (int i = 0; i < HALF; ++i) {
             const int b = 2 * i;
@@ -1659,7 +1703,16 @@ struct PairAcc {
             g[rhs0 + r + 1] = rhs[i][0].y;
             g[rhs0 + r + 2] = rhs[i][1].x;
             g[rhs0 + r + 3] = rhs[i][1].y;
+            if constexpr (SCHUR) {   // block 0 is held by both lanes: same sums
+                constexpr int UO = PairGeom<NBK>::UOFF;
+                g[UO + r] = ux[i][0].x;
+                g[UO + r + 1] = ux[i][0].y;
+                g[UO + r + 2] = ux[i][1].x;
+                g[UO + r + 3] = ux[i][1].y;
+            }
         }
+        if constexpr (SCHUR)
+            if (h == 0) g[PairGeom<NBK>::DOFF] = dd;
         int o = 0;
 #pragma unroll
         for (int d = 1; d <= (NBK - 1) / 2; ++d) {
@@ -1692,7 +1745,7 @@ struct PairAcc {
 // s+NS-1 is issued -- no register ever waits on an in-flight load.
 // L2 policy: the once-read idx/val/weight streams are loaded evict_first,
 // so they do not push the fixed factor rows (50-80 MB at config 1) out of L2.
-template <int NBK, int R, bool HAS_W, bool FULLBLK>
+template <int NBK, int R, bool HAS_W, bool FULLBLK, bool SCHUR = false>
 __global__ void __launch_bounds__(PairCfg<NBK, R>::WARPS * 32, PairCfg<NBK, R>::MIN_CTAS)
 k_als_pair(AlsParams p, PairPlan q) {
     using C = PairCfg<NBK, R>;
@@ -1703,7 +1756,8 @@ k_als_pair(AlsParams p, PairPlan q) {
     unsigned char *wbase = smem_raw + warp * C::WARP_BYTES;
     const unsigned wbase_s = static_cast<unsigned>(__cvta_generic_to_shared(wbase));
     const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[warp][0]));
-    float *my_g = reinterpret_cast<float *>(wbase) + pair * C::GSTRIDE;  // aliases the ring
+    float *my_g = reinterpret_cast<float *>(wbase) +
+                  pair * (SCHUR ? C::GSTRIDE_S : C::GSTRIDE);   // aliases the ring
     const unsigned my_slot_s = wbase_s + pair * C::SLOT * 4;
     const float *my_slot = reinterpret_cast<const float *>(wbase) + pair * C::SLOT;
     // ids ring: [PAIRS][IDSTR] int32 after the gather ring / solve area
@@ -1750,7 +1804,7 @@ k_als_pair(AlsParams p, PairPlan q) {
                 prefetch_l2(h ? (const void *)(valp + o) : (const void *)(idxp + o));
         __syncwarp();   // the previous group's solve is done with the (aliased) ring
 
-        PairAcc<NBK> acc;
+        PairAcc<NBK, SCHUR> acc;
         acc.zero();
 
         const unsigned gbase = gst;
@@ -1869,11 +1923,14 @@ k_als_pair(AlsParams p, PairPlan q) {
         double o_sse = 0.0, o_reg = 0.0;
         if (task < q.n_tasks) {
             if (slot >= 0) {
-                float *dst = p.partials + (size_t)slot * C::PSTR;
+                float *dst = p.partials + (size_t)slot * (SCHUR ? C::PSTR_S : C::PSTR);
                 for (int i = h; i < C::GRAM; i += 2) dst[i] = my_g[i];
                 if (h == 0) dst[C::GRAM] = acc.yy;
+                if constexpr (SCHUR) {
+                    for (int i = h; i <= C::LDK; i += 2) dst[C::PU + i] = my_g[C::UOFF + i];
+                }
             } else if (h == 0) {
-                finish_row<C::LDK>(p, my_g, row, n, acc.yy, o_sse, o_reg);
+                finish_row<C::LDK, SCHUR>(p, my_g, row, n, acc.yy, o_sse, o_reg);
             }
         }
         if (p.obj_partial) {   // fixed-order butterfly: deterministic per group
@@ -1895,14 +1952,15 @@ k_als_pair(AlsParams p, PairPlan q) {
 // partials (chunks split over the warps, combined in a fixed order), then
 // warp w solves row w cooperatively (lane i owns row i of A, right-looking
 // Cholesky with shuffles).
-template <int NBK>
+template <int NBK, bool SCHUR = false>
 __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
     using C = PairGeom<NBK>;
     constexpr int LDK = C::LDK;
     constexpr int HW = 8;                            // warps (and hot rows) per CTA
-    constexpr int NE = (C::GRAM + 1 + 31) / 32;      // partial elements per lane
-    __shared__ float part[HW][C::GRAM + 1];
-    __shared__ float Gs[HW][C::GSTRIDE + 1];
+    constexpr int PS = SCHUR ? C::PSTR_S : C::PSTR;  // floats per partial slot
+    constexpr int NE = (PS + 31) / 32;               // partial elements per lane
+    __shared__ float part[HW][PS];
+    __shared__ float Gs[HW][(SCHUR ? C::PSTR_S : C::GSTRIDE) + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // phase 1, row by row: warp w sums chunks s0+w, s0+w+HW, ... (incl.
     // sum w y^2 at GRAM), the HW warp sums are then added in warp order --
@@ -1916,12 +1974,12 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) a[e] = 0.f;
         for (int c = c0 + warp; c < c1; c += HW) {
-            const float *src = p.partials + (size_t)c * C::PSTR;
+            const float *src = p.partials + (size_t)c * PS;
             float v[NE];
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
                 const int i = lane + 32 * e;
-                v[e] = i <= C::GRAM ? __ldcg(src + i) : 0.f;
+                v[e] = i < PS ? __ldcg(src + i) : 0.f;
             }
 #pragma unroll
             for (int e = 0; e < NE; ++e) a[e] += v[e];
@@ -1929,10 +1987,10 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
             const int i = lane + 32 * e;
-            if (i <= C::GRAM) part[warp][i] = a[e];
+            if (i < PS) part[warp][i] = a[e];
         }
         __syncthreads();
-        for (int i = threadIdx.x; i <= C::GRAM; i += 32 * HW) {
+        for (int i = threadIdx.x; i < PS; i += 32 * HW) {
             float t = 0.f;
 #pragma unroll
             for (int w = 0; w < HW; ++w) t += part[w][i];
@@ -1956,6 +2014,17 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
     for (int c = 0; c < LDK; ++c) a[c] = (lane < D && c <= lane) ? G[pidx(lane, c)] : 0.f;
     float b = lane < D ? G[C::RHS0 + lane] : 0.f;
     if (lane < D) b = tax_rhs(p, r, lane, b);
+    float sb = 1.f, db = 0.f, ul = 0.f;
+    if constexpr (SCHUR) {   // eliminate the bias: A -= u u^T / s, c -= u d / s
+        sb = (float)n + (n > 0 ? fmaf(p.bias_lam_n, (float)n, p.bias_lam_c) : 1.f);
+        db = G[C::PD];
+        ul = lane < D ? G[C::PU + lane] : 0.f;
+        const float us = ul / sb;
+#pragma unroll
+        for (int c = 0; c < LDK; ++c)
+            if (lane < D && c <= lane) a[c] = fmaf(-us, G[C::PU + c], a[c]);
+        b = fmaf(-us, db, b);
+    }
     const float b0 = b, yy = G[C::GRAM];
 #pragma unroll
     for (int c = 0; c < LDK; ++c)
@@ -2002,7 +2071,14 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
         const float xj = __shfl_sync(FULL, b, j2);
         if (lane < j2) b = fmaf(-G[pidx(j2, lane)], xj, b);
     }
-    if (lane < p.ld) put_out(p, r, lane, lane < D ? b : 0.f);
+    float bias = 0.f;
+    if constexpr (SCHUR) {   // b = (d - u.f) / s
+        float uf = lane < D ? ul * b : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) uf += __shfl_xor_sync(FULL, uf, o);
+        bias = (db - uf) / sb;
+    }
+    if (lane < p.ld) put_out(p, r, lane, lane < D ? b : (SCHUR && lane == D) ? bias : 0.f);
     if (p.obj_partial) {
         float bx = lane < D ? b0 * b : 0.f, xx = lane < D ? b * b : 0.f;
 #pragma unroll
@@ -2201,28 +2277,28 @@ PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_
 
 bool use_pair(int D) { return D <= 20; }
 
-template <int NBK, int R, bool W, bool FB>
+template <int NBK, int R, bool W, bool FB, bool SC = false>
 int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     using C = PairCfg<NBK, R>;
     const size_t smem = (size_t)C::WARP_BYTES * C::WARPS;
 
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_pair<NBK, R, W, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_pair<NBK, R, W, FB, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, R, W, FB>, C::WARPS * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, R, W, FB, SC>, C::WARPS * 32,
                                                   smem);
     const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
     const int64_t want = ceil_div(groups, C::WARPS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_pair<NBK, R, W, FB><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
+    if (grid > 0) k_als_pair<NBK, R, W, FB, SC><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
-        k_als_heavy<NBK><<<(unsigned)ceil_div(q.n_heavy, 8), 256, 0, s>>>(p, q);
+        k_als_heavy<NBK, SC><<<(unsigned)ceil_div(q.n_heavy, 8), 256, 0, s>>>(p, q);
     if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
     return check_launch("mcf_als_half_step(pair)");
 }
@@ -2230,6 +2306,11 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int nb = (p.D + 3) / 4;
+    if (p.schur) {   // [f | b] rows with the bias eliminated in the epilogue (no weights)
+        if (nb <= 1) return launch_pair<1, 4, false, false, true>(p, q, s);
+        if (nb <= 3) return launch_pair<3, 4, false, false, true>(p, q, s);
+        return launch_pair<5, 4, false, false, true>(p, q, s);
+    }
     if (nb <= 1) return launch_pair<1, 4, W, false>(p, q, s);
     if (nb <= 3) return launch_pair<3, 4, W, false>(p, q, s);
     if (nb == 5) return launch_pair<5, 4, W, true>(p, q, s);
@@ -2324,7 +2405,12 @@ extern "C" int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t
 
 extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D) {
     if (D < 1 || n_list < 0 || slots < 0) return 0;
-    const size_t per = use_pair(D) ? pair_gram(D) : pstride_of(D);
+    size_t per = use_pair(D) ? pair_gram(D) : pstride_of(D);
+    if (D >= 2 && D - 1 <= 20) {   // a bias-last system may run as D - 1 + Schur (+ u, d)
+        const int nb = (D - 1 + 3) / 4;
+        const int ldk = 4 * (nb <= 1 ? 1 : nb <= 3 ? 3 : 5);
+        per = std::max(per, pair_gram(D - 1) + (size_t)ldk + 1);
+    }
     const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
     return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) +
            sizeof(float) * (size_t)slots * per;
@@ -2370,6 +2456,15 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
     p.total_items = total_items;
     p.fail = reinterpret_cast<unsigned long long *>(fail_row);
     p.bias_dim = bias_dim;
+    // a bias in the last coordinate of a D <= 21 system, unweighted: the pair
+    // kernel solves the D - 1 factor coordinates and eliminates the bias
+    // (Schur complement) instead of the 4x4-tile warp kernel on D + 1
+    if (bias_dim >= 1 && bias_dim == D - 1 && D - 1 <= 20 && !wts && !obj_out &&
+        !getenv("MCF_NO_SCHUR")) {
+        p.D = D - 1;
+        p.schur = 1;
+        p.bias_dim = -1;
+    }
     p.peer_out = peer_out;
     p.n_peers = peer_out ? n_peers : 0;
     if (n_peers < 0 || (n_peers > 0 && !peer_out)) {
@@ -2398,10 +2493,24 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         return MCF_E_WORKSPACE;
     }
     p.partials = reinterpret_cast<float *>(static_cast<char *>(ws) + fixed_part);
+    {   // the partial-Gram slots of the hot-row chunks must fit too
+        size_t per;
+        if (p.schur) {
+            const int nb = (p.D + 3) / 4;
+            per = pair_gram(p.D) + (size_t)(4 * (nb <= 1 ? 1 : nb <= 3 ? 3 : 5)) + 1;
+        } else {
+            per = use_pair(p.D) ? pair_gram(p.D) : pstride_of(p.D);
+        }
+        const size_t slots = (size_t)std::max<int64_t>(plan_info[3], plan_info[1]);
+        if (ws_bytes < fixed_part + sizeof(float) * slots * per) {
+            set_error("mcf_als_half_step: workspace too small for the partial slots");
+            return MCF_E_WORKSPACE;
+        }
+    }
     if ((rc = cuda_status(cudaMemsetAsync(p.counters, 0, sizeof(int32_t) * ((size_t)n_list + 64), s),
                           "memset")))
         return rc;
-    if (use_pair(D)) {
+    if (use_pair(p.D)) {
         PairPlan q;
         q.task_row = L.task_row;
         q.task_k0 = L.task_k0;

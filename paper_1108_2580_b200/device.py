@@ -166,7 +166,7 @@ class LayoutSolver:
             buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, PAIR_CHUNK_CAP, adaptive=True)
         else:
             buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, DEFAULT_CHUNK)
-        slots = info[3] if self.D <= 20 else info[1]
+        slots = max(info[1], info[3])   # hot-chunk slots (pair path / warp+CTA paths)
         k = (id(lay), rows_key)
         need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
         if k not in self._ws or self._ws[k].numel() < need:
