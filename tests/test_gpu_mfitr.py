@@ -184,7 +184,8 @@ def _host_params(fs):
 
 
 @pytest.mark.parametrize("fixture,D", [("mfitr.npz", None), ("mfitr_cfg2s.npz", None),
-                                       ("mfitr_cfg2s.npz", 24), ("mfitr_cfg2s.npz", 40)])
+                                       ("mfitr_cfg2s.npz", 20), ("mfitr_cfg2s.npz", 24),
+                                       ("mfitr_cfg2s.npz", 40)])
 def test_full_blocks_zero_gradient_and_monotone(golden, fixture, D):
     """MFITR full blocks: every block solve is exact, so the
     reference's own gradient (grad_mfitr, restated in oracle/ and pinned to
@@ -274,3 +275,26 @@ def test_sharded_mfitr_device_world1_matches_solver(golden):
     P1, Q1 = run.factors()
     P2, Q2 = eng.factors()
     assert torch.equal(P1, P2) and torch.equal(Q1, Q2)
+
+
+def test_schur_bias_equals_coordinate_bias(golden, monkeypatch):
+    """The pair kernel's Schur-complement bias (D + 1 <= 21, D = 20 here) and
+    the plain bias-coordinate solve (MCF_NO_SCHUR: the 4x4-tile warp kernel
+    on D + 1) give the same blocks to fp32 accuracy."""
+    g = dict(golden("mfitr_cfg2s.npz"))
+    rng = np.random.default_rng(20)
+    U, I, D = int(g["U"]), int(g["I"]), 20
+    g["P"], g["Q"] = rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D))
+    g["Qa"] = rng.normal(0, 0.05, (I, D))
+    g["bu"], g["bi"], g["ba"] = rng.normal(0, 1, U), rng.normal(0, 1, I), rng.normal(0, 1, I)
+    g["lam1"] = 0.02
+    outs = []
+    for no_schur in (False, True):
+        if no_schur:
+            monkeypatch.setenv("MCF_NO_SCHUR", "1")
+        fs = _full_solver(g)
+        fs.sweep()
+        fs.check()
+        outs.append(_host_params(fs))
+    for a, b in zip(*outs):
+        assert np.abs(a - b).max() <= 1e-4 * max(np.abs(b).max(), 1e-6)
