@@ -7,33 +7,26 @@
 //     A_r = sum_k w_k x_k x_k^T + (lam_c + lam_n n_r + tau S_r) I
 //     b_r = sum_k w_k (y_k - y_shift) x_k + tau T_r,     out_r = A_r^{-1} b_r
 //
+// Kernel per factor dimension (dispatch / dispatch_pair below):
+//   D <= 20      k_als_pair: row-parallel lane pairs, FFMA2 Gram over a
+//                4-rating cp.async + mbarrier ring, one-lane Cholesky;
+//                hot rows as chunk partials summed by k_als_heavy.  Also the
+//                bias-last D + 1 systems of MFITR (Schur-complement bias).
+//   D 21..28     k_als_warp: 4x4 register tiles, one tile per lane of a team,
+//                shuffle Cholesky.
+//   D 29..103    k_als_tile_warp: warp per work item, 8x8 register tiles,
+//                augmented Gram (rating in column D), blocked register
+//                Cholesky, persistent warps.
+//   D 104..128   k_als_cta: CTA per work item, CTA Cholesky.
 // Work decomposition (the "plan"): every row is cut into chunks of at most
-// CHUNK ratings; one warp owns one chunk (a work item).  Single-chunk rows
-// (all users at cfg1) are solved by the same warp that built their Gram.
-// Rows spanning several chunks (Zipf-hot items, up to ~1 M ratings) write
-// partial Grams to a workspace slot; the last chunk to finish (atomic
-// counter) sums the partials in chunk order -- a fixed order, so results are
-// deterministic and independent of scheduling -- and solves.
-//
-// Gram formation for D <= 28 (NB = ceil(D/4) <= 7 4-wide blocks): a team of
-// TS lanes owns the NB(NB+1)/2 lower-triangle 4x4 tiles of A, one tile per
-// lane, held in registers; 32/TS teams split the ratings of a batch.  Each
-// batch of 32 partner rows is gathered HBM/L2 -> shared memory with 16-byte
-// cp.async (zero-fill past the chunk end), double buffered so the gather of
-// batch j+1 overlaps the FMAs of batch j.  Per rating a lane issues two
-// LDS.128 (its row block and column block) and 16 + 4 FFMA (the diagonal
-// tiles' lanes keep the right-hand side; off-diagonal lanes compute the same
-// 4 rhs FMAs redundantly so the warp never diverges).
-//
-// Solve for D <= 28: the reduced Gram is staged in shared memory, lane i
-// holds row i of A in registers, right-looking Cholesky with shuffles,
-// forward substitution with shuffles, backward substitution reading L^T
-// from shared memory.  fp32 throughout; the pivot test matches the
-// reference (s > 0 and finite, _kernels.py:197).
-//
-// D in 29..128: one CTA per work item, Gram tiles spread over the CTA's
-// threads, CTA-cooperative Cholesky (correctness path for configs 3/4; the
-// tensor-core path for D >= 64 replaces it).
+// CHUNK ratings (on the pair path CHUNK follows the layout size).  Rows
+// spanning several chunks (Zipf-hot items, up to ~1 M ratings) write partial
+// Grams to a workspace slot and are summed in chunk order -- a fixed order,
+// so results are deterministic and independent of scheduling -- then solved.
+// fp32 throughout; the pivot test matches the reference (s > 0 and finite,
+// _kernels.py:197).  Every solved row can also be stored into peer replicas
+// (the fused all-gather of the sharded sweep, put_out).
+
 #include <algorithm>
 #include <cstdlib>
 #include <string>
