@@ -118,7 +118,8 @@ class DeviceRatings:
         self.nnz = int(u.numel())
         self.by_user = SideLayout(u, i, s, num_users, keep_perm)
         self.by_item = SideLayout(i, u, s, num_items, keep_perm)
-        self.global_mean = float(s.double().mean()) if self.nnz else 0.0
+        # float64 sum without a float64 copy of the ratings
+        self.global_mean = float(torch.sum(s, dtype=torch.float64)) / self.nnz if self.nnz else 0.0
 
     @classmethod
     def from_dataset(cls, ds, device=None, keep_perm: bool = False) -> "DeviceRatings":
