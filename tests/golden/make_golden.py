@@ -32,6 +32,9 @@ Fixtures (reference entry point -> file):
   mfitr.npz          mfitr.edge_weights, loss_mfitr, grad_mfitr (every group:
                      p, q, b_u, b_i, b_a, q_a) on a small
                      synth.generate_synthetic instance with random parameters
+  mfitr_sgd.npz      mfitr.train_mfitr (the reference's SGD trainer, 1 thread)
+                     on the mfitr.npz instance: init, shuffles, per-epoch
+                     loss / RMSE, final parameters
   mfitr_cfg2s.npz    config-2 shaped workload (this repo's generator, scaled):
                      reference edge weights, loss_mfitr, grad_mfitr
   formats.npz        data.load_ratings on ratings_small.tsv; modelio.save_model
@@ -272,6 +275,32 @@ def mfitr_fx():
                         grad_bi=grad["b_i"], grad_ba=grad["b_a"], grad_qa=grad["q_a"])
 
 
+def mfitr_sgd_fx():
+    """The reference's own MFITR trainer (SGD, single thread): train_mfitr
+    on the mfitr.npz instance for 3 epochs -- per-epoch loss / validation
+    RMSE / gamma, the seeded shuffles, and the final parameters."""
+    cfg = synth.SynthConfig(users=60, artists=4, albums_per_artist=2, tracks_per_album=6,
+                            ratings_per_user=12, dim=4, drift=False)
+    train, valid, test, g = synth.generate_synthetic(cfg, seed=2)
+    ew = mfitr.edge_weights(g, train)
+    h = mfitr.MfitrHyper(D=4, lam1=1e-3, lam2=0.065, lam3=0.1, lam4=0.05, gamma=0.01,
+                         decay=0.9, iters=3)
+    m0 = mfitr.init_mfitr("mfitr", train, g, h, 5)
+    perms = [np.random.default_rng([5, 2]).permutation(train.num_users)]
+    rng = np.random.default_rng([5, 2])
+    perms = [rng.permutation(train.num_users) for _ in range(h.iters)]
+    m, rep = mfitr.train_mfitr("mfitr", train, valid, g, h, threads=1, seed=5, ew=ew)
+    np.savez_compressed(os.path.join(HERE, "mfitr_sgd.npz"),
+                        P0=m0.base.p, Q0=m0.base.q, Qa0=m0.q_a, mu=m0.base.mu,
+                        perms=np.stack(perms), loss=np.array([r.objective for r in rep]),
+                        rmse=np.array([r.valid_rmse for r in rep]),
+                        gamma=np.array([r.gamma for r in rep]),
+                        P=m.base.p, Q=m.base.q, Qa=m.q_a, bu=m.base.b_u, bi=m.base.b_i, ba=m.b_a,
+                        vu=valid.users, vi=valid.items, vs=valid.scores, seed=5,
+                        lam1=h.lam1, lam2=h.lam2, lam3=h.lam3, lam4=h.lam4, decay=h.decay,
+                        gamma0=0.01)
+
+
 def mfitr_cfg2s():
     """Config-2 shaped MFITR workload (this repo's generator, scaled 0.001):
     the reference's own edge weights (adjusted_cosine over one cached
@@ -363,6 +392,7 @@ def main():
     mfitr_fx()
     als_cfg0()
     mfitr_cfg2s()
+    mfitr_sgd_fx()
     formats()
     print("golden fixtures written to", HERE)
 

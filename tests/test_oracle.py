@@ -183,3 +183,26 @@ def test_layered_item_solve_zeroes_gradient(golden):
         cur = oracle.loss_mfitr(*args(Q))
         assert cur <= last * (1 + 1e-12)
         last = cur
+
+
+def test_mfitr_sgd_epoch_matches_reference_trainer(golden):
+    """oracle.mfitr_sgd_epoch restates the reference's own MFITR trainer
+    (sgd_epoch_mfitr: rate_update over users in the seeded shuffle, then the
+    edge pass, gamma decay): 3 epochs reproduce its parameters and losses."""
+    g = golden("mfitr_sgd.npz")
+    f = golden("mfitr.npz")
+    U, I = int(f["U"]), int(f["I"])
+    P, Q, Qa = g["P0"].copy(), g["Q0"].copy(), g["Qa0"].copy()
+    bu, bi, ba = np.zeros(U), np.zeros(I), np.zeros(I)
+    lam = [float(g[k]) for k in ("lam1", "lam2", "lam3", "lam4")]
+    gamma = float(g["gamma0"])
+    for ep in range(3):
+        oracle.mfitr_sgd_epoch(P, Q, bu, bi, f["art"], ba, Qa, float(g["mu"]), f["users"],
+                               f["items"], f["scores"], g["perms"][ep], f["ec"], f["ep"],
+                               f["w"], gamma, *lam)
+        loss = oracle.loss_mfitr(P, Q, f["users"], f["items"], f["scores"], float(g["mu"]), bu,
+                                 bi, f["art"], ba, Qa, f["ec"], f["ep"], f["w"], *lam)
+        np.testing.assert_allclose(loss, g["loss"][ep], rtol=1e-10)
+        gamma *= float(g["decay"])
+    for a, b in ((P, "P"), (Q, "Q"), (Qa, "Qa"), (bu, "bu"), (bi, "bi"), (ba, "ba")):
+        np.testing.assert_allclose(a, g[b], rtol=1e-10, atol=1e-12)
