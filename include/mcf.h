@@ -31,6 +31,7 @@
  *                      multi-GPU sweep (the reference is single-process)
  *   mcf_als_half_step_bias  the lam1 (bias) / lam2 (factor) regularisers of
  *                      mfitr.loss_mfitr for augmented [f | b] blocks  mfitr.py:226-242
+ *   mcf_mfitr_sgd_epoch  mfitr.sgd_epoch_mfitr (the reference's SGD trainer) mfitr.py:323-336
  *   mcf_mfitr_fixed, mcf_mfitr_targets  the block terms of mfitr._rating_terms
  *                      (prediction mu + b_u + b_i + b_a + (q_i + q_a).p_u)  mfitr.py:203-216
  */
@@ -163,6 +164,24 @@ int mcf_als_half_step_peers(const int64_t *ptr, const int32_t *idx, const float 
  * (Pa = [p | b_u], Qa = [q | b_i], Aa = [q_a | b_a] indexed by artist id). */
 int mcf_mfitr_fixed(const float *main_t, const float *add_t, const int32_t *art, int64_t n,
                     int32_t D, float *out, void *stream);
+
+/* The reference's own MFITR trainer, one epoch of mfitr.sgd_epoch_mfitr
+ * (mfitr.py:323-336; time / implicit terms off): users in order[0..n_order)
+ * (the seeded shuffle), each user's ratings in the by-user layout's order
+ * through _kernels.rate_update (_kernels.py:21-77), then the taxonomy edges
+ * through _kernels.edge_pass_range (_kernels.py:129-148).  Device form:
+ * Hogwild (a warp per user, item-side state updated without locks, atomic
+ * adds in the edge pass), so not bit-reproducible.  Tables [rows][ld(D)];
+ * b_u/b_i/b_a float; art nullable (no artist terms); counter: one device
+ * int32 of scratch.  workers: concurrent user warps (and edge warps) --
+ * 1 reproduces the reference's single-thread order (strictly sequential),
+ * <= 0 uses the whole GPU. */
+int mcf_mfitr_sgd_epoch(const int64_t *uptr, const int32_t *uidx, const float *uval,
+                        const int32_t *order, int32_t n_order, int32_t *counter, float *P,
+                        float *Q, float *b_u, float *b_i, const int32_t *art, float *b_a,
+                        float *Q_a, float mu, int32_t D, float gamma, float lam_bias,
+                        float lam_fac, const int64_t *ec, const int64_t *ep, const double *w,
+                        int64_t E, float lam3, float lam4, int32_t workers, void *stream);
 int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t *idx, const float *val,
                       const int32_t *aux, int32_t n_rows, const float *Pa, const float *Qa,
                       const float *Aa, const int32_t *art, float mu, int32_t D, float *out,

@@ -442,22 +442,129 @@ class MfitrFullSolver:
         return sse + h.lam1 * reg1 + h.lam2 * reg2 + self.tau * (self.w64 * d2).sum()
 
 
+def train_mfitr_sgd(kind: str, train_data: Dataset, validation: Dataset | None,
+                    graph: TaxonomyGraph, hyper: MfitrHyper, seed: int = 0,
+                    ew: TaxonomyEdgeWeights | None = None, num_users: int | None = None,
+                    num_items: int | None = None, *, device=None, objective: bool = True,
+                    workers: int = 0) -> tuple[MfitrModel, list[EpochStats]]:
+    """The reference's own MFITR trainer on device:
+    mfitr.train_mfitr (mfitr.py:347-371) with sgd_epoch_mfitr per epoch --
+    the same seeded init (init_mfitr), the same per-epoch user shuffle
+    (default_rng([seed, 2]), factor.py:166, 408), rate_update over each
+    user's ratings then the edge pass (mcf_mfitr_sgd_epoch, Hogwild across
+    users), gamma *= decay after every epoch; one EpochStats row per epoch
+    with loss_mfitr and the clipped validation RMSE.  workers: concurrent
+    user warps -- 0 (default) the whole GPU (Hogwild; on a small problem the
+    users then see each other's updates much later than in the reference's
+    sequential pass), 1 the reference's single-thread order exactly."""
+    hyper = dataclasses.replace(hyper)
+    model = init_mfitr(kind, train_data, graph, hyper, seed, num_users=num_users,
+                       num_items=num_items)
+    base = model.base
+    r = _ratings_for(train_data, device, False, base.num_users, base.num_items)
+    if ew is None:
+        ew = edge_weights(graph, train_data, device=r.device, num_items=base.num_items)
+    dev = r.device
+    D = base.D
+    ld = _lib.factor_ld(D)
+    f32 = lambda a: torch.as_tensor(np.asarray(_host(a), np.float32), device=dev)  # noqa: E731
+    P = torch.zeros(base.num_users, ld, dtype=torch.float32, device=dev)
+    Q = torch.zeros(base.num_items, ld, dtype=torch.float32, device=dev)
+    Qa = torch.zeros(base.num_items, ld, dtype=torch.float32, device=dev)
+    P[:, :D], Q[:, :D], Qa[:, :D] = f32(base.p), f32(base.q), f32(model.q_a)
+    bu, bi, ba = f32(base.b_u), f32(base.b_i), f32(model.b_a)
+    art = torch.as_tensor(model.artist_of_item.astype(np.int32), device=dev)
+    ec = torch.as_tensor(np.asarray(ew.edge_child, np.int64), device=dev)
+    ep = torch.as_tensor(np.asarray(ew.edge_parent, np.int64), device=dev)
+    w = torch.as_tensor(np.asarray(ew.w, np.float64), device=dev)
+    lay = r.by_user
+    deg = lay.degrees().cpu().numpy()
+    counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    shuffle = np.random.default_rng([seed, 2])
+    eng = AlsEngine(r, D)            # prediction / loss helpers
+    vu = vi = vs = None
+    if validation is not None and len(validation):
+        vu = torch.as_tensor(validation.users.astype(np.int32), device=dev)
+        vi = torch.as_tensor(validation.items.astype(np.int32), device=dev)
+        vs = torch.as_tensor(validation.scores.astype(np.float32), device=dev)
+    rec_u = torch.repeat_interleave(torch.arange(base.num_users, device=dev, dtype=torch.int32),
+                                    lay.degrees())
+    cnt_u, cnt_i = lay.degrees().double(), r.by_item.degrees().double()
+    has = art >= 0
+    cnt_a = torch.zeros(base.num_items, dtype=torch.float64, device=dev)
+    cnt_a.index_add_(0, art[lay.idx.long()][has[lay.idx.long()]].long(),
+                     torch.ones(int(has[lay.idx.long()].sum()), dtype=torch.float64, device=dev))
+    report = []
+    L = _lib.lib()
+    for ep_i in range(hyper.iters):
+        gamma_used = hyper.gamma
+        perm = shuffle.permutation(base.num_users)
+        active = perm[deg[perm] > 0].astype(np.int32)
+        order = torch.as_tensor(active, device=dev)
+        check(L.mcf_mfitr_sgd_epoch(ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(order),
+                                    int(order.numel()), ptr(counter), ptr(P), ptr(Q), ptr(bu),
+                                    ptr(bi), ptr(art), ptr(ba), ptr(Qa), float(base.mu), D,
+                                    float(hyper.gamma), float(hyper.lam1), float(hyper.lam2),
+                                    ptr(ec), ptr(ep), ptr(w), int(ec.numel()), float(hyper.lam3),
+                                    float(hyper.lam4), int(workers), stream_ptr(dev)),
+              "mcf_mfitr_sgd_epoch")
+        base.epochs_done += 1
+        hyper.gamma *= hyper.decay
+        obj = float("nan")
+        if objective:
+            _, sse = eng.predict(rec_u, lay.idx, lay.val, want_pred=False, mu=base.mu, b_u=bu,
+                                 b_i=bi, art=art, b_a=ba, Q_a=Qa, P=P, Q=Q,
+                                 clip=(-3.0e38, 3.0e38))
+            d = lambda x: x.double()  # noqa: E731
+            reg1 = ((cnt_u * d(bu) ** 2).sum() + (cnt_i * d(bi) ** 2).sum()
+                    + (cnt_a * d(ba) ** 2).sum())
+            reg2 = ((cnt_u * (d(P[:, :D]) ** 2).sum(1)).sum()
+                    + (cnt_i * (d(Q[:, :D]) ** 2).sum(1)).sum()
+                    + (cnt_a * (d(Qa[:, :D]) ** 2).sum(1)).sum())
+            d2 = ((d(Q[:, :D])[ec] - d(Q[:, :D])[ep]) ** 2).sum(1)
+            graph_t = (hyper.lam3 + hyper.lam4) * (w * d2).sum()
+            obj = float((sse + hyper.lam1 * reg1 + hyper.lam2 * reg2 + graph_t).item())
+        rm = float("nan")
+        if vu is not None:
+            _, sse = eng.predict(vu, vi, vs, want_pred=False, mu=base.mu, b_u=bu, b_i=bi,
+                                 art=art, b_a=ba, Q_a=Qa, P=P, Q=Q,
+                                 clip=(train_data.scale.lo, train_data.scale.hi))
+            rm = float(torch.sqrt(sse / vu.numel()).item())
+        if not (np.isfinite(obj) if objective else True):
+            raise DivergenceError(f"MFITR SGD diverged at epoch {ep_i}")
+        report.append(EpochStats(ep_i, gamma_used, obj, rm))
+    host = lambda t: t.double().cpu().numpy()  # noqa: E731
+    base.p, base.q, model.q_a = host(P[:, :D]), host(Q[:, :D]), host(Qa[:, :D])
+    base.b_u, base.b_i, model.b_a = host(bu), host(bi), host(ba)
+    eng.set_factors(P[:, :D], Q[:, :D])
+    base.engine = eng
+    model.ew = ew
+    return model, report
+
+
 def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
                 graph: TaxonomyGraph, hyper: MfitrHyper, threads: int = 1, seed: int = 0,
                 binner=None, ew: TaxonomyEdgeWeights | None = None,
                 num_users: int | None = None, num_items: int | None = None, *, init=None,
                 device=None, as_torch: bool = False, objective: bool = True,
-                blocks: str = "full",
+                blocks: str = "full", method: str = "als", sgd_workers: int = 0,
                 ) -> tuple[MfitrModel, list[EpochStats]]:
     """hyper.iters ALS-MFITR sweeps; one EpochStats row per sweep with
     loss_mfitr and the clipped validation RMSE (mfitr.py:347-371 signature).
 
+    method="sgd": the reference's own SGD trainer instead (train_mfitr_sgd).
     blocks="full" (default): every parameter of the reference's MFITR model
     (mfitr.py:92-149) -- [q_i|b_i] per taxonomy layer, [q_a|b_a] per artist,
     [p_u|b_u] (MfitrFullSolver); blocks="q": factors only, biases and q_a
     frozen at 0 (MfitrSolver, the benchmark's configs 2 and 4)."""
     if kind == "time-mfitr":
         raise ConfigError("time-mfitr is outside the device path (no time terms)")
+    if method == "sgd":   # the reference's own trainer (mfitr.py:347-371), on device
+        return train_mfitr_sgd(kind, train_data, validation, graph, hyper, seed, ew,
+                               num_users, num_items, device=device, objective=objective,
+                               workers=sgd_workers)
+    if method != "als":
+        raise ConfigError(f"method must be 'als' or 'sgd', got {method!r}")
     if blocks not in ("full", "q"):
         raise ConfigError(f"blocks must be 'full' or 'q', got {blocks!r}")
     hyper = dataclasses.replace(hyper)

@@ -298,3 +298,37 @@ def test_schur_bias_equals_coordinate_bias(golden, monkeypatch):
         outs.append(_host_params(fs))
     for a, b in zip(*outs):
         assert np.abs(a - b).max() <= 1e-4 * max(np.abs(b).max(), 1e-6)
+
+
+def test_mfitr_sgd_trainer_follows_reference(golden):
+    """train_mfitr(method="sgd"): the reference's own SGD trainer on device
+    (same seeded init and user shuffles, rate_update + edge pass, gamma
+    decay; Hogwild across users) tracks the reference trainer's per-epoch
+    loss and validation RMSE (tests/golden/mfitr_sgd.npz, made by running
+    mfitr.train_mfitr itself)."""
+    from paper_1108_2580_b200 import mfitr
+    from paper_1108_2580_b200.data import Dataset
+    g = golden("mfitr_sgd.npz")
+    f = golden("mfitr.npz")
+    graph = _graph(f)
+    tr = _train(f)
+    va = Dataset.from_arrays(g["vu"], g["vi"], g["vs"], num_users=int(f["U"]),
+                             num_items=int(f["I"]), compact=True)
+    h = mfitr.MfitrHyper(D=4, lam1=float(g["lam1"]), lam2=float(g["lam2"]),
+                         lam3=float(g["lam3"]), lam4=float(g["lam4"]), gamma=float(g["gamma0"]),
+                         decay=float(g["decay"]), iters=3)
+    # one worker: the reference's strictly sequential order -> fp32 rounding only
+    m, rep = mfitr.train_mfitr("mfitr", tr, va, graph, h, seed=int(g["seed"]), method="sgd",
+                               sgd_workers=1)
+    loss = np.array([r.objective for r in rep])
+    rmse = np.array([r.valid_rmse for r in rep])
+    gam = np.array([r.gamma for r in rep])
+    np.testing.assert_allclose(gam, g["gamma"], rtol=1e-6)
+    np.testing.assert_allclose(loss, g["loss"], rtol=2e-3)
+    np.testing.assert_allclose(rmse, g["rmse"], rtol=2e-3)
+    for a, b in ((m.base.p, "P"), (m.base.q, "Q"), (m.b_a, "ba"), (m.base.b_u, "bu")):
+        assert np.abs(a - g[b]).max() < 2e-3 * np.abs(g[b]).max(), b
+    # the whole GPU (Hogwild across users): still a descent on every epoch
+    m2, rep2 = mfitr.train_mfitr("mfitr", tr, va, graph, h, seed=int(g["seed"]), method="sgd")
+    loss2 = np.array([r.objective for r in rep2])
+    assert np.all(np.isfinite(loss2)) and np.all(np.diff(loss2) < 0)
