@@ -1421,6 +1421,7 @@ __device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add, in
                                              float bias_add = 0.f) {
     constexpr int RHS0 = LDK * (LDK + 1) / 2;
     float inv[LDK];
+    float y[LDK];   // forward substitution fused into the row loop (row i of L is in r[])
     bool ok = true;
 #pragma unroll
     for (int i = 0; i < LDK; ++i) {
@@ -1445,19 +1446,13 @@ __device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add, in
             const float ri = rsqrtf(d);
             g[pidx(i, i)] = d * ri;
             inv[i] = ri;
+            float t = g[RHS0 + i];
+#pragma unroll
+            for (int k = 0; k < i; ++k) t = fmaf(-r[k], y[k], t);
+            y[i] = t * ri;
         }
     }
     if (!ok) return false;
-    float y[LDK];
-#pragma unroll
-    for (int i = 0; i < LDK; ++i) {
-        if (i < D) {
-            float t = g[RHS0 + i];
-#pragma unroll
-            for (int k = 0; k < i; ++k) t = fmaf(-g[pidx(i, k)], y[k], t);
-            y[i] = t * inv[i];
-        }
-    }
 #pragma unroll
     for (int i = LDK - 1; i >= 0; --i) {
         if (i < D) {
