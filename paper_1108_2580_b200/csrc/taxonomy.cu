@@ -7,7 +7,7 @@
 // item i that term contributes tau * S_i * q_i to the normal matrix and
 // tau * T_i to the right-hand side, tau = l3 + l4, with
 //     S_i = sum_{e incident to i} w_e,   T_i = sum_{e incident} w_e q_other(e).
-// One warp per item walks the item's incident edges in CSR (= edge-list)
+// A team of lanes per item walks the item's incident edges in CSR (= edge-list)
 // order, lanes own float4 column blocks of q, so the sums have a fixed order.
 #include "common.cuh"
 #include "../../include/mcf.h"
@@ -15,44 +15,38 @@
 namespace mcf {
 namespace {
 
+// A team of TL lanes per item (TL = the power of two >= ld/4, so D = 20
+// packs 4 items into a warp instead of leaving 26 lanes idle); lane sub of
+// the team owns float4 column block sub of T_i.  Per item and column the
+// sums run in edge order exactly as before.
 __global__ void __launch_bounds__(256) k_tax_terms(const int64_t *inc_ptr, const int32_t *inc_edge,
                                                    const int32_t *inc_other, const float *w,
                                                    const float *q, int32_t n_items, int ld,
                                                    const int32_t *row_list, int32_t n_list,
-                                                   float *S, float *T) {
+                                                   float *S, float *T, int TL) {
     const int lane = threadIdx.x & 31;
-    const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int team = lane / TL, sub = lane % TL;
+    const int64_t j = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / TL) +
+                      team;
     if (j >= n_list) return;
     const int i = row_list ? row_list[j] : (int)j;
     const int nq = ld / 4;
-    float4 acc[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float s = 0.f;
     for (int64_t e = inc_ptr[i]; e < inc_ptr[i + 1]; ++e) {
         const float we = w[inc_edge[e]];
         const int o = inc_other[e];
         s += we;
-        const float4 *q4 = reinterpret_cast<const float4 *>(q + (size_t)o * ld);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int blk = lane + 32 * c;
-            if (blk < nq) {
-                const float4 v = q4[blk];
-                acc[c].x = fmaf(we, v.x, acc[c].x);
-                acc[c].y = fmaf(we, v.y, acc[c].y);
-                acc[c].z = fmaf(we, v.z, acc[c].z);
-                acc[c].w = fmaf(we, v.w, acc[c].w);
-            }
+        if (sub < nq) {
+            const float4 v = reinterpret_cast<const float4 *>(q + (size_t)o * ld)[sub];
+            acc.x = fmaf(we, v.x, acc.x);
+            acc.y = fmaf(we, v.y, acc.y);
+            acc.z = fmaf(we, v.z, acc.z);
+            acc.w = fmaf(we, v.w, acc.w);
         }
     }
-    if (lane == 0) S[i] = s;
-    float4 *t4 = reinterpret_cast<float4 *>(T + (size_t)i * ld);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int blk = lane + 32 * c;
-        if (blk < nq) t4[blk] = acc[c];
-    }
+    if (sub == 0) S[i] = s;
+    if (sub < nq) reinterpret_cast<float4 *>(T + (size_t)i * ld)[sub] = acc;
 }
 
 }  // namespace
@@ -71,9 +65,13 @@ extern "C" int mcf_taxonomy_terms(const int64_t *inc_ptr, const int32_t *inc_edg
     const int32_t n = row_list ? n_list : n_items;
     if (n <= 0) return MCF_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    k_tax_terms<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(inc_ptr, inc_edge, inc_other, edge_w, q,
-                                                         n_items, mcf_factor_ld(D), row_list, n,
-                                                         S_out, T_out);
+    const int ld = mcf_factor_ld(D);
+    int TL = 1;
+    while (TL < ld / 4) TL <<= 1;          // ld <= 128 -> TL <= 32
+    const int64_t per_block = 8 * (32 / TL);
+    k_tax_terms<<<(unsigned)ceil_div(n, per_block), 256, 0, s>>>(inc_ptr, inc_edge, inc_other,
+                                                                 edge_w, q, n_items, ld, row_list,
+                                                                 n, S_out, T_out, TL);
     return check_launch("mcf_taxonomy_terms");
 }
 
