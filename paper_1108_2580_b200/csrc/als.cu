@@ -1181,9 +1181,13 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
                         tel(t, rr, c2) = fmaf(-tel(t, rr, c), tel(t, c2, c), tel(t, rr, c2));
             }
 #pragma unroll
-            for (int m = 0; m < 8; ++m)
-#pragma unroll
-                for (int n = 0; n < 8; ++n) Ls[m * 8 + n] = n <= m ? tel(t, m, n) : 0.f;
+            for (int m = 0; m < 8; ++m) {   // row m of L_JJ: two 16-byte stores
+                float4 *d4 = reinterpret_cast<float4 *>(Ls + 8 * m);
+                d4[0] = make_float4(tel(t, m, 0), 1 <= m ? tel(t, m, 1) : 0.f,
+                                    2 <= m ? tel(t, m, 2) : 0.f, 3 <= m ? tel(t, m, 3) : 0.f);
+                d4[1] = make_float4(4 <= m ? tel(t, m, 4) : 0.f, 5 <= m ? tel(t, m, 5) : 0.f,
+                                    6 <= m ? tel(t, m, 6) : 0.f, 7 <= m ? tel(t, m, 7) : 0.f);
+            }
             float yv[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
