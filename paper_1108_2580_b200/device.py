@@ -116,20 +116,8 @@ class DeviceRatings:
         u, i, s = _as_i32(users, dev), _as_i32(items, dev), _as_f32(scores, dev)
         self.device, self.num_users, self.num_items = dev, int(num_users), int(num_items)
         self.nnz = int(u.numel())
-        # the two layout builds are independent (scatter-bound radix passes):
-        # the items layout is built on a side stream, overlapping the users one
-        main = torch.cuda.current_stream(dev)
-        side = torch.cuda.Stream(dev)
-        side.wait_stream(main)
-        for t in (u, i, s):
-            t.record_stream(side)
-        with torch.cuda.stream(side):
-            self.by_item = SideLayout(i, u, s, num_items, keep_perm)
         self.by_user = SideLayout(u, i, s, num_users, keep_perm)
-        main.wait_stream(side)
-        for t in (self.by_item.ptr, self.by_item.idx, self.by_item.val, self.by_item.perm):
-            if t is not None:
-                t.record_stream(main)
+        self.by_item = SideLayout(i, u, s, num_items, keep_perm)
         # float64 sum without a float64 copy of the ratings
         self.global_mean = float(torch.sum(s, dtype=torch.float64)) / self.nnz if self.nnz else 0.0
 
