@@ -284,6 +284,20 @@ class AlsEngine:
         final factors, plus both sides' regularisers."""
         return obj[2:3] + obj[3:4] + obj[1:2]
 
+    def check_with(self, *values):
+        """check() and read device scalars in ONE host synchronisation: the
+        per-sweep metrics of train() ride along with the failure flags."""
+        parts = [v.reshape(-1)[:1].double() for v in values if v is not None]
+        flat = torch.cat(parts + [self._fail_acc.double()]).tolist()
+        items_row, users_row = int(flat[-2]), int(flat[-1])
+        self._fail_acc.fill_(-1)
+        for side, row in (("items", items_row), ("users", users_row)):
+            if row >= 0:
+                raise SingularSystemError(
+                    f"singular normal equations at {side} row {row}; use lam > 0")
+        it = iter(flat[:-2])
+        return [next(it) if v is not None else None for v in values]
+
     def check(self):
         """Synchronise and raise SingularSystemError for a failed row
         (factor.py:535-537); the items half-step runs first in a sweep, so

@@ -319,10 +319,10 @@ def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: Hyp
         elif objective:
             obj = eng.objective(hyper.lam, reg)
         rm = eng.rmse(vu, vi, vs, (train_data.scale.lo, train_data.scale.hi)) if vu is not None else None
-        eng.check()
+        obj_v, rm_v = eng.check_with(obj, rm)     # one host sync per sweep
         report.append(EpochStats(ep, hyper.gamma,
-                                 float(obj.item()) if obj is not None else float("nan"),
-                                 float(rm.item()) if rm is not None else float("nan")))
+                                 float(obj_v) if obj_v is not None else float("nan"),
+                                 float(rm_v) if rm_v is not None else float("nan")))
     if as_torch:
         model.p, model.q = eng.factors()
     else:
