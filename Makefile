@@ -8,8 +8,16 @@ NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
 
 all: $(PKG)/libmcf.so oracle
 
+# ptxas -v output (registers / spills per kernel) goes to build/ptxas.log
 $(PKG)/libmcf.so: $(SRC) $(PKG)/csrc/common.cuh include/mcf.h
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build_ptxas.log || (cat build_ptxas.log; false)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -ldl 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+# micro-benchmarks used for the roofline peaks (profiles/fp32_peak.json)
+MICRO := $(patsubst %.cu,%,$(wildcard tools/micro/*.cu))
+micro: $(MICRO)
+tools/micro/%: tools/micro/%.cu
+	$(NVCC) -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o $@ $<
 
 oracle:
 	$(MAKE) -s -C oracle
@@ -17,4 +25,4 @@ oracle:
 clean:
 	rm -f $(PKG)/libmcf.so oracle/liboracle.so
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean micro

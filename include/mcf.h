@@ -34,6 +34,11 @@
  *   mcf_mfitr_sgd_epoch  mfitr.sgd_epoch_mfitr (the reference's SGD trainer) mfitr.py:323-336
  *   mcf_mfitr_fixed, mcf_mfitr_targets  the block terms of mfitr._rating_terms
  *                      (prediction mu + b_u + b_i + b_a + (q_i + q_a).p_u)  mfitr.py:203-216
+ *   mcf_als_half_step_multicast  the half-step + the replica all-gather through
+ *                      one NVLS multicast store per element
+ *   mcf_comm_*, mcf_allgather_rows  the exchange of the row-sharded sweep
+ *                      (SURVEY §8(b)); the reference's worker layer that hands
+ *                      row blocks to threads, parallel.py:101-145
  */
 #ifndef MCF_H
 #define MCF_H
@@ -148,6 +153,39 @@ int mcf_als_half_step_peers(const int64_t *ptr, const int32_t *idx, const float 
                             int32_t chunk, const void *plan, const int64_t *plan_info,
                             int64_t *fail_row, double *obj_out, void *ws, size_t ws_bytes,
                             float *const *peer_out, int32_t n_peers, void *stream);
+
+/* mcf_als_half_step fused with the all-gather through NVLS multicast: every
+ * solved row of this rank's shard is written with one multimem store to
+ * mc_out, the multicast address of the replicated table (e.g. torch symmetric
+ * memory's multicast_ptr, offset to this rank's shard), which reaches every
+ * GPU's replica, this one's included -- `out` is not written separately.  The
+ * caller orders the next half-step after every rank's stores (a device
+ * barrier).  Other arguments as mcf_als_half_step. */
+int mcf_als_half_step_multicast(const int64_t *ptr, const int32_t *idx, const float *val,
+                                const float *wts, const float *fixed, int64_t n_fixed, float *out,
+                                int32_t D, float lam_c, float lam_n, float y_shift,
+                                const float *tax_S, const float *tax_T, float tau,
+                                const int32_t *row_list, int32_t n_list, int32_t row_lo,
+                                int32_t chunk, const void *plan, const int64_t *plan_info,
+                                int64_t *fail_row, double *obj_out, void *ws, size_t ws_bytes,
+                                float *mc_out, void *stream);
+
+/* ---- multi-GPU exchange: libmcf's own NCCL communicator -------------------
+ * For a C caller that shards the half-step over the GPUs of one node without
+ * torch.distributed.  NCCL is loaded at run time (the copy already in the
+ * process, else libnccl.so.2; MCF_NCCL_LIB overrides).  Rank 0 creates a
+ * unique id (mcf_comm_id_bytes() bytes) and ships it to the other ranks by
+ * any channel; every rank then calls mcf_comm_init on its own device.
+ * mcf_allgather_rows: rows [offsets[k], offsets[k] + counts[k]) of the
+ * [rows][ld] float table belong to rank k; afterwards every rank holds every
+ * rank's rows (one grouped ncclBroadcast per rank, in place, exact sizes). */
+size_t mcf_comm_id_bytes(void);
+int mcf_comm_get_unique_id(void *id_out, size_t id_bytes);
+int mcf_comm_init(const void *id, size_t id_bytes, int32_t nranks, int32_t rank,
+                  void **comm_out);
+int mcf_comm_destroy(void *comm);
+int mcf_allgather_rows(void *comm, float *table, int32_t ld, const int64_t *offsets,
+                       const int64_t *counts, void *stream);
 
 /* ---- MFITR full-model blocks (mfitr.py:203-216 prediction) -----------------
  * Tables are [rows][mcf_factor_ld(D + 1)] with the factor in columns 0..D-1

@@ -183,6 +183,60 @@ int64_t oracle_als_half_step(int64_t row_lo, int64_t row_hi, const int64_t *ptr,
     return failed;
 }
 
+/* The same half-step with rows handed out dynamically (an atomic counter,
+ * 16 rows at a time) instead of static blocks: rows are independent, so the
+ * output is bit-identical to oracle_als_half_step; used to check full-size
+ * configurations, whose Zipf-hot rows serialise static blocks.  The minimum
+ * failing row is returned, but a failing row does not stop other rows. */
+typedef struct {
+    block_arg base;
+    int64_t *next;
+} dyn_arg;
+
+static void *dyn_main(void *p) {
+    dyn_arg *a = (dyn_arg *)p;
+    block_arg *b = &a->base;
+    for (;;) {
+        const int64_t lo = __atomic_fetch_add(a->next, 16, __ATOMIC_RELAXED);
+        if (lo >= b->hi) break;
+        const int64_t hi = lo + 16 < b->hi ? lo + 16 : b->hi;
+        for (int64_t r = lo; r < hi; ++r) {
+            int64_t f = oracle_als_solve_rows(r, r + 1, b->ptr, b->idx, b->val, b->wts, b->fixed,
+                                              b->D, b->out, b->lam_c, b->lam_n, b->tax_S,
+                                              b->tax_T, b->tau);
+            if (f >= 0 && (b->failed < 0 || f < b->failed)) b->failed = f;
+        }
+    }
+    return NULL;
+}
+
+int64_t oracle_als_half_step_dynamic(int64_t row_lo, int64_t row_hi, const int64_t *ptr,
+                                     const int64_t *idx, const double *val, const double *wts,
+                                     const double *fixed, int64_t D, double *out, double lam_c,
+                                     double lam_n, const double *tax_S, const double *tax_T,
+                                     double tau, int threads) {
+    if (threads < 1) threads = 1;
+    int64_t next = row_lo;
+    dyn_arg *args = (dyn_arg *)calloc((size_t)threads, sizeof(dyn_arg));
+    pthread_t *tid = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    for (int t = 0; t < threads; ++t) {
+        block_arg a = {row_lo, row_hi, ptr, idx, val, wts, fixed, tax_S, tax_T, D, out,
+                       lam_c, lam_n, tau, -1};
+        args[t].base = a;
+        args[t].next = &next;
+        pthread_create(&tid[t], NULL, dyn_main, &args[t]);
+    }
+    int64_t failed = -1;
+    for (int t = 0; t < threads; ++t) {
+        pthread_join(tid[t], NULL);
+        const int64_t f = args[t].base.failed;
+        if (f >= 0 && (failed < 0 || f < failed)) failed = f;
+    }
+    free(args);
+    free(tid);
+    return failed;
+}
+
 /* mu + b_u + b_i (+ b_a) + (q_i (+ q_a)) . p_u with the reference's
  * cold-start rules (_kernels.py:344-375); arts may be NULL (ALS). */
 void oracle_predict(const int64_t *qu, const int64_t *qi, int64_t n, double mu,

@@ -41,6 +41,15 @@ SIGNATURES = {
                                         vp, vp, c_f32, vp, c_i32, c_i32, c_i32, vp,
                                         ctypes.POINTER(c_i64), vp, vp, vp, c_size, vp, c_i32,
                                         vp]),
+    "mcf_als_half_step_multicast": (c_int, [vp, vp, vp, vp, vp, c_i64, vp, c_i32, c_f32, c_f32,
+                                            c_f32, vp, vp, c_f32, vp, c_i32, c_i32, c_i32, vp,
+                                            ctypes.POINTER(c_i64), vp, vp, vp, c_size, vp, vp]),
+    "mcf_comm_id_bytes": (c_size, []),
+    "mcf_comm_get_unique_id": (c_int, [vp, c_size]),
+    "mcf_comm_init": (c_int, [vp, c_size, c_i32, c_i32, ctypes.POINTER(vp)]),
+    "mcf_comm_destroy": (c_int, [vp]),
+    "mcf_allgather_rows": (c_int, [vp, vp, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
+                                   vp]),
     "mcf_mfitr_fixed": (c_int, [vp, vp, vp, c_i64, c_i32, vp, vp]),
     "mcf_mfitr_sgd_epoch": (c_int, [vp, vp, vp, vp, c_i32, vp, vp, vp, vp, vp, vp, vp, vp, c_f32,
                                     c_i32, c_f32, c_f32, c_f32, vp, vp, vp, c_i64, c_f32, c_f32,

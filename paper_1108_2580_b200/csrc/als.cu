@@ -69,6 +69,10 @@ struct AlsParams {
     // n_peers peer replicas (NVLink peer pointers, same row offsets as out)
     float *const *peer_out;
     int n_peers;
+    // fused all-gather through NVLS multicast: the multicast address of the
+    // replicated table (offset to this shard); one multimem store reaches
+    // every GPU's replica, this one's included (replaces out + peer_out)
+    float *mc_out;
     // Schur bias (pair path): the rows are [f | b] with f in columns 0..D-1
     // and b in column D; the kernel accumulates u = sum x, d = sum y beside
     // the Gram and eliminates b exactly: (A - u u^T/s) f = c - u d/s,
@@ -79,6 +83,11 @@ struct AlsParams {
 // one element of row r of the solved shard: local table + every peer replica
 __device__ __forceinline__ void put_out(const AlsParams &p, int r, int i, float v) {
     const size_t off = (size_t)r * p.ld + i;
+    if (p.mc_out) {
+        asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p.mc_out + off), "f"(v)
+                     : "memory");
+        return;
+    }
     p.out[off] = v;
     for (int k = 0; k < p.n_peers; ++k) p.peer_out[k][off] = v;
 }
@@ -2417,7 +2426,7 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
                           const int64_t *plan_info, int64_t *fail_row, double *obj_out, void *ws,
                           size_t ws_bytes, void *stream, int32_t bias_dim, float bias_lam_c,
                           float bias_lam_n, float *const *peer_out = nullptr,
-                          int32_t n_peers = 0) {
+                          int32_t n_peers = 0, float *mc_out = nullptr) {
     if (D < 1 || D > 128) {
         set_error("mcf_als_half_step: D must be in [1, 128]");
         return MCF_E_UNSUPPORTED;
@@ -2460,6 +2469,7 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
     }
     p.peer_out = peer_out;
     p.n_peers = peer_out ? n_peers : 0;
+    p.mc_out = mc_out;
     if (n_peers < 0 || (n_peers > 0 && !peer_out)) {
         set_error("mcf_als_half_step: peer_out must hold n_peers >= 0 device pointers");
         return MCF_E_ARG;
@@ -2569,4 +2579,22 @@ extern "C" int mcf_als_half_step_peers(const int64_t *ptr, const int32_t *idx, c
     return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
                           tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
                           obj_out, ws, ws_bytes, stream, -1, 0.f, 0.f, peer_out, n_peers);
+}
+
+extern "C" int mcf_als_half_step_multicast(const int64_t *ptr, const int32_t *idx,
+                                           const float *val, const float *wts, const float *fixed,
+                                           int64_t n_fixed, float *out, int32_t D, float lam_c,
+                                           float lam_n, float y_shift, const float *tax_S,
+                                           const float *tax_T, float tau, const int32_t *row_list,
+                                           int32_t n_list, int32_t row_lo, int32_t chunk,
+                                           const void *plan, const int64_t *plan_info,
+                                           int64_t *fail_row, double *obj_out, void *ws,
+                                           size_t ws_bytes, float *mc_out, void *stream) {
+    if (!mc_out) {
+        set_error("mcf_als_half_step_multicast: mc_out (multicast address) is required");
+        return MCF_E_ARG;
+    }
+    return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
+                          tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
+                          obj_out, ws, ws_bytes, stream, -1, 0.f, 0.f, nullptr, 0, mc_out);
 }

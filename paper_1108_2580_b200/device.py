@@ -148,12 +148,15 @@ class LayoutSolver:
               y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
               fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None,
               val: torch.Tensor | None = None, bias=None, peers: torch.Tensor | None = None,
-              chunk: int | None = None):
+              chunk: int | None = None, multicast: int | None = None):
         """bias = (dim, lam_c, lam_n): coordinate `dim` is a bias with its own
         regulariser (mcf_als_half_step_bias); val: per-rating targets in the
         layout's CSR order instead of the ratings; peers: device int64 tensor
         of peer replica pointers -- the kernel stores every solved row there
-        too (mcf_als_half_step_peers, the fused all-gather)."""
+        too (mcf_als_half_step_peers, the fused all-gather); multicast: the
+        NVLS multicast address of the replicated table at this shard -- one
+        multimem store per element reaches every replica
+        (mcf_als_half_step_multicast)."""
         dev = lay.device
         if fail is None:
             if self.fail is None:
@@ -174,6 +177,16 @@ class LayoutSolver:
             self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = self._ws[k]
         vals = lay.val if val is None else val
+        if multicast is not None:
+            if bias is not None or peers is not None:
+                raise ConfigError("multicast stores exclude bias blocks and peer stores")
+            check(_lib.lib().mcf_als_half_step_multicast(
+                ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(wts), ptr(fixed), fixed.shape[0],
+                ptr(out), self.D, float(lam_c), float(lam_n), float(y_shift), ptr(tax_S),
+                ptr(tax_T), float(tau), ptr(rl), n_list, 0, chunk, ptr(buf), info, ptr(fail),
+                ptr(obj_out), ptr(ws), ws.numel(), int(multicast), stream_ptr(dev)),
+                "mcf_als_half_step_multicast")
+            return fail
         if peers is not None:
             if bias is not None:
                 raise ConfigError("bias blocks and peer stores are not combined")
@@ -357,7 +370,15 @@ class AlsEngine:
                     torch.arange(self.r.num_users, device=self.device, dtype=torch.int32),
                     lay.degrees())
             users, items, scores = self._rows_of_records, lay.idx, lay.val
-        _, sse = self.predict(users, items, scores, want_pred=False, clip=(-3.0e38, 3.0e38))
+            w = self._wts.get("users")      # record weights in the users layout's order
+        else:
+            w = None
+        if w is not None:
+            # the reference's weighted data term sum w (r - q.p)^2 (factor.py:541-547)
+            pred, _ = self.predict(users, items, None, want_pred=True)
+            sse = (w.double() * (scores.double() - pred.double()) ** 2).sum().reshape(1)
+        else:
+            _, sse = self.predict(users, items, scores, want_pred=False, clip=(-3.0e38, 3.0e38))
         if reg == "weighted":
             regp = self.sq_norms(self.P, self.r.by_user.ptr)
             regq = self.sq_norms(self.Q, self.r.by_item.ptr)

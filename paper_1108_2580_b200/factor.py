@@ -11,7 +11,12 @@ Additive keyword-only options:
 * ``init``: ``(P0, Q0)`` initial factors instead of the reference's uniform
   draw (BASELINE initialises N(0, 0.1));
 * ``device``: the CUDA device; ``as_torch``: keep the fitted factors as
-  device tensors instead of numpy float64 copies.
+  device tensors instead of numpy float64 copies;
+* ``devices``: ``N > 1`` fits with the rows of each half-step sharded over N
+  GPUs -- the device form of the reference's ``threads`` (parallel.py:134-145,
+  factor.py:528-534): one process per GPU (``torchrun --nproc-per-node N``)
+  and every rank calls ``train(..., devices=N)`` on the same data (SPMD);
+  results are identical to one GPU (G-invariance) and returned on every rank.
 
 ``threads`` is accepted and ignored (the device decides the parallelism).
 There is no CPU fallback: without libmcf.so or a GPU these raise DeviceError.
@@ -261,11 +266,29 @@ class EpochStats:
     valid_rmse: float
 
 
+def sharded_world(devices) -> int:
+    """World size of a devices= request: 1 (single GPU) or N > 1, which needs
+    an initialised torch.distributed group of exactly N ranks (one process
+    per GPU)."""
+    if devices is None:
+        return 1
+    n = len(devices) if isinstance(devices, (list, tuple)) else int(devices)
+    if n <= 1:
+        return 1
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() != n:
+        raise ConfigError(
+            f"devices={n}: the sharded fit runs one process per GPU -- launch {n} ranks "
+            f"(torchrun --nproc-per-node {n}), init_process_group('nccl'), and call "
+            f"train(..., devices={n}) on every rank")
+    return n
+
+
 def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: HyperParams,
           threads: int = 1, seed: int = 0, binner=None, weights: np.ndarray | None = None,
           num_users: int | None = None, num_items: int | None = None, *, reg: str | None = None,
           init=None, device=None, as_torch: bool = False, objective: bool = True,
-          ) -> tuple[FactorModel, list[EpochStats]]:
+          devices=None, collective: str = "nccl") -> tuple[FactorModel, list[EpochStats]]:
     """hyper.iters ALS sweeps from a seeded (or given) initialisation; one
     EpochStats row per sweep with the training objective and the clipped
     validation RMSE (factor.py:595-618).  Factors, layouts and the
@@ -293,6 +316,12 @@ def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: Hyp
     else:
         model = init_model(kind, train_data, hyper, seed, num_users=num_users,
                            num_items=num_items)
+    world = sharded_world(devices)
+    if world > 1:
+        if weights is not None:
+            raise ConfigError("per-observation weights are not supported by the sharded fit")
+        return _train_sharded(model, train_data, validation, hyper, reg, init, device, as_torch,
+                              objective, collective)
     eng = _engine_for(model, train_data, device, keep_perm=weights is not None)
     if init is not None:
         # uploaded as given (fp32 stays fp32; a pinned source copies asynchronously)
@@ -328,3 +357,80 @@ def train(kind: str, train_data: Dataset, validation: Dataset | None, hyper: Hyp
     else:
         _sync_host(model)
     return model, report
+
+
+def _train_sharded(model: FactorModel, train_data: Dataset, validation, hyper: HyperParams,
+                   reg: str, init, device, as_torch: bool, objective: bool, collective: str):
+    """train() with rows sharded over the ranks of the default process group
+    (parallel.ShardedAls): each rank solves its nnz-balanced row ranges and the
+    solved rows are all-gathered after every half-step.  Per sweep, the
+    objective terms are summed over ranks and failures reduced to the minimum
+    global row (one host synchronisation); the held-out RMSE is evaluated on
+    every rank from the replicated factors."""
+    import torch.distributed as dist
+
+    from .parallel import ShardedAls
+    dev = cuda_device(device if device is not None else
+                      torch.device("cuda", torch.cuda.current_device()))
+    lam_c, lam_n = _lam_pair(hyper.lam, reg)
+    U, I, D = model.num_users, model.num_items, model.D
+    run = ShardedAls(train_data.users, train_data.items, train_data.scores, U, I, D,
+                     device=dev, collective=collective)
+    P0, Q0 = (init if init is not None else (model.p, model.q))
+    run.set_factors(P0, Q0)
+    ev = _standalone_engine_for(U, I, D, dev)
+    vu = vi = vs = None
+    if validation is not None and len(validation):
+        vu = torch.as_tensor(validation.users.astype(np.int32), device=dev)
+        vi = torch.as_tensor(validation.items.astype(np.int32), device=dev)
+        vs = torch.as_tensor(validation.scores.astype(np.float32), device=dev)
+    fused = objective and D <= 20
+    obj_buf = torch.zeros(4, dtype=torch.float64, device=dev) if fused else None
+    report: list[EpochStats] = []
+    for ep in range(hyper.iters):
+        run.sweep(lam_c, lam_n, obj_buf)
+        model.epochs_done += 1
+        terms = torch.zeros(1, dtype=torch.float64, device=dev)
+        if fused:
+            terms = obj_buf[2:3] + obj_buf[3:4] + obj_buf[1:2]   # my rows' share
+        elif objective:
+            terms = _sharded_objective(run, ev, hyper.lam, reg)
+        dist.all_reduce(terms)
+        run.check()                                            # all-reduce MIN of failures
+        rm = None
+        if vu is not None:
+            _, sse = ev.predict(vu, vi, vs, want_pred=False, P=run.P, Q=run.Q,
+                                clip=(train_data.scale.lo, train_data.scale.hi))
+            rm = torch.sqrt(sse / vu.numel())
+        vals = torch.cat([terms, rm if rm is not None else terms]).tolist()
+        report.append(EpochStats(ep, hyper.gamma, float(vals[0]) if objective else float("nan"),
+                                 float(vals[1]) if rm is not None else float("nan")))
+    P, Q = run.factors()
+    ev.set_factors(P, Q)
+    model.engine = ev
+    if as_torch:
+        model.p, model.q = ev.factors()
+    else:
+        model.p, model.q = P.double().cpu().numpy(), Q.double().cpu().numpy()
+    return model, report
+
+
+def _standalone_engine_for(U: int, I: int, D: int, dev) -> AlsEngine:
+    empty = np.zeros(0, np.int32)
+    return AlsEngine(DeviceRatings(empty, empty, np.zeros(0, np.float32), U, I, dev), D)
+
+
+def _sharded_objective(run, ev: AlsEngine, lam: float, reg: str) -> torch.Tensor:
+    """This rank's share of the objective: the data term over its users'
+    ratings and the regulariser of its own rows (D > 20, no fused epilogue)."""
+    lay_u, lay_i = run.local["users"], run.local["items"]
+    ulo, uhi = run.umap.range(run.rank)
+    ilo, ihi = run.imap.range(run.rank)
+    rows = ulo + torch.repeat_interleave(
+        torch.arange(lay_u.n_rows, device=run.device, dtype=torch.int32), lay_u.degrees())
+    _, sse = ev.predict(rows.to(torch.int32), lay_u.idx, lay_u.val, want_pred=False, P=run.P,
+                        Q=run.Q, clip=(-3.0e38, 3.0e38))
+    wu = lay_u.ptr if reg == "weighted" else None
+    wi = lay_i.ptr if reg == "weighted" else None
+    reg_t = ev.sq_norms(run.P[ulo:uhi], wu) + ev.sq_norms(run.Q[ilo:ihi], wi)
+    return sse + lam * reg_t

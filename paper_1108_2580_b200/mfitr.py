@@ -214,18 +214,24 @@ class MfitrSolver:
         self.T = torch.zeros(I, engine.ld, dtype=torch.float32, device=dev)
         self.tau = hyper.lam3 + hyper.lam4
 
-    def item_layers(self):
-        L = _lib.lib()
+    def solve_layer(self, k: int):
+        """Layer k of the item half-step: S/T from the current Q, then the
+        layer's rows solved exactly."""
         eng, h = self.eng, self.hyper
-        for k, rows in enumerate(self.layers):
-            if rows.numel() == 0:
-                continue
-            check(L.mcf_taxonomy_terms(ptr(self.inc_ptr), ptr(self.inc_edge), ptr(self.inc_other),
-                                       ptr(self.w), ptr(eng.Q), eng.r.num_items, eng.D,
-                                       ptr(rows), rows.numel(), ptr(self.S), ptr(self.T),
-                                       stream_ptr(eng.device)), "mcf_taxonomy_terms")
-            eng.half_step("items", 0.0, h.lam2, self.mu, self.S, self.T, self.tau, rows=rows,
-                          rows_key=("layer", k))
+        rows = self.layers[k]
+        if rows.numel() == 0:
+            return
+        check(_lib.lib().mcf_taxonomy_terms(ptr(self.inc_ptr), ptr(self.inc_edge),
+                                            ptr(self.inc_other), ptr(self.w), ptr(eng.Q),
+                                            eng.r.num_items, eng.D, ptr(rows), rows.numel(),
+                                            ptr(self.S), ptr(self.T), stream_ptr(eng.device)),
+              "mcf_taxonomy_terms")
+        eng.half_step("items", 0.0, h.lam2, self.mu, self.S, self.T, self.tau, rows=rows,
+                      rows_key=("layer", k))
+
+    def item_layers(self):
+        for k in range(len(self.layers)):
+            self.solve_layer(k)
 
     def users(self):
         self.eng.half_step("users", 0.0, self.hyper.lam2, self.mu)
@@ -329,6 +335,15 @@ class MfitrFullSolver:
         self.tau = hyper.lam3 + hyper.lam4
         self.solver = LayoutSolver(D + 1, chunk)
         self.fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
+        # every solve resets `fail`; the first failing row of each block
+        # (items layers, artists, users) since the last check() is kept here
+        self._fail_acc = torch.full((3,), -1, dtype=torch.int64, device=dev)
+
+    BLOCKS = ("items", "artists", "users")
+
+    def _fold(self, block: int):
+        acc = self._fail_acc[block:block + 1]
+        torch.where(acc < 0, self.fail, acc, out=acc)
 
     def _bias(self):
         return (self.D, 0.0, self.hyper.lam1)
@@ -369,18 +384,21 @@ class MfitrFullSolver:
             self.solver.solve(self.r.by_item, self.Xu, self.Qa, 0.0, h.lam2, 0.0, self.S, self.T,
                               self.tau, rows, ("layer", k), None, self.fail, None,
                               val=self.t_items, bias=self._bias())
+            self._fold(0)
 
     def artists(self):
         self._fixed(self.Pa, None, None, self.U, self.Xu)
         self._targets(2, self.by_artist, self.art_item, self.t_art)
         self.solver.solve(self.by_artist, self.Xu, self.Aa, 0.0, self.hyper.lam2, fail=self.fail,
                           val=self.t_art, bias=self._bias())
+        self._fold(1)
 
     def users(self):
         self._fixed(self.Qa, self.Aa, self.art, self.I, self.Xi)
         self._targets(0, self.r.by_user, None, self.t_users)
         self.solver.solve(self.r.by_user, self.Xi, self.Pa, 0.0, self.hyper.lam2, fail=self.fail,
                           val=self.t_users, bias=self._bias())
+        self._fold(2)
 
     def sweep(self):
         self.item_layers()
@@ -388,11 +406,14 @@ class MfitrFullSolver:
         self.users()
 
     def check(self):
-        row = int(self.fail.item())
-        self.fail.fill_(-1)
-        if row >= 0:
-            from .errors import SingularSystemError
-            raise SingularSystemError(f"singular MFITR block system at row {row}")
+        """Raise SingularSystemError for the first block (in sweep order)
+        that had a failing row since the last check."""
+        rows = [int(x) for x in self._fail_acc.tolist()]
+        self._fail_acc.fill_(-1)
+        for block, row in zip(self.BLOCKS, rows):
+            if row >= 0:
+                from .errors import SingularSystemError
+                raise SingularSystemError(f"singular MFITR block system at {block} row {row}")
 
     def params(self):
         """(P, Q, b_u, b_i, b_a, Q_a) device views."""
@@ -548,7 +569,7 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
                 num_users: int | None = None, num_items: int | None = None, *, init=None,
                 device=None, as_torch: bool = False, objective: bool = True,
                 blocks: str = "full", method: str = "als", sgd_workers: int = 0,
-                ) -> tuple[MfitrModel, list[EpochStats]]:
+                devices=None) -> tuple[MfitrModel, list[EpochStats]]:
     """hyper.iters ALS-MFITR sweeps; one EpochStats row per sweep with
     loss_mfitr and the clipped validation RMSE (mfitr.py:347-371 signature).
 
@@ -556,7 +577,11 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
     blocks="full" (default): every parameter of the reference's MFITR model
     (mfitr.py:92-149) -- [q_i|b_i] per taxonomy layer, [q_a|b_a] per artist,
     [p_u|b_u] (MfitrFullSolver); blocks="q": factors only, biases and q_a
-    frozen at 0 (MfitrSolver, the benchmark's configs 2 and 4)."""
+    frozen at 0 (MfitrSolver, the benchmark's configs 2 and 4).
+    devices=N > 1 (blocks="q"): the factor blocks sharded over N GPUs, one
+    process per GPU calling train_mfitr(..., devices=N) on the same data --
+    users by nnz, items by whole taxonomy subtree (parallel.ShardedMfitr);
+    identical results for any N."""
     if kind == "time-mfitr":
         raise ConfigError("time-mfitr is outside the device path (no time terms)")
     if method == "sgd":   # the reference's own trainer (mfitr.py:347-371), on device
@@ -567,6 +592,10 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
         raise ConfigError(f"method must be 'als' or 'sgd', got {method!r}")
     if blocks not in ("full", "q"):
         raise ConfigError(f"blocks must be 'full' or 'q', got {blocks!r}")
+    from .factor import sharded_world
+    world = sharded_world(devices)
+    if world > 1 and blocks != "q":
+        raise ConfigError("the sharded ALS-MFITR fit covers the factor blocks (blocks='q')")
     hyper = dataclasses.replace(hyper)
     model = init_mfitr(kind, train_data, graph, hyper, seed, num_users=num_users,
                        num_items=num_items)
@@ -586,6 +615,9 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
         vs = torch.as_tensor(validation.scores.astype(np.float32), device=dev)
     clip = (train_data.scale.lo, train_data.scale.hi)
     report = []
+    if world > 1:
+        return _train_mfitr_sharded(model, train_data, graph, ew, hyper, dev, (vu, vi, vs), clip,
+                                    objective, as_torch)
     if blocks == "full":
         solver = MfitrFullSolver(r, graph, ew.w, hyper, base.mu, model.artist_of_item, base.p,
                                  base.q, model.q_a, base.b_u, base.b_i, model.b_a)
@@ -635,3 +667,69 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
         base.p, base.q = P.double().cpu().numpy(), Q.double().cpu().numpy()
     model.ew = ew
     return model, report
+
+
+def _train_mfitr_sharded(model: MfitrModel, train_data: Dataset, graph: TaxonomyGraph,
+                         ew: TaxonomyEdgeWeights, hyper: MfitrHyper, dev, valid, clip,
+                         objective: bool, as_torch: bool):
+    """train_mfitr(blocks='q') over the ranks of the default process group
+    (parallel.ShardedMfitr).  Per sweep: loss_mfitr (time off, biases and q_a
+    at 0) from the replicated factors, the clipped held-out RMSE, and the
+    failure check reduced over ranks."""
+    from .factor import _standalone_engine_for
+    from .parallel import ShardedMfitr
+    base = model.base
+    U, I, D = base.num_users, base.num_items, base.D
+    run = ShardedMfitr(train_data.users, train_data.items, train_data.scores, U, I, D, graph,
+                       ew.w, hyper.lam2, hyper.lam3 + hyper.lam4, base.mu, device=dev)
+    run.set_factors(base.p, base.q)
+    ev = _standalone_engine_for(U, I, D, dev)
+    art = torch.as_tensor(model.artist_of_item.astype(np.int32), device=dev)
+    vu, vi, vs = valid
+    w64 = torch.as_tensor(np.asarray(ew.w, np.float64), device=dev)
+    ec = torch.as_tensor(graph.edge_child, device=dev)
+    ep = torch.as_tensor(graph.edge_parent, device=dev)
+    report = []
+    for it in range(hyper.iters):
+        run.sweep()
+        base.epochs_done += 1
+        run.check()
+        P, Q = run.factors()
+        ev.set_factors(P, Q)
+        obj = float("nan")
+        if objective:
+            obj = float(_loss_q(ev, train_data, dev, base.mu, hyper, w64, ec, ep).item())
+        rm = float("nan")
+        if vu is not None:
+            _, sse = ev.predict(vu, vi, vs, want_pred=False, mu=base.mu, art=art,
+                                Q_a=torch.zeros_like(ev.Q), clip=clip)
+            rm = float(torch.sqrt(sse / vu.numel()).item())
+        report.append(EpochStats(it, hyper.gamma, obj, rm))
+    base.engine = ev
+    if as_torch:
+        base.p, base.q = ev.factors()
+    else:
+        P, Q = ev.factors()
+        base.p, base.q = P.double().cpu().numpy(), Q.double().cpu().numpy()
+    model.ew = ew
+    return model, report
+
+
+def _loss_q(ev: AlsEngine, train_data: Dataset, dev, mu: float, hyper: MfitrHyper, w64, ec, ep):
+    """loss_mfitr with biases / q_a at 0 and time off (mfitr.py:219-242) from
+    replicated factors over the full training split."""
+    cache = train_data.__dict__.setdefault("_loss_q_cache", {})
+    key = str(dev)
+    if key not in cache:
+        u = torch.as_tensor(np.asarray(train_data.users, np.int32), device=dev)
+        i = torch.as_tensor(np.asarray(train_data.items, np.int32), device=dev)
+        s = torch.as_tensor(np.asarray(train_data.scores, np.float32), device=dev)
+        cu = torch.bincount(u.long(), minlength=ev.P.shape[0]).double()
+        ci = torch.bincount(i.long(), minlength=ev.Q.shape[0]).double()
+        cache[key] = (u, i, s, cu, ci)
+    u, i, s, cu, ci = cache[key]
+    _, sse = ev.predict(u, i, s, want_pred=False, mu=mu, clip=(-3.0e38, 3.0e38))
+    P, Q = (t.double() for t in ev.factors())
+    reg = (cu * (P ** 2).sum(1)).sum() + (ci * (Q ** 2).sum(1)).sum()
+    d2 = ((Q[ec] - Q[ep]) ** 2).sum(1)
+    return sse + hyper.lam2 * reg + (hyper.lam3 + hyper.lam4) * (w64 * d2).sum()

@@ -75,3 +75,22 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(root, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt, f
+
+
+def test_integration_md_binding_matches_header():
+    """Every argtypes list INTEGRATION.md documents equals the binding
+    generated from include/mcf.h (_lib.SIGNATURES), argument for argument."""
+    from paper_1108_2580_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libmcf.so not built")
+    from integration_snippets import load_binding, snippets
+    assert len(snippets()) >= 2
+    ns = load_binding()
+    L = ns["L"]
+    documented = set(re.findall(r"L\.(mcf_[a-z0-9_]+)\.argtypes", "".join(snippets())))
+    assert "mcf_als_half_step" in documented and len(documented) >= 8
+    for name in sorted(documented):
+        got = getattr(L, name).argtypes
+        want = _lib.SIGNATURES[name][1]
+        assert len(got) == len(want), (name, len(got), len(want))
+        assert list(got) == list(want), name

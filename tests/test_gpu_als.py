@@ -361,6 +361,27 @@ def test_fused_objective_matches_explicit(golden, reg, D):
     assert abs(fused - ref) < 1e-4 * ref, (fused, explicit, ref)
 
 
+@pytest.mark.parametrize("D", [10, 24])
+def test_train_objective_with_observation_weights(golden, D):
+    """train(..., weights=w) reports the reference's weighted objective
+    sum w (r - q.p)^2 + lam (|P|^2 + |Q|^2) (factor.py:541-547) on both the
+    fused (D <= 20) and the explicit (D > 20) objective paths."""
+    from paper_1108_2580_b200 import factor
+    from paper_1108_2580_b200.data import Dataset
+    g = golden("als_cfg0.npz")
+    u, i, s = g["train_users"], g["train_items"], g["train_scores"]
+    U, I = int(g["U"]), int(g["I"])
+    tr = Dataset.from_arrays(u, i, s, num_users=U, num_items=I)
+    w = np.random.default_rng(5).uniform(0.2, 2.0, len(tr))
+    hp = factor.HyperParams(lam=0.5, D=D, iters=2)
+    rng = np.random.default_rng(1)
+    init = (rng.normal(0, 0.1, (U, D)).astype(np.float32),
+            rng.normal(0, 0.1, (I, D)).astype(np.float32))
+    model, rep = factor.train("wals", tr, None, hp, weights=w, init=init)
+    ref = factor.als_objective(model, tr, hp.lam, w)
+    assert abs(rep[-1].objective - ref) < 1e-4 * ref, (rep[-1].objective, ref)
+
+
 def test_fused_peer_stores_replicate_every_row():
     """mcf_als_half_step_peers: the solve kernel writes every solved row into
     each peer replica too (the fused all-gather of the sharded sweep) -- two

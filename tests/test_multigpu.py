@@ -1,8 +1,10 @@
 """Multi-GPU G-invariance on a real multi-GPU box (the device
 analogue of the reference's thread-count invariance): factors
 after row-sharded sweeps on 2 GPUs equal the 1-GPU factors bit for bit, for
-ALS with the NCCL all-gather, ALS with the fused peer stores (symmetric
-memory), and ALS-MFITR sharded by taxonomy subtree.  Skipped when fewer than
+ALS with the NCCL all-gather (torch and libmcf's own communicator), ALS
+with the fused peer stores and NVLS multicast stores (symmetric memory),
+ALS-MFITR sharded by taxonomy subtree, and the public factor.train(...,
+devices=2).  Skipped when fewer than
 2 GPUs are visible (this round's boxes have one)."""
 import os
 import socket
@@ -61,17 +63,30 @@ def _mfitr():
     return [t.cpu().numpy() for t in run.factors()]
 
 
+def _train(devices):
+    from paper_1108_2580_b200 import factor
+    from paper_1108_2580_b200.data import Dataset
+    u, i, s, U, I, D, P0, Q0 = _data()
+    tr = Dataset.from_arrays(u, i, s, num_users=U, num_items=I)
+    hp = factor.HyperParams(lam=0.065, D=D, iters=2)
+    model, rep = factor.train("wals", tr, None, hp, reg="weighted", init=(P0, Q0),
+                              devices=devices)
+    return [model.p, model.q, np.array([r.objective for r in rep])]
+
+
 def _worker(rank, world, port, results):
     import torch.distributed as dist
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world, device_id=torch.device("cuda", rank))
     try:
-        out = {"nccl": _als("nccl"), "mfitr": _mfitr()}
-        try:
-            out["peer"] = _als("peer")
-        except Exception as e:   # symmetric memory unavailable on this box
-            out["peer_error"] = repr(e)
+        out = {"nccl": _als("nccl"), "mcf": _als("mcf"), "mfitr": _mfitr(),
+               "train": _train(2)}
+        for coll in ("peer", "multicast"):
+            try:
+                out[coll] = _als(coll)
+            except Exception as e:   # symmetric memory / NVLS unavailable on this box
+                out[f"{coll}_error"] = repr(e)
         if rank == 0:
             results.update(out)
     finally:
@@ -81,13 +96,22 @@ def _worker(rank, world, port, results):
 def test_two_gpus_equal_one_gpu():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs (this box has fewer)")
-    ref = {"nccl": _als("nccl"), "mfitr": _mfitr()}
+    ref = {"nccl": _als("nccl"), "mfitr": _mfitr(), "train": _train(None)}
     with mp.Manager() as man:
         res = man.dict()
         mp.spawn(_worker, args=(2, _port(), res), nprocs=2, join=True)
         for k in ("nccl", "mfitr"):
             assert all(np.array_equal(a, b) for a, b in zip(res[k], ref[k])), k
-        if "peer" in res:
-            assert all(np.array_equal(a, b) for a, b in zip(res["peer"], ref["nccl"]))
-        else:
-            pytest.skip(f"fused peer path not exercised: {res.get('peer_error')}")
+        assert all(np.array_equal(a, b) for a, b in zip(res["mcf"], ref["nccl"]))
+        P2, Q2, obj2 = res["train"]
+        P1, Q1, obj1 = ref["train"]
+        assert np.array_equal(P2, P1) and np.array_equal(Q2, Q1)
+        np.testing.assert_allclose(obj2, obj1, rtol=1e-9)    # summed over ranks
+        missing = []
+        for coll in ("peer", "multicast"):
+            if coll in res:
+                assert all(np.array_equal(a, b) for a, b in zip(res[coll], ref["nccl"])), coll
+            else:
+                missing.append(f"{coll}: {res.get(coll + '_error')}")
+        if missing:
+            pytest.skip("fused path not exercised: " + "; ".join(missing))

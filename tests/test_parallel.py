@@ -53,8 +53,8 @@ def test_cuts_balanced_and_cover():
         assert sum(loads) == int(deg.sum())
         assert max(loads) <= int(deg.sum()) // w + int(deg.max())
     m = ShardMap(nnz_balanced_cuts(deg, 3))
-    pad = m.padded_index()
-    assert pad.unique().numel() == deg.numel() and int(pad.max()) < m.rows
+    assert sum(m.sizes) == m.rows == deg.numel()
+    assert torch.equal(m.table_index(), torch.arange(deg.numel()))
 
 
 def _worker(rank, world, port, results):
@@ -113,10 +113,10 @@ class OracleMfitrSolver:
     def __init__(self):
         self.fail = None
 
-    def terms(self, run, padded_rows):
-        pc, pp, w = run.edges_padded
+    def terms(self, run, table_rows):
+        pc, pp, w = run.edges_table
         S, T = oracle.taxonomy_terms(pc, pp, w, run.Q[:, : run.D].double().numpy(), run.imap.rows)
-        r = padded_rows.to(torch.int64)
+        r = table_rows.to(torch.int64)
         run.S_t[r] = torch.from_numpy(S[r.numpy()]).float()
         run.T_t[r, : run.D] = torch.from_numpy(T[r.numpy()]).float()
 
@@ -188,7 +188,10 @@ def test_subtree_cuts_keep_every_edge_local():
         loads = np.bincount(owner, weights=deg, minlength=world)
         assert loads.max() <= deg.sum() / world + cw.max()     # LPT bound
         m = PermMap(owner, world, "cpu")
-        assert np.unique(m.padded_np).size == I and m.padded_np.max() < m.rows
+        assert np.array_equal(np.sort(m.table_np), np.arange(I))      # exact, no padding
+        for r in range(world):                                         # rank-major blocks
+            lo, hi = m.range(r)
+            assert np.all(owner[m.global_rows(r).numpy()] == r) and hi - lo == m.counts[r]
 
 
 @pytest.mark.parametrize("world", [2])
@@ -226,3 +229,49 @@ def test_sharded_mfitr_g_invariant_and_oracle(world):
         res, f = oracle.solve_rows(ucsr, Q, U, 0.0, lam2)
         P = res.astype(np.float32).astype(np.float64)
     assert np.array_equal(P1, P.astype(np.float32)) and np.array_equal(Q1, Q.astype(np.float32))
+
+
+# ---------------------------------------------------------------------------
+# a failing row on one rank is raised on every rank, as its global row id
+
+class FailingSolver(OracleSolver):
+    """Reports local row 1 of the items layout of rank 1 as singular."""
+
+    def __init__(self, rank):
+        super().__init__()
+        self.rank = rank
+
+    def solve(self, lay, fixed, out, lam_c, lam_n):
+        super().solve(lay, fixed, out, lam_c, lam_n)
+        bad = self.rank == 1 and out.shape[0] == lay.n_rows and getattr(lay, "side", "") == "items"
+        return torch.tensor([1 if bad else -1], dtype=torch.int64)
+
+
+def _fail_worker(rank, world, port, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1108_2580_b200.errors import SingularSystemError
+        u, i, s, U, I, D, P0, Q0 = _data()
+        run = ShardedAls(u, i, s, U, I, D, solver=FailingSolver(rank), device="cpu")
+        for side, lay in run.local.items():
+            lay.side = side
+        run.set_factors(P0, Q0)
+        run.sweep(0.0, 0.065)
+        try:
+            run.check()
+            results[f"r{rank}"] = "no error"
+        except SingularSystemError as e:
+            results[f"r{rank}"] = str(e)
+        results[f"lo{rank}"] = run.imap.range(1)[0]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_failure_raised_on_every_rank():
+    with mp.Manager() as man:
+        res = man.dict()
+        mp.spawn(_fail_worker, args=(2, _free_port(), res), nprocs=2, join=True)
+        row = res["lo0"] + 1                       # rank 1's local row 1, global id
+        assert res["r0"] == res["r1"]
+        assert f"items row {row}" in res["r0"], res["r0"]
