@@ -1,0 +1,839 @@
+// ALS half-step, wide path on the 5th-generation tensor cores (sm_100a):
+// Gram, Cholesky and both substitutions of every row system in one
+// persistent kernel, the system never leaving the SM.
+//
+// Replaces _kernels.als_solve_rows (reference _kernels.py:151-215) for
+// 21 <= D <= 127 without per-observation weights; same plan, same
+// arithmetic contract as als.cu:
+//     A_r = sum_k x_k x_k^T + (lam_c + lam_n n_r + tau S_r) I,
+//     b_r = sum_k (y_k - y_shift) x_k + tau T_r,   out_r = A_r^{-1} b_r.
+//
+// Team = 4 warps (128 threads = the 128 TMEM lanes); 4 teams per CTA, each
+// owning DP = round_up(D + 1, 16) TMEM columns: the augmented system
+// [x | y] [x | y]^T of its current row lives in TMEM (lane m = row m).
+//
+// * Gram: 16 ratings per stage.  The team gathers the partner rows (fp32,
+//   16-byte loads, prefetched one stage ahead, ids two ahead), scales them
+//   by a power of two s (ratings by s_y) and splits every value into fp16
+//   h + l (22 significant bits); the rating rides in column D.  Tiles H and
+//   L2 = 2 l are stored MN-major (no swizzle: 8 ratings x 16 B core
+//   matrices), exactly as gathered -- no transpose.  One thread issues
+//       C' += H H^T + H L2^T      (tcgen05.mma kind::f16, M 128, N DP, K 16)
+//   so that (C'[i][j] + C'[j][i]) / 2 = sum (h_i h_j + h_i l_j + l_i h_j):
+//   fp32-class products from two MMAs (the dropped l l^T term is ~2^-22).
+// * Cholesky: right-looking, 16-column blocks.  Per block the panel is read
+//   from TMEM (tcgen05.ld), symmetrised against the block rows (C' + C'^T)/2,
+//   regularised (lam_c + lam_n n + tau S, scaled), the 16 x 16 diagonal block
+//   factorised by 16 lanes (MUFU.RSQ pivots, the reference's > 0 and finite
+//   test), the panel solved by every row thread, written back to TMEM (L),
+//   split into fp16 h / 2 l K-major tiles, and the trailing update
+//       C' -= P_h P_h^T + P_h (2 P_l)^T
+//   issued as two negated MMAs on the trailing columns only.  The rating
+//   row D is factorised with the rest: its L entries are z = L^{-1} b (the
+//   forward substitution rides along).
+// * Back substitution L^T x = z by 16-row blocks (L read back from TMEM),
+//   rescaled by s / s_y, stored like every other path (put_out).
+// * Hot rows (more than `chunk` ratings): every chunk dumps its C' to a
+//   workspace slot; the last chunk to finish sums the slots in chunk order
+//   (deterministic) into TMEM (tcgen05.st) and solves.
+//
+// Scaling: s and s_y are powers of two chosen per call (k_tc_prep) so that
+// every scaled diagonal entry stays below 2^30: all panel values then fit
+// fp16 (|L_ij| <= sqrt(A_ii) < 2^15) and the result is exact rescaling.
+
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "als_params.cuh"
+#include "../../include/mcf.h"
+
+namespace mcf {
+namespace {
+
+constexpr int TC_TEAMS = 4;   // teams (4 warps each) per CTA
+constexpr int TC_NST = 2;     // Gram pipeline stages per team
+
+__host__ __device__ constexpr int tc_pow2_cols(int c) {
+    return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+template <int NBLK>
+struct TcCfg {
+    static constexpr int DP = 16 * NBLK;           // padded dimension (features = rows of L)
+    static constexpr int NCH = DP / 8;             // 16-byte fp16 chunks per operand row
+    static constexpr int KG = NCH * 128;           // bytes per 8-rating k-group (MN-major)
+    static constexpr int TILE = 2 * KG;            // 16 ratings
+    static constexpr int YT = 512;                 // rating tile: 16 ratings x 16 cols (y_h, y_l)
+    static constexpr int STAGE = 2 * TILE + YT;    // H | L | Y
+    static constexpr int PT = 2 * KG;              // panel tile: DP rows x 16 k, K-major
+    static constexpr int COLS = DP + 16;           // TMEM columns per team: Gram | rhs
+    static constexpr int OFF_PH = TC_NST * STAGE;
+    static constexpr int OFF_PL = OFF_PH + PT;
+    static constexpr int OFF_LJJ = OFF_PL + PT;    // L_JJ, column-major 16 x 16
+    static constexpr int OFF_RD = OFF_LJJ + 1024;  // 1 / L_ii [DP]
+    static constexpr int OFF_Z = OFF_RD + DP * 4;  // z = L^{-1} b [DP]
+    static constexpr int OFF_X = OFF_Z + DP * 4;   // x [128]
+    static constexpr int OFF_L = OFF_X + 512;      // L, packed rows (row r at r(r+1)/2)
+    static constexpr int TEAM_BYTES = (OFF_L + DP * (DP + 1) / 2 * 4 + 127) / 128 * 128;
+    static constexpr int SLACK = 2048;             // operand over-read past the last team
+    static constexpr int TEAMS = (4 * TEAM_BYTES + SLACK <= 227 * 1024 && 4 * COLS <= 512) ? 4 : 3;
+    static constexpr int SMEM = TEAMS * TEAM_BYTES + SLACK;
+    static constexpr int TMEM_COLS = tc_pow2_cols(TEAMS * COLS);
+    static constexpr int ITEMS = (16 * NCH + 127) / 128;   // gather items per thread per stage
+    static_assert(SMEM <= 227 * 1024 && TEAMS * COLS <= 512, "tensor-core path resources");
+};
+
+struct TcWs {
+    unsigned *scal;      // [0] max|x| bits, [1] max|y| bits, [2] max n, [3] max tau*S bits
+    int32_t *hot_count;  // [slots] chunks finished per hot row (at its first slot)
+    float *partials;     // [slots][DP * (DP + 16)]
+    int64_t n_slots;
+    unsigned long long *prof;   // phase cycle counters (MCF_TC_PROF) or null
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void team_bar(int team) {
+    asm volatile("bar.sync %0, 128;" ::"r"(team + 1) : "memory");
+}
+// shared-memory matrix descriptor, no swizzle (version 1, sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+// kind::f16 instruction descriptor: fp16 A/B, fp32 accumulator, M = 128
+__device__ __forceinline__ uint32_t idesc(int N, bool mn_major, bool neg_a) {
+    return (1u << 4) | (neg_a ? 1u << 13 : 0u) | (mn_major ? (1u << 15) | (1u << 16) : 0u) |
+           ((uint32_t)(N >> 3) << 17) | (8u << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t id,
+                                     uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+// all threads of a warp wait for an mbarrier phase: lane 0 polls (no
+// suspend), the warp follows
+__device__ __forceinline__ void warp_mbar_wait(uint32_t bar, uint32_t parity) {
+    if ((threadIdx.x & 31) == 0) {
+        uint32_t done = 0;
+        do {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(bar), "r"(parity)
+                : "memory");
+        } while (!done);
+    }
+    __syncwarp();
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void proxy_fence() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// fp32 -> (h, l) fp16 pairs: v = h + l with h = rn(v), l = rn(v - h)
+__device__ __forceinline__ void split2(float a, float b, uint32_t &h, uint32_t &l2) {
+    const __half2 hh = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+    h = *reinterpret_cast<const uint32_t *>(&hh);
+    l2 = *reinterpret_cast<const uint32_t *>(&ll);
+}
+
+// power of two s with s^2 * den <= 2^30 (1 when den == 0)
+__device__ __forceinline__ float tc_scale(float den) {
+    if (!(den > 0.f) || !isfinite(den)) return 1.f;
+    const float e = floorf(0.5f * log2f(1073741824.f / den));
+    return exp2f(fminf(fmaxf(e, -100.f), 40.f));
+}
+
+// maxima for the scales, over the planned rows' ratings and the fixed table;
+// zeroes the hot-row chunk counters
+__global__ void k_tc_prep(AlsParams p, PairPlan q, TcWs w) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nthr = gridDim.x * blockDim.x;
+    for (int64_t i = tid; i < w.n_slots; i += nthr) w.hot_count[i] = 0;
+    float mx = 0.f, my = 0.f, ms = 0.f;
+    unsigned mn = 0;
+    const int64_t nf = p.n_fixed * (int64_t)p.ld;
+    for (int64_t i = tid; i < nf; i += nthr) {
+        if ((int)(i % p.ld) < p.D) mx = fmaxf(mx, fabsf(__ldg(p.fixed + i)));
+    }
+    // ratings: a warp per task, lanes over its ratings
+    const int warp = tid >> 5, lane = threadIdx.x & 31, nwarps = nthr >> 5;
+    for (int64_t t = warp; t < q.n_tasks; t += nwarps) {
+        const int r = q.task_row[t];
+        const int64_t k0 = q.task_k0[t];
+        const int n = q.task_n[t];
+        for (int k = lane; k < n; k += 32) my = fmaxf(my, fabsf(__ldg(p.val + k0 + k) - p.y_shift));
+        if (lane == 0) {
+            mn = max(mn, (unsigned)(p.ptr[r + 1] - p.ptr[r]));
+            if (p.tax_S) ms = fmaxf(ms, p.tau * fabsf(p.tax_S[r]));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+        my = fmaxf(my, __shfl_xor_sync(FULL, my, o));
+        ms = fmaxf(ms, __shfl_xor_sync(FULL, ms, o));
+        mn = max(mn, __shfl_xor_sync(FULL, mn, o));
+    }
+    if (lane == 0) {
+        atomicMax(&w.scal[0], __float_as_uint(mx));
+        atomicMax(&w.scal[1], __float_as_uint(my));
+        atomicMax(&w.scal[2], mn);
+        atomicMax(&w.scal[3], __float_as_uint(ms));
+    }
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void ffma2(float &x, float &y, float a, float bx, float by) {
+    unsigned long long A, B, C;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(A) : "f"(a));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(B) : "f"(bx), "f"(by));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(C) : "f"(x), "f"(y));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(C));
+}
+__device__ __forceinline__ void lds16(const float *p, float (&v)[16]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 t = reinterpret_cast<const float4 *>(p)[q];
+        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+    }
+}
+
+template <int NBLK>
+__global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs w) {
+    using C = TcCfg<NBLK>;
+    constexpr int DP = C::DP;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ __align__(8) unsigned long long bars[4][TC_NST + 1];
+    __shared__ int64_t team_task[4];
+    __shared__ int team_flag[4];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int team = warp >> 2, wq = warp & 3, m = threadIdx.x & 127;
+    unsigned char *tb = smem_raw + team * C::TEAM_BYTES;
+    const uint32_t tbs = smem_u32(tb);
+    float *Ljj = reinterpret_cast<float *>(tb + C::OFF_LJJ);
+    float *rdiag = reinterpret_cast<float *>(tb + C::OFF_RD);
+    float *zbuf = reinterpret_cast<float *>(tb + C::OFF_Z);
+    float *xbuf = reinterpret_cast<float *>(tb + C::OFF_X);
+    float *Ls = reinterpret_cast<float *>(tb + C::OFF_L);
+    const uint32_t bar0 = smem_u32(&bars[team][0]);
+    const uint32_t cbar = bar0 + 8 * TC_NST;
+
+    for (int e = threadIdx.x; e < C::SMEM / 16; e += blockDim.x)
+        reinterpret_cast<uint4 *>(smem_raw)[e] = make_uint4(0u, 0u, 0u, 0u);
+    if (m == 0) {
+        for (int st = 0; st <= TC_NST; ++st) mbar_init(bar0 + 8 * st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_sh)),
+                     "r"(C::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh + (uint32_t)(team * C::COLS);
+    const uint32_t tl = tmem + ((uint32_t)(32 * wq) << 16);   // this warp's lane quadrant
+
+    const int D = p.D;
+    const float xmax = __uint_as_float(w.scal[0]), ymax = __uint_as_float(w.scal[1]);
+    const float nmax = (float)w.scal[2], smax = __uint_as_float(w.scal[3]);
+    const float regmax = p.lam_c + p.lam_n * nmax + smax + 1.f +
+                         (p.bias_dim >= 0 ? p.bias_lam_c + p.bias_lam_n * nmax : 0.f);
+    const float s = tc_scale(nmax * xmax * xmax + regmax);
+    const float sy = ymax > 0.f ? exp2f(floorf(log2f(16384.f / ymax))) : 1.f;
+    const float s2 = s * s, ssy = s * sy, out_scale = s / sy;
+
+    const uint32_t id_gram = idesc(DP, true, false);
+    const uint32_t id_rhs = idesc(16, true, false);
+    const int ldc = p.ld / 8;                  // 8-float chunks of a fixed row
+    const int nchu = (D + 7) / 8;              // chunks holding features
+    unsigned gst = 0;                          // Gram stages issued by this team
+    unsigned cph = 0;                          // Cholesky barrier phase
+    long long tcp_t = clock64();
+    unsigned long long tcp_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define TCP(k)                                                       \
+    do {                                                             \
+        if (w.prof && m == 0) {                                      \
+            const long long t1_ = clock64();                         \
+            tcp_acc[k] += (unsigned long long)(t1_ - tcp_t);         \
+            tcp_t = t1_;                                             \
+        }                                                            \
+    } while (0)
+
+    for (;;) {
+        if (m == 0) team_task[team] = atomicAdd(q.group_counter, 1);
+        team_bar(team);
+        const int64_t task = team_task[team];
+        if (task >= q.n_tasks) break;
+        const int row = q.task_row[task];
+        const int64_t k0 = q.task_k0[task];
+        const int n = q.task_n[task];
+        const int slot = q.task_slot[task];
+        const int64_t nrow = p.ptr[row + 1] - p.ptr[row];
+        const float Srow = p.tax_S ? p.tax_S[row] : 0.f;
+        if (nrow == 0 && Srow == 0.f) {   // empty row: 0 with a regulariser, else singular
+            if (p.lam_c > 0.f || p.lam_n > 0.f) {
+                if (m < p.ld) put_out(p, row, m, 0.f);
+            } else if (m == 0) {
+                report_fail(p.fail, row);
+            }
+            team_bar(team);   // team_task is rewritten next
+            continue;
+        }
+        TCP(0);
+
+        // ---------------- Gram: C = H H^T + H L^T + L H^T, rhs = (H + L) [y_h y_l]
+        const int nst = (n + 15) >> 4;
+        if (nst == 0) {   // taxonomy-only row: zero accumulator
+            float zr[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) zr[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c <= NBLK; ++c) tmem_st16(tl + 16 * c, zr);
+            tmem_wait_st();
+        }
+        int idc[C::ITEMS], idn[C::ITEMS];
+        float4 dc[C::ITEMS][2];
+        float yc = 0.f, yn = 0.f;   // thread m < 16: rating of stage rating m
+        auto load_ids = [&](int st, int (&ids)[C::ITEMS], float &y) {
+#pragma unroll
+            for (int t = 0; t < C::ITEMS; ++t) {
+                const int e = m + 128 * t, kk = e & 15, c = e >> 4;
+                const int kr = 16 * st + kk;
+                ids[t] = (c < nchu && kr < n) ? __ldg(p.idx + k0 + kr) : -1;
+            }
+            const int kr = 16 * st + m;
+            y = (m < 16 && kr < n) ? __ldg(p.val + k0 + kr) - p.y_shift : 0.f;
+        };
+        auto load_data = [&](const int (&ids)[C::ITEMS], float4 (&d)[C::ITEMS][2]) {
+#pragma unroll
+            for (int t = 0; t < C::ITEMS; ++t) {
+                const int c = (m + 128 * t) >> 4;
+                if (ids[t] >= 0 && c < ldc) {
+                    const float4 *src = reinterpret_cast<const float4 *>(
+                        p.fixed + (size_t)ids[t] * p.ld + 8 * c);
+                    d[t][0] = __ldg(src);
+                    d[t][1] = __ldg(src + 1);
+                } else {
+                    d[t][0] = d[t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        };
+        if (nst > 0) {
+            load_ids(0, idc, yc);
+            load_data(idc, dc);
+            if (nst > 1) load_ids(1, idn, yn);
+        }
+        for (int st = 0; st < nst; ++st) {
+            float4 dn[C::ITEMS][2];
+            int idn2[C::ITEMS];
+            float yn2 = 0.f;
+            if (st + 1 < nst) load_data(idn, dn);
+            if (st + 2 < nst) load_ids(st + 2, idn2, yn2);
+            const unsigned b = gst % TC_NST;
+            if (gst >= TC_NST) warp_mbar_wait(bar0 + 8 * b, ((gst / TC_NST) - 1) & 1);
+            unsigned char *H = tb + b * C::STAGE;
+#pragma unroll
+            for (int t = 0; t < C::ITEMS; ++t) {
+                const int e = m + 128 * t, kk = e & 15, c = e >> 4;
+                if (c < nchu) {
+                    const float v[8] = {dc[t][0].x * s, dc[t][0].y * s, dc[t][0].z * s, dc[t][0].w * s,
+                                        dc[t][1].x * s, dc[t][1].y * s, dc[t][1].z * s, dc[t][1].w * s};
+                    uint4 hv, lv;
+                    split2(v[0], v[1], hv.x, lv.x);
+                    split2(v[2], v[3], hv.y, lv.y);
+                    split2(v[4], v[5], hv.z, lv.z);
+                    split2(v[6], v[7], hv.w, lv.w);
+                    const int off = (kk >> 3) * C::KG + c * 128 + (kk & 7) * 16;
+                    *reinterpret_cast<uint4 *>(H + off) = hv;
+                    *reinterpret_cast<uint4 *>(H + C::TILE + off) = lv;
+                }
+            }
+            if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l)
+                uint32_t yh, yl;
+                split2(yc * sy, 0.f, yh, yl);
+                const uint32_t pair = (yh & 0xffffu) | (yl << 16);
+                *reinterpret_cast<uint32_t *>(H + 2 * C::TILE + (m >> 3) * 256 + (m & 7) * 16) = pair;
+            }
+            proxy_fence();
+            team_bar(team);
+            if (m == 0) {
+                tc_fence_after();
+                const uint32_t ha = tbs + b * C::STAGE;
+                const uint64_t dh = sdesc(ha, C::KG, 128), dl = sdesc(ha + C::TILE, C::KG, 128);
+                const uint64_t dy = sdesc(ha + 2 * C::TILE, 256, 128);
+                const uint32_t acc = st > 0 ? 1u : 0u;
+                umma(tmem, dh, dh, id_gram, acc);
+                umma(tmem, dh, dl, id_gram, 1u);
+                umma(tmem, dl, dh, id_gram, 1u);
+                umma(tmem + DP, dh, dy, id_rhs, acc);
+                umma(tmem + DP, dl, dy, id_rhs, 1u);
+                umma_commit(bar0 + 8 * b);
+            }
+            ++gst;
+#pragma unroll
+            for (int t = 0; t < C::ITEMS; ++t) {
+                dc[t][0] = dn[t][0];
+                dc[t][1] = dn[t][1];
+                idc[t] = idn[t];
+                idn[t] = idn2[t];
+            }
+            yc = yn;
+            yn = yn2;
+        }
+        if (nst > 0) {
+            const unsigned g = gst - 1;
+            warp_mbar_wait(bar0 + 8 * (g % TC_NST), (g / TC_NST) & 1);
+            tc_fence_after();
+        }
+        TCP(1);
+
+        // ---------------- hot-row chunk: dump C | rhs, the last chunk sums them
+        if (slot >= 0) {
+            float *dst = w.partials + (size_t)slot * DP * C::COLS + (size_t)m * C::COLS;
+#pragma unroll 1
+            for (int c = 0; c <= NBLK; ++c) {
+                float v[16];
+                tmem_ld16(tl + 16 * c, v);
+                tmem_wait_ld();
+                if (m < DP) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        __stcg(reinterpret_cast<float4 *>(dst + 16 * c + j),
+                               make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                }
+            }
+            __threadfence();
+            tc_fence_before();
+            team_bar(team);
+            const int chunk_i = (int)((k0 - p.ptr[row]) / p.chunk);
+            const int s0 = slot - chunk_i;
+            const int nch = (int)((nrow + p.chunk - 1) / p.chunk);
+            if (m == 0) team_flag[team] = atomicAdd(w.hot_count + s0, 1) == nch - 1;
+            team_bar(team);
+            if (!team_flag[team]) continue;
+            __threadfence();
+#pragma unroll 1
+            for (int c = 0; c <= NBLK; ++c) {
+                float acc[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+                if (m < DP) {
+                    for (int sl = s0; sl < s0 + nch; ++sl) {
+                        const float4 *src = reinterpret_cast<const float4 *>(
+                            w.partials + (size_t)sl * DP * C::COLS + (size_t)m * C::COLS + 16 * c);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float4 v = __ldcg(src + j);
+                            acc[4 * j] += v.x;
+                            acc[4 * j + 1] += v.y;
+                            acc[4 * j + 2] += v.z;
+                            acc[4 * j + 3] += v.w;
+                        }
+                    }
+                }
+                tmem_st16(tl + 16 * c, acc);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            team_bar(team);
+            tc_fence_after();
+        }
+        TCP(2);
+
+        // ---------------- blocked Cholesky, forward substitution fused.  Padding
+        // coordinates (>= D) have zero Gram rows and a unit regulariser: pivot
+        // s^2, L = s I there, z = x = 0 -- every block runs the same code.
+        float rg = s2;   // this row's regulariser (scaled)
+        float r;         // rhs b_m, reduced by the finished blocks (forward subst.)
+        {
+            const float diag = p.lam_c + p.lam_n * (float)nrow + p.tau * Srow;
+            if (m < D) rg = diag_at(p, m, diag, (float)nrow) * s2;
+            uint32_t rb[2];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                         : "=r"(rb[0]), "=r"(rb[1])
+                         : "r"(tl + DP));
+            tmem_wait_ld();
+            r = __uint_as_float(rb[0]) + __uint_as_float(rb[1]);
+            if (m < D && p.tax_T && m != p.bias_dim)
+                r = fmaf(ssy * p.tau, p.tax_T[(size_t)row * p.ld + m], r);
+        }
+        bool failed = false;
+#pragma unroll 1
+        for (int J = 0; J < NBLK; ++J) {
+            const int c0 = 16 * J;
+            const int dw = c0 >> 5, lo = c0 & 31, ime = lane - lo;
+            const bool inblk = wq == dw && ime >= 0 && ime < 16;
+            float a[16];
+            if (32 * wq + 31 >= c0) tmem_ld16(tl + c0, a);
+            if (wq == dw) {
+                const long long dt0 = clock64();
+                tmem_wait_ld();
+                const long long dt1 = clock64();
+                float fa[16], fr = inblk ? r : 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) fa[i] = inblk ? a[i] + (i == ime ? rg : 0.f) : 0.f;
+                // right-looking on the unscaled Schur complement: a_mj -= a_mi a_ij / p_i
+                // (rows above the pivot are finished; their upper entries are never read)
+                float piv[16], ri[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float lj[16];
+                    piv[i] = __shfl_sync(FULL, fa[i], lo + i);
+#pragma unroll
+                    for (int j = i + 1; j < 16; ++j) lj[j] = __shfl_sync(FULL, fa[i], lo + j);
+                    const float rv = __shfl_sync(FULL, fr, lo + i);
+                    const float t = fa[i] * rcp_approx(piv[i]);
+                    ri[i] = rsqrtf(piv[i]);   // off the pivot chain
+                    int j = i + 1;
+                    if (j & 1) {
+                        fa[j] = fmaf(-t, lj[j], fa[j]);
+                        ++j;
+                    }
+#pragma unroll
+                    for (; j < 16; j += 2) ffma2(fa[j], fa[j + 1], -t, lj[j], lj[j + 1]);
+                    const float frn = fmaf(-t, rv, fr);
+                    fr = ime > i ? frn : fr;
+                }
+                const long long dt2 = clock64();
+                bool ok = true;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) ok = ok && piv[i] > 0.f && piv[i] < 3.0e38f;
+                if (inblk) {   // L row = a_mi / sqrt(p_i) (i < m), sqrt(p_m); z_m = r / sqrt(p_m)
+                    float zm = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float sc = fa[i] * ri[i], dg = piv[i] * ri[i];
+                        fa[i] = i < ime ? sc : (i == ime ? dg : fa[i]);
+                        zm = i == ime ? fr * ri[i] : zm;
+                    }
+                    const int mr = c0 + ime;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) Ljj[j * 16 + ime] = fa[j];   // column-major
+                    float *Lr = Ls + mr * (mr + 1) / 2 + c0;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j <= ime) Lr[j] = fa[j];
+                    zbuf[mr] = zm;
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        reinterpret_cast<float4 *>(rdiag + c0)[q4] =
+                            make_float4(ri[4 * q4], ri[4 * q4 + 1], ri[4 * q4 + 2], ri[4 * q4 + 3]);
+                    team_flag[team] = !ok;
+                }
+                if (w.prof && lane == lo) {
+                    const long long dt3 = clock64();
+                    atomicAdd(w.prof + 10, (unsigned long long)(dt1 - dt0));
+                    atomicAdd(w.prof + 11, (unsigned long long)(dt2 - dt1));
+                    atomicAdd(w.prof + 12, (unsigned long long)(dt3 - dt2));
+                }
+            }
+            tmem_wait_ld();
+            team_bar(team);
+            TCP(3);
+            if (team_flag[team]) {
+                failed = true;
+                break;
+            }
+            if (m >= c0 + 16 && m < DP) {   // panel rows: x L_JJ^T = a (right-looking), r -= x.z_J
+                float rd[16], zj[16];
+                lds16(rdiag + c0, rd);
+                lds16(zbuf + c0, zj);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float lc[16];   // column i of L_JJ
+#pragma unroll
+                    for (int q4 = (i + 1) / 4; q4 < 4; ++q4) {
+                        const float4 v = reinterpret_cast<const float4 *>(Ljj + 16 * i)[q4];
+                        lc[4 * q4] = v.x; lc[4 * q4 + 1] = v.y; lc[4 * q4 + 2] = v.z; lc[4 * q4 + 3] = v.w;
+                    }
+                    const float xi = a[i] * rd[i];
+                    a[i] = xi;
+                    int j = i + 1;
+                    if (j & 1 && j < 16) {
+                        a[j] = fmaf(-xi, lc[j], a[j]);
+                        ++j;
+                    }
+#pragma unroll
+                    for (; j < 16; j += 2) ffma2(a[j], a[j + 1], -xi, lc[j], lc[j + 1]);
+                }
+                float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    r0 = fmaf(a[i], zj[i], r0);
+                    r1 = fmaf(a[i + 1], zj[i + 1], r1);
+                }
+                r -= r0 + r1;
+                float *Lr = Ls + m * (m + 1) / 2 + c0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) Lr[j] = a[j];
+            }
+            TCP(4);
+            if (c0 + 16 < DP) {   // panel tiles, K-major: rows >= c0 + 16 carry L, others 0
+                const bool pr = m >= c0 + 16 && m < DP;
+                uint4 h0, l0, h1, l1;
+                split2(pr ? a[0] : 0.f, pr ? a[1] : 0.f, h0.x, l0.x);
+                split2(pr ? a[2] : 0.f, pr ? a[3] : 0.f, h0.y, l0.y);
+                split2(pr ? a[4] : 0.f, pr ? a[5] : 0.f, h0.z, l0.z);
+                split2(pr ? a[6] : 0.f, pr ? a[7] : 0.f, h0.w, l0.w);
+                split2(pr ? a[8] : 0.f, pr ? a[9] : 0.f, h1.x, l1.x);
+                split2(pr ? a[10] : 0.f, pr ? a[11] : 0.f, h1.y, l1.y);
+                split2(pr ? a[12] : 0.f, pr ? a[13] : 0.f, h1.z, l1.z);
+                split2(pr ? a[14] : 0.f, pr ? a[15] : 0.f, h1.w, l1.w);
+                if (m < DP) {
+                    const int off = (m >> 3) * 128 + (m & 7) * 16;
+                    *reinterpret_cast<uint4 *>(tb + C::OFF_PH + off) = h0;
+                    *reinterpret_cast<uint4 *>(tb + C::OFF_PH + C::KG + off) = h1;
+                    *reinterpret_cast<uint4 *>(tb + C::OFF_PL + off) = l0;
+                    *reinterpret_cast<uint4 *>(tb + C::OFF_PL + C::KG + off) = l1;
+                }
+                TCP(9);
+                tc_fence_before();
+                proxy_fence();
+                team_bar(team);
+                // trailing update C -= P_h P_h^T + P_h P_l^T + P_l P_h^T
+                if (m == 0) {
+                    tc_fence_after();
+                    const int N = DP - c0 - 16;
+                    const uint32_t id = idesc(N, false, true);
+                    const uint32_t boff = (uint32_t)((c0 + 16) >> 3) * 128;
+                    const uint64_t da = sdesc(tbs + C::OFF_PH, C::KG, 128);
+                    const uint64_t dl = sdesc(tbs + C::OFF_PL, C::KG, 128);
+                    umma(tmem + c0 + 16, da, sdesc(tbs + C::OFF_PH + boff, C::KG, 128), id, 1u);
+                    umma(tmem + c0 + 16, da, sdesc(tbs + C::OFF_PL + boff, C::KG, 128), id, 1u);
+                    umma(tmem + c0 + 16, dl, sdesc(tbs + C::OFF_PH + boff, C::KG, 128), id, 1u);
+                    umma_commit(cbar);
+                }
+                warp_mbar_wait(cbar, cph);
+                cph ^= 1u;
+                tc_fence_after();
+                TCP(7);
+            }
+        }
+        tc_fence_before();   // TMEM is free for the next task from here on
+        if (failed) {
+            if (m == 0) report_fail(p.fail, row);
+            team_bar(team);
+            continue;
+        }
+        TCP(5);
+
+        // ---------------- back substitution L^T x = z by warp 0 (L from smem),
+        // 4 unknowns per step: their z's are shuffled to every lane, each lane
+        // solves the 4 x 4 upper-triangular block redundantly, then updates its
+        // own rows (lane l holds rows l, l + 32, l + 64, l + 96)
+        team_bar(team);
+        if (wq == 0) {
+            float zr[4], xr[4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const int mq = lane + 32 * q4;
+                zr[q4] = mq < DP ? zbuf[mq] : 0.f;
+                xr[q4] = 0.f;
+            }
+#pragma unroll
+            for (int g = DP / 4 - 1; g >= 0; --g) {
+                const int i0 = 4 * g, qs = i0 >> 5, l0 = i0 & 31;
+                float zs[4], x4[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) zs[k] = __shfl_sync(FULL, zr[qs], l0 + k);
+                const float4 rd4 = *reinterpret_cast<const float4 *>(rdiag + i0);
+                const float rdv[4] = {rd4.x, rd4.y, rd4.z, rd4.w};
+#pragma unroll
+                for (int k = 3; k >= 0; --k) {
+                    float t = zs[k];
+#pragma unroll
+                    for (int k2 = k + 1; k2 < 4; ++k2)
+                        t = fmaf(-Ls[(i0 + k2) * (i0 + k2 + 1) / 2 + i0 + k], x4[k2], t);
+                    x4[k] = t * rdv[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) xr[qs] = lane == l0 + k ? x4[k] : xr[qs];
+#pragma unroll
+                for (int q5 = 0; q5 < 4; ++q5) {
+                    if (32 * q5 < i0) {   // rows below i0 of this slot (reads past i0 are discarded)
+                        const int mq = lane + 32 * q5;
+                        float zn = zr[q5];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            zn = fmaf(-Ls[(i0 + k) * (i0 + k + 1) / 2 + mq], x4[k], zn);
+                        zr[q5] = mq < i0 ? zn : zr[q5];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) xbuf[lane + 32 * q4] = xr[q4];
+        }
+        team_bar(team);
+        TCP(6);
+        const float xo = (m < DP ? xbuf[m] : 0.f) * out_scale;
+        if (m == 0) team_flag[team] = 0;
+        team_bar(team);
+        if (m < D && !isfinite(xo)) team_flag[team] = 1;
+        team_bar(team);
+        if (team_flag[team]) {
+            if (m == 0) report_fail(p.fail, row);
+        } else if (m < p.ld) {
+            put_out(p, row, m, m < D ? xo : 0.f);
+        }
+        TCP(8);
+    }
+#undef TCP
+    if (w.prof && m == 0)
+        for (int k = 0; k < 10; ++k) atomicAdd(w.prof + k, tcp_acc[k]);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh),
+                     "r"(C::TMEM_COLS));
+    }
+}
+
+template <int NBLK>
+int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t s) {
+    using C = TcCfg<NBLK>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_als_tc<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        attr = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_tc<NBLK>, C::TEAMS * 128, C::SMEM);
+    per_sm = std::max(1, std::min(per_sm, 512 / C::TMEM_COLS));
+    const int64_t want = ceil_div(q.n_tasks, C::TEAMS);
+    const int64_t grid = std::min<int64_t>(want, (int64_t)sms * per_sm);
+    if (grid > 0) k_als_tc<NBLK><<<(unsigned)grid, C::TEAMS * 128, C::SMEM, s>>>(p, q, w);
+    return check_launch("mcf_als_half_step(tensor core)");
+}
+
+}  // namespace
+
+static unsigned long long *g_tc_prof = nullptr;
+
+bool tc_path(int D, bool weighted) {
+    return !weighted && D >= 21 && D <= 128 && !getenv("MCF_NO_TC");
+}
+
+size_t tc_slot_floats(int D) {
+    const int dp = (D + 15) / 16 * 16;
+    return (size_t)dp * (dp + 16);
+}
+
+size_t tc_workspace_bytes(int D, int64_t slots) {
+    return 256 + align_up(sizeof(int32_t) * (size_t)(slots + 1), 256) +
+           sizeof(float) * (size_t)slots * tc_slot_floats(D);
+}
+
+int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
+                  cudaStream_t s) {
+    if (ws_bytes < tc_workspace_bytes(p.D, slots)) {
+        set_error("mcf_als_half_step: workspace too small for the tensor-core path");
+        return MCF_E_WORKSPACE;
+    }
+    Carve c(ws, ws_bytes);
+    TcWs w;
+    w.scal = c.take<unsigned>(4);
+    w.hot_count = c.take<int32_t>((size_t)slots + 1);
+    w.partials = c.take<float>((size_t)slots * tc_slot_floats(p.D));
+    w.n_slots = slots;
+    w.prof = nullptr;
+    if (getenv("MCF_TC_PROF")) {
+        static unsigned long long *buf = nullptr;
+        if (!buf) cudaMalloc(&buf, 16 * sizeof(unsigned long long));
+        cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+        w.prof = buf;
+        g_tc_prof = buf;
+    }
+    int rc;
+    if ((rc = cuda_status(cudaMemsetAsync(w.scal, 0, 4 * sizeof(unsigned), s), "memset"))) return rc;
+    k_tc_prep<<<148 * 4, 256, 0, s>>>(p, q, w);
+    if ((rc = check_launch("mcf_als_half_step(tensor-core prep)"))) return rc;
+    switch ((p.D + 15) / 16) {
+        case 2: return launch_tc<2>(p, q, w, s);
+        case 3: return launch_tc<3>(p, q, w, s);
+        case 4: return launch_tc<4>(p, q, w, s);
+        case 5: return launch_tc<5>(p, q, w, s);
+        case 6: return launch_tc<6>(p, q, w, s);
+        case 7: return launch_tc<7>(p, q, w, s);
+        case 8: return launch_tc<8>(p, q, w, s);
+        default:
+            set_error("mcf_als_half_step: tensor-core path needs 21 <= D <= 128");
+            return MCF_E_UNSUPPORTED;
+    }
+}
+
+}  // namespace mcf
+
+// phase cycle counters of the tensor-core path (MCF_TC_PROF=1): per team,
+// summed over CTAs; read and reset
+extern "C" int mcf_tc_prof_read(unsigned long long *out10) {
+    if (!mcf::g_tc_prof) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out10, mcf::g_tc_prof, 14 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(mcf::g_tc_prof, 0, 16 * sizeof(unsigned long long));
+    return 0;
+}

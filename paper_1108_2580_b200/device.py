@@ -14,6 +14,8 @@ HBM layout (per GPU):
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -22,6 +24,8 @@ from ._lib import check, ptr
 from .errors import ConfigError, DeviceError, SingularSystemError
 
 DEFAULT_CHUNK = 2048
+TC_CHUNK = 8192                      # tensor-core wide path: ratings per hot-row chunk (a
+                                     # chunk's partial Gram is DP^2 floats, ~6 B per rating)
 PAIR_CHUNK_CAP = 8192                # pair path: longest task (config 1: 11.5 -> 11.3 ms)
 TASKS_IN_FLIGHT = 2 * 148 * 8 * 16   # 2 x (SMs x pair-kernel warps x lane pairs)
 
@@ -32,6 +36,13 @@ def adaptive_chunk(nnz_rows: int, cap: int = PAIR_CHUNK_CAP) -> int:
     least ~2 tasks per lane pair in flight, multiples of 32, 64..cap."""
     return max(64, min(cap, nnz_rows // TASKS_IN_FLIGHT // 32 * 32))
 PLAN_INFO_LEN = 6   # MCF_PLAN_INFO_LEN
+
+
+def tc_path(D: int, weighted: bool = False) -> bool:
+    """mcf_als_half_step runs the tensor-core wide path (als_tc.cu) for this
+    dimension: 21 <= D <= 127 without per-observation weights (MCF_NO_TC=1
+    selects the CUDA-core kernels instead)."""
+    return 21 <= D <= 127 and not weighted and not os.environ.get("MCF_NO_TC")
 
 
 def cuda_device(device=None) -> torch.device:
@@ -168,6 +179,8 @@ class LayoutSolver:
             buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, chunk)
         elif self.D <= 20:          # pair path: adaptive task length
             buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, PAIR_CHUNK_CAP, adaptive=True)
+        elif tc_path(self.D, wts is not None):   # tensor-core wide path: long chunks
+            buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, TC_CHUNK)
         else:
             buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, DEFAULT_CHUNK)
         slots = max(info[1], info[3])   # hot-chunk slots (pair path / warp+CTA paths)

@@ -10,7 +10,7 @@ from paper_1108_2580_b200.device import AlsEngine, DeviceRatings  # noqa: E402
 
 U, I = 1_000_000, 4096
 for D in [int(x) for x in sys.argv[1:]] or [50, 100]:
-    for n in (8, 64, 256):
+    for n in [int(x) for x in os.environ.get("NS", "8,64,256").split(",")]:
         g = torch.Generator(device="cuda").manual_seed(0)
         users = torch.arange(U, device="cuda", dtype=torch.int32).repeat_interleave(n)
         items = torch.randint(0, I, (U * n,), device="cuda", dtype=torch.int32, generator=g)
