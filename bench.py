@@ -136,6 +136,10 @@ def fp32_peak():
 
 
 def kernel_name(D: int) -> str:
+    from paper_1108_2580_b200.device import tc_path
+    if tc_path(D):
+        return ("k_als_tc<NBLK> (tcgen05 kind::f16 Gram, fp16 h/l split, TMEM-resident blocked "
+                "Cholesky with negated-MMA trailing updates; + k_tc_prep)")
     if D <= 20:
         return "k_als_pair<5,4> (fused Gram + lam*n + Cholesky + solve; + k_als_heavy for hot rows)"
     if D <= 28:
@@ -146,11 +150,17 @@ def kernel_name(D: int) -> str:
 
 
 def roofline_for(D, bytes_launch, flops_launch, launch_s, traffic=None, kernel=None):
-    """roofline time = max(bytes / HBM, flops / FP32 peak) per
+    """roofline time = max(bytes / HBM, flops / compute peak) per
     launch; the bound is whichever is larger and `achieved` is reported in
-    that resource's unit (GB/s or TFLOP/s), the other view beside it."""
+    that resource's unit (GB/s or TFLOP/s), the other view beside it.  The
+    compute peak is the FP32 CUDA-core peak, or -- on the tensor-core path
+    (D >= 64) -- the measured dense 16-bit tensor peak / 3: every fp32
+    product is three fp16 MMAs (h h + h l + l h)."""
     hbm, hbm_kind = peaks()
     f32, f32_kind = fp32_peak()
+    from paper_1108_2580_b200.device import tc_path
+    if tc_path(D):
+        f32, f32_kind = tensor_peak_3x()
     t_hbm = bytes_launch / (hbm * 1e9)
     t_f32 = flops_launch / (f32 * 1e12)
     gbs = bytes_launch / launch_s / 1e9
@@ -159,7 +169,8 @@ def roofline_for(D, bytes_launch, flops_launch, launch_s, traffic=None, kernel=N
         r = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
              "peak_kind": hbm_kind, "achieved_tflops": tfs, "fp32_peak_tflops": f32}
     else:
-        r = {"bound": "fp32", "achieved": tfs, "peak": f32, "unit": "TFLOP/s", "frac": tfs / f32,
+        r = {"bound": "tensor" if tc_path(D) else "fp32", "achieved": tfs, "peak": f32,
+             "unit": "TFLOP/s", "frac": tfs / f32,
              "peak_kind": f32_kind, "achieved_gbs": gbs, "hbm_peak_gbs": hbm}
     r.update({"traffic": traffic, "kernel": kernel or kernel_name(D),
               "roofline_ms_per_launch": 1e3 * max(t_hbm, t_f32),
@@ -170,12 +181,24 @@ def roofline_for(D, bytes_launch, flops_launch, launch_s, traffic=None, kernel=N
 
 def launches_per_sweep(eng) -> int:
     """libmcf kernels per sweep: per half-step the row kernel, plus the hot-row
-    reduce kernel when the layout has hot rows (D <= 20 path)."""
+    reduce kernel when the layout has hot rows (D <= 20 path) or the scale
+    pre-pass (tensor-core path)."""
+    from paper_1108_2580_b200.device import tc_path
     n = 0
     for lay in (eng.r.by_item, eng.r.by_user):
         info = lay.plan()[1]
-        n += 1 + (1 if eng.D <= 20 and info[4] > 0 else 0)
+        n += 1 + (1 if (eng.D <= 20 and info[4] > 0) or tc_path(eng.D) else 0)
     return n
+
+
+def tensor_peak_3x():
+    """Dense 16-bit tensor peak (MEASURED_PEAKS.json bf16, the same pipe rate as
+    fp16) / 3 -- the effective fp32-product rate of the 3-term fp16 split."""
+    try:
+        with open(PEAKS) as fh:
+            return float(json.load(fh)["bf16_tflops"]) / 3.0, "measured bf16 / 3 (3 fp16 MMAs per product)"
+    except Exception:
+        return 2250.0 / 3.0, "nominal dense 16-bit / 3"
 
 
 def peaks():

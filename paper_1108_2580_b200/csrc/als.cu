@@ -2310,7 +2310,7 @@ extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t
     }
     const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
     size_t part = sizeof(float) * (size_t)slots * per;
-    if (D >= 21 && D <= 128) part = std::max(part, tc_workspace_bytes(D, slots));
+    if (D >= 64 && D <= 128) part = std::max(part, tc_workspace_bytes(D, slots));
     return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) + part;
 }
 

@@ -91,6 +91,7 @@ struct TcWs {
     float *partials;     // [slots][DP * (DP + 16)]
     int64_t n_slots;
     unsigned long long *prof;   // phase cycle counters (MCF_TC_PROF) or null
+    int team_limit;             // teams per CTA that take work (MCF_TC_TEAMS, experiments)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -252,6 +253,106 @@ __device__ __forceinline__ void lds16(const float *p, float (&v)[16]) {
     }
 }
 
+// Triangular solve with the packed lower factor L (smem, row r at r(r+1)/2)
+// by one warp, lane l holding rows l, l + 32, l + 64, l + 96 of the
+// right-hand side zr.  8 unknowns per step: their right-hand sides are
+// shuffled to every lane, each lane solves the 8 x 8 diagonal block
+// redundantly (rdiag = 1 / L_ii), then updates its own rows.
+//   UPPER: L^T x = z, x -> out[128];   else L z = r, z -> zr (in place).
+template <int DP, bool UPPER>
+__device__ __forceinline__ void warp_trsv(float (&zr)[4], const float *Ls, const float *rdiag,
+                                          int lane, float *out) {
+    float xr[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+    const int qs = UPPER ? 3 - qq : qq;
+    if (32 * qs >= DP) continue;
+#pragma unroll
+    for (int gq = 0; gq < 4; ++gq) {
+        const int l0 = 8 * (UPPER ? 3 - gq : gq), i0 = 32 * qs + l0;
+        if (i0 >= DP) continue;
+        // all loads of the group first (their latency overlaps the shuffles)
+        float lb[8][8], lu[4][8], rd[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2)
+                if (k2 < k) lb[k][k2] = Ls[(i0 + k) * (i0 + k + 1) / 2 + i0 + k2];   // L[i0+k][i0+k2]
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 v = reinterpret_cast<const float4 *>(rdiag + i0)[h];
+            rd[4 * h] = v.x; rd[4 * h + 1] = v.y; rd[4 * h + 2] = v.z; rd[4 * h + 3] = v.w;
+        }
+#pragma unroll
+        for (int q5 = 0; q5 < 4; ++q5) {
+            if (UPPER ? (q5 <= qs) : (q5 >= qs && 32 * q5 < DP)) {
+                const int mq = lane + 32 * q5, ma = min(mq, DP - 1);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    lu[q5][k] = UPPER ? Ls[(i0 + k) * (i0 + k + 1) / 2 + mq]   // L[i0+k][mq]
+                                      : Ls[ma * (ma + 1) / 2 + i0 + k];        // L[mq][i0+k]
+            }
+        }
+        float zs[8], x8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zs[k] = __shfl_sync(FULL, zr[qs], l0 + k);
+        // right-looking inside the block: each solved unknown updates the rest
+        // at once (dependency chain of 8 multiply + fma pairs)
+        if (UPPER) {
+#pragma unroll
+            for (int k = 7; k >= 0; --k) {
+                x8[k] = zs[k] * rd[k];
+#pragma unroll
+                for (int k2 = 0; k2 < k; ++k2) zs[k2] = fmaf(-lb[k][k2], x8[k], zs[k2]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                x8[k] = zs[k] * rd[k];
+#pragma unroll
+                for (int k2 = k + 1; k2 < 8; ++k2) zs[k2] = fmaf(-lb[k2][k], x8[k], zs[k2]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xr[qs] = lane == l0 + k ? x8[k] : xr[qs];
+#pragma unroll
+        for (int q5 = 0; q5 < 4; ++q5) {
+            if (UPPER ? (q5 <= qs) : (q5 >= qs && 32 * q5 < DP)) {
+                const int mq = lane + 32 * q5;
+                float za = 0.f, zb = 0.f;   // two short chains
+#pragma unroll
+                for (int k = 0; k < 8; k += 2) {
+                    za = fmaf(lu[q5][k], x8[k], za);
+                    zb = fmaf(lu[q5][k + 1], x8[k + 1], zb);
+                }
+                zr[q5] = (UPPER ? mq < i0 : mq > i0 + 7) ? zr[q5] - (za + zb) : zr[q5];
+            }
+        }
+    }
+    }
+    if (UPPER) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) out[lane + 32 * q4] = xr[q4];
+    } else {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) zr[q4] = xr[q4];
+    }
+}
+
+// the refinement's two solves, out of line (keeps the kernel's registers)
+template <int DP>
+__device__ __noinline__ float4 trsv_fwd(float4 z, const float *Ls, const float *rdiag, int lane) {
+    float zr[4] = {z.x, z.y, z.z, z.w};
+    warp_trsv<DP, false>(zr, Ls, rdiag, lane, nullptr);
+    return make_float4(zr[0], zr[1], zr[2], zr[3]);
+}
+template <int DP>
+__device__ __noinline__ void trsv_back(float4 z, const float *Ls, const float *rdiag, int lane,
+                                       float *out) {
+    float zr[4] = {z.x, z.y, z.z, z.w};
+    warp_trsv<DP, true>(zr, Ls, rdiag, lane, out);
+}
+
 template <int NBLK>
 __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs w) {
     using C = TcCfg<NBLK>;
@@ -320,6 +421,7 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
     } while (0)
 
     for (;;) {
+        if (team >= w.team_limit) break;
         if (m == 0) team_task[team] = atomicAdd(q.group_counter, 1);
         team_bar(team);
         const int64_t task = team_task[team];
@@ -679,55 +781,88 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
         }
         TCP(5);
 
-        // ---------------- back substitution L^T x = z by warp 0 (L from smem),
-        // 4 unknowns per step: their z's are shuffled to every lane, each lane
-        // solves the 4 x 4 upper-triangular block redundantly, then updates its
-        // own rows (lane l holds rows l, l + 32, l + 64, l + 96)
+        // ---------------- triangular solves by warp 0 (L from smem), 4 unknowns
+        // per step: their right-hand sides are shuffled to every lane, each lane
+        // solves the 4 x 4 diagonal block redundantly, then updates its own rows
+        // (lane l holds rows l, l + 32, l + 64, l + 96); result -> xbuf
+        auto back_sub = [&](float (&zr)[4]) { warp_trsv<DP, true>(zr, Ls, rdiag, lane, xbuf); };
         team_bar(team);
         if (wq == 0) {
-            float zr[4], xr[4];
+            float zr[4];
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
                 const int mq = lane + 32 * q4;
                 zr[q4] = mq < DP ? zbuf[mq] : 0.f;
-                xr[q4] = 0.f;
             }
-#pragma unroll
-            for (int g = DP / 4 - 1; g >= 0; --g) {
-                const int i0 = 4 * g, qs = i0 >> 5, l0 = i0 & 31;
-                float zs[4], x4[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) zs[k] = __shfl_sync(FULL, zr[qs], l0 + k);
-                const float4 rd4 = *reinterpret_cast<const float4 *>(rdiag + i0);
-                const float rdv[4] = {rd4.x, rd4.y, rd4.z, rd4.w};
-#pragma unroll
-                for (int k = 3; k >= 0; --k) {
-                    float t = zs[k];
-#pragma unroll
-                    for (int k2 = k + 1; k2 < 4; ++k2)
-                        t = fmaf(-Ls[(i0 + k2) * (i0 + k2 + 1) / 2 + i0 + k], x4[k2], t);
-                    x4[k] = t * rdv[k];
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) xr[qs] = lane == l0 + k ? x4[k] : xr[qs];
-#pragma unroll
-                for (int q5 = 0; q5 < 4; ++q5) {
-                    if (32 * q5 < i0) {   // rows below i0 of this slot (reads past i0 are discarded)
-                        const int mq = lane + 32 * q5;
-                        float zn = zr[q5];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            zn = fmaf(-Ls[(i0 + k) * (i0 + k + 1) / 2 + mq], x4[k], zn);
-                        zr[q5] = mq < i0 ? zn : zr[q5];
-                    }
-                }
-            }
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) xbuf[lane + 32 * q4] = xr[q4];
+            back_sub(zr);
         }
         team_bar(team);
         TCP(6);
-        const float xo = (m < DP ? xbuf[m] : 0.f) * out_scale;
+        float xo = (m < DP ? xbuf[m] : 0.f) * out_scale;
+        // ---------------- one step of iterative refinement for short rows
+        // (n < D): fp32 rounding of the Gram times cond(A) (up to ~1e4 at
+        // D = 100: the partner factors share a dominant mean direction, the
+        // rank-deficient Gram leaves D - n eigenvalues at lam n) exceeds the
+        // 1e-4 budget there; r = b - A x0 is formed from the ratings
+        // (e_k = y_k - x_k.x0, r = sum x_k e_k + tau T - reg x0) and
+        // x1 = x0 + A^{-1} r reuses the factorisation.
+        if (slot < 0 && nrow < D && nrow > 0) {
+            xbuf[m] = m < D ? xo : 0.f;   // x0, original units (own element)
+            team_bar(team);
+            // residuals e_k, a thread per rating (n < D <= 128)
+            if (m < n) {
+                const int id = __ldg(p.idx + k0 + m);
+                const float4 *xr4 = reinterpret_cast<const float4 *>(p.fixed + (size_t)id * p.ld);
+                float d0 = 0.f, d1 = 0.f;
+                for (int c = 0; c < p.ld / 4; c += 2) {
+                    const float4 u = __ldg(xr4 + c);
+                    const float4 xv = *reinterpret_cast<const float4 *>(xbuf + 4 * c);
+                    d0 = fmaf(u.x, xv.x, d0); d1 = fmaf(u.y, xv.y, d1);
+                    d0 = fmaf(u.z, xv.z, d0); d1 = fmaf(u.w, xv.w, d1);
+                    if (c + 1 < p.ld / 4) {
+                        const float4 u2 = __ldg(xr4 + c + 1);
+                        const float4 xv2 = *reinterpret_cast<const float4 *>(xbuf + 4 * c + 4);
+                        d0 = fmaf(u2.x, xv2.x, d0); d1 = fmaf(u2.y, xv2.y, d1);
+                        d0 = fmaf(u2.z, xv2.z, d0); d1 = fmaf(u2.w, xv2.w, d1);
+                    }
+                }
+                zbuf[m] = (__ldg(p.val + k0 + m) - p.y_shift) - (d0 + d1);
+                reinterpret_cast<int *>(tb + C::OFF_PH)[m] = id;
+            }
+            team_bar(team);
+            // r_f = sum_k x_k[f] e_k, a thread per feature
+            float rf = 0.f;
+            if (m < D) {
+                const int *ids = reinterpret_cast<const int *>(tb + C::OFF_PH);
+                float r1 = 0.f;
+                int k = 0;
+                for (; k + 1 < n; k += 2) {
+                    rf = fmaf(__ldg(p.fixed + (size_t)ids[k] * p.ld + m), zbuf[k], rf);
+                    r1 = fmaf(__ldg(p.fixed + (size_t)ids[k + 1] * p.ld + m), zbuf[k + 1], r1);
+                }
+                if (k < n) rf = fmaf(__ldg(p.fixed + (size_t)ids[k] * p.ld + m), zbuf[k], rf);
+                rf += r1;
+            }
+            team_bar(team);
+            if (m < D) {
+                rf = fmaf(-rg / s2, xo, rf);
+                if (p.tax_T && m != p.bias_dim) rf = fmaf(p.tau, p.tax_T[(size_t)row * p.ld + m], rf);
+            }
+            if (m < DP) zbuf[m] = m < D ? rf : 0.f;
+            team_bar(team);
+            if (wq == 0) {
+                float zr[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int mq = lane + 32 * q4;
+                    zr[q4] = mq < DP ? zbuf[mq] : 0.f;
+                }
+                const float4 w4 = trsv_fwd<DP>(make_float4(zr[0], zr[1], zr[2], zr[3]), Ls, rdiag, lane);
+                trsv_back<DP>(w4, Ls, rdiag, lane, xbuf);
+            }
+            team_bar(team);
+            if (m < D) xo = fmaf(s2, xbuf[m], xo);
+        }
         if (m == 0) team_flag[team] = 0;
         team_bar(team);
         if (m < D && !isfinite(xo)) team_flag[team] = 1;
@@ -775,7 +910,7 @@ int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t
 static unsigned long long *g_tc_prof = nullptr;
 
 bool tc_path(int D, bool weighted) {
-    return !weighted && D >= 21 && D <= 128 && !getenv("MCF_NO_TC");
+    return !weighted && D >= 64 && D <= 128 && !getenv("MCF_NO_TC");
 }
 
 size_t tc_slot_floats(int D) {
@@ -801,6 +936,7 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     w.partials = c.take<float>((size_t)slots * tc_slot_floats(p.D));
     w.n_slots = slots;
     w.prof = nullptr;
+    w.team_limit = getenv("MCF_TC_TEAMS") ? atoi(getenv("MCF_TC_TEAMS")) : 4;
     if (getenv("MCF_TC_PROF")) {
         static unsigned long long *buf = nullptr;
         if (!buf) cudaMalloc(&buf, 16 * sizeof(unsigned long long));

@@ -24,7 +24,7 @@ from ._lib import check, ptr
 from .errors import ConfigError, DeviceError, SingularSystemError
 
 DEFAULT_CHUNK = 2048
-TC_CHUNK = 8192                      # tensor-core wide path: ratings per hot-row chunk (a
+TC_CHUNK = int(os.environ.get("MCF_TC_CHUNK", 2048))   # tensor-core wide path: ratings per hot-row chunk (a
                                      # chunk's partial Gram is DP^2 floats, ~6 B per rating)
 PAIR_CHUNK_CAP = 8192                # pair path: longest task (config 1: 11.5 -> 11.3 ms)
 TASKS_IN_FLIGHT = 2 * 148 * 8 * 16   # 2 x (SMs x pair-kernel warps x lane pairs)
@@ -40,9 +40,9 @@ PLAN_INFO_LEN = 6   # MCF_PLAN_INFO_LEN
 
 def tc_path(D: int, weighted: bool = False) -> bool:
     """mcf_als_half_step runs the tensor-core wide path (als_tc.cu) for this
-    dimension: 21 <= D <= 127 without per-observation weights (MCF_NO_TC=1
+    dimension: 64 <= D <= 128 without per-observation weights (MCF_NO_TC=1
     selects the CUDA-core kernels instead)."""
-    return 21 <= D <= 127 and not weighted and not os.environ.get("MCF_NO_TC")
+    return 64 <= D <= 128 and not weighted and not os.environ.get("MCF_NO_TC")
 
 
 def cuda_device(device=None) -> torch.device:
