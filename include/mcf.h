@@ -207,9 +207,10 @@ int mcf_mfitr_fixed(const float *main_t, const float *add_t, const int32_t *art,
  * (mfitr.py:323-336; time / implicit terms off): users in order[0..n_order)
  * (the seeded shuffle), each user's ratings in the by-user layout's order
  * through _kernels.rate_update (_kernels.py:21-77), then the taxonomy edges
- * through _kernels.edge_pass_range (_kernels.py:129-148).  Device form:
+ * through _kernels.edge_pass_range (_kernels.py:129-148).  This entry:
  * Hogwild (a warp per user, item-side state updated without locks, atomic
- * adds in the edge pass), so not bit-reproducible.  Tables [rows][ld(D)];
+ * adds in the edge pass), not bit-reproducible; mcf_mfitr_sgd_epoch_locked
+ * below keeps the reference's per-item locking.  Tables [rows][ld(D)];
  * b_u/b_i/b_a float; art nullable (no artist terms); counter: one device
  * int32 of scratch.  workers: concurrent user warps (and edge warps) --
  * 1 reproduces the reference's single-thread order (strictly sequential),
@@ -220,6 +221,26 @@ int mcf_mfitr_sgd_epoch(const int64_t *uptr, const int32_t *uidx, const float *u
                         float *Q_a, float mu, int32_t D, float gamma, float lam_bias,
                         float lam_fac, const int64_t *ec, const int64_t *ep, const double *w,
                         int64_t E, float lam3, float lam4, int32_t workers, void *stream);
+/* The same epoch under the reference's LockTable contract (parallel.py:21-49,
+ * factor.py:430-444, mfitr.py:298-320): every rating's
+ * item-side update (q_i, b_i, q_a, b_a) holds one spin lock per item id --
+ * the (item, artist) pair acquired in ascending id order, released after
+ * the update -- and every edge update locks both endpoints, so no update is
+ * lost for any worker count.  locks: int32[num_items], zeroed by the caller
+ * (left zeroed). */
+int mcf_mfitr_sgd_epoch_locked(const int64_t *uptr, const int32_t *uidx, const float *uval,
+                               const int32_t *order, int32_t n_order, int32_t *counter, float *P,
+                               float *Q, float *b_u, float *b_i, const int32_t *art, float *b_a,
+                               float *Q_a, float mu, int32_t D, float gamma, float lam_bias,
+                               float lam_fac, const int64_t *ec, const int64_t *ep,
+                               const double *w, int64_t E, float lam3, float lam4,
+                               int32_t workers, int32_t *locks, void *stream);
+/* Stress test of that lock table: `workers` warps each take
+ * `iters` ascending-order lock pairs over n_items ids and add 1 to both
+ * locked accumulators acc[] non-atomically; afterwards sum(acc) must be
+ * exactly 2 * workers * iters. */
+int mcf_lock_stress(int32_t *locks, float *acc, int32_t n_items, int32_t workers, int32_t iters,
+                    void *stream);
 int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t *idx, const float *val,
                       const int32_t *aux, int32_t n_rows, const float *Pa, const float *Qa,
                       const float *Aa, const int32_t *art, float mu, int32_t D, float *out,

@@ -54,6 +54,10 @@ SIGNATURES = {
     "mcf_mfitr_sgd_epoch": (c_int, [vp, vp, vp, vp, c_i32, vp, vp, vp, vp, vp, vp, vp, vp, c_f32,
                                     c_i32, c_f32, c_f32, c_f32, vp, vp, vp, c_i64, c_f32, c_f32,
                                     c_i32, vp]),
+    "mcf_mfitr_sgd_epoch_locked": (c_int, [vp, vp, vp, vp, c_i32, vp, vp, vp, vp, vp, vp, vp, vp,
+                                           c_f32, c_i32, c_f32, c_f32, c_f32, vp, vp, vp, c_i64,
+                                           c_f32, c_f32, c_i32, vp, vp]),
+    "mcf_lock_stress": (c_int, [vp, vp, c_i32, c_i32, c_i32, vp]),
     "mcf_mfitr_targets": (c_int, [c_i32, vp, vp, vp, vp, c_i32, vp, vp, vp, vp, c_f32, c_i32, vp,
                                   vp]),
     "mcf_taxonomy_terms": (c_int, [vp, vp, vp, vp, vp, c_i32, c_i32, vp, c_i32, vp, vp, vp]),

@@ -144,22 +144,47 @@ extern "C" int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t
 // mfitr.sgd_epoch_mfitr (mfitr.py:323-336) = factor._sgd_pass (users in a
 // seeded shuffle, each user's ratings in record order through
 // _kernels.rate_update, _kernels.py:21-77) + _kernels.edge_pass_range
-// (_kernels.py:129-148).  Device form (Hogwild, as GPU SGD trainers do): a
-// warp per user -- warps take users in shuffle order -- walks that user's
-// ratings sequentially with the reference's update order (item side sees
-// the pre-update user factor, the user side the pre-update effective item
-// factor); item / artist state shared between concurrent users is updated
-// without locks.  The edge pass runs a warp per edge with atomic adds.  Not
-// bit-reproducible (neither is the reference's threaded path);
-// parity is the loss trajectory (tests/test_gpu_mfitr.py).
+// (_kernels.py:129-148).  Device form: a warp per user -- warps take users
+// in shuffle order -- walks that user's ratings sequentially with the
+// reference's update order (item side sees the pre-update user factor, the
+// user side the pre-update effective item factor).
+// Conflict handling, the reference's LockTable contract (parallel.py:21-49,
+// factor.py:430-444): with `locks` every rating's
+// item-side read-modify-write (q_i, b_i and the artist's q_a, b_a) runs
+// under one spin lock per item id, the (item, artist) pair acquired in
+// ascending id order and released right after the update; user state is
+// warp-private.  The edge pass then locks both endpoints of each edge
+// (mfitr.py:298-320) and applies the reference's two directed updates.
+// Locked item data is read through L2 (ld.global.cg), so a warp never sees
+// a stale L1 line of another SM's update.  Without locks: Hogwild.
 namespace mcf {
 namespace {
 
+__device__ __forceinline__ void lock_ids(int32_t *locks, int a, int b) {
+    // ascending id order, a pair or a single id (a == b or b < 0)
+    const int lo = b < 0 ? a : min(a, b), hi = b < 0 ? a : max(a, b);
+    while (atomicCAS(locks + lo, 0, 1) != 0) __nanosleep(32);
+    if (hi != lo)
+        while (atomicCAS(locks + hi, 0, 1) != 0) __nanosleep(32);
+    __threadfence();
+}
+__device__ __forceinline__ void unlock_ids(int32_t *locks, int a, int b) {
+    const int lo = b < 0 ? a : min(a, b), hi = b < 0 ? a : max(a, b);
+    __threadfence();
+    if (hi != lo) atomicExch(locks + hi, 0);
+    atomicExch(locks + lo, 0);
+}
+template <bool LOCK>
+__device__ __forceinline__ float ld_item(const float *p) {
+    return LOCK ? __ldcg(p) : *p;
+}
+
+template <bool LOCK>
 __global__ void k_sgd_users(const int64_t *uptr, const int32_t *uidx, const float *uval,
                             const int32_t *order, int32_t n_order, int32_t *counter, float *P,
                             float *Q, float *bu, float *bi, const int32_t *art, float *ba,
                             float *Qa, float mu, int D, int ld, float gamma, float lam_b,
-                            float lam_f) {
+                            float lam_f, int32_t *locks) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int t = 0;
@@ -172,75 +197,121 @@ __global__ void k_sgd_users(const int64_t *uptr, const int32_t *uidx, const floa
             const int i = uidx[k];
             const float r = uval[k];
             const int a = art ? art[i] : -1;
+            const int la = (a >= 0 && a != i) ? a : -1;
+            if (LOCK) {
+                if (lane == 0) lock_ids(locks, i, la);
+                __syncwarp();
+            }
             float *qi = Q + (size_t)i * ld;
             float *qa = a >= 0 ? Qa + (size_t)a * ld : nullptr;
             float dot = 0.f;
-            float qe[4], pe[4];
+            float qe[4], pe[4], qiv[4], qav[4];
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 const int d = lane + 32 * s;
-                qe[s] = pe[s] = 0.f;
+                qe[s] = pe[s] = qiv[s] = qav[s] = 0.f;
                 if (d < D) {
-                    qe[s] = qi[d] + (qa ? qa[d] : 0.f);
+                    qiv[s] = ld_item<LOCK>(qi + d);
+                    qav[s] = qa ? ld_item<LOCK>(qa + d) : 0.f;
+                    qe[s] = qiv[s] + qav[s];
                     pe[s] = pu[d];
                     dot = fmaf(qe[s], pe[s], dot);
                 }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(FULL, dot, o);
-            float pred = mu + bu[u] + bi[i] + (a >= 0 ? ba[a] : 0.f) + dot;
+            const float bi0 = ld_item<LOCK>(bi + i), ba0 = a >= 0 ? ld_item<LOCK>(ba + a) : 0.f;
+            float pred = mu + bu[u] + bi0 + ba0 + dot;
             const float e = r - pred;
             __syncwarp();
             if (lane == 0) {
                 bu[u] += gamma * (e - lam_b * bu[u]);
-                bi[i] += gamma * (e - lam_b * bi[i]);
-                if (a >= 0) ba[a] += gamma * (e - lam_b * ba[a]);
+                bi[i] = bi0 + gamma * (e - lam_b * bi0);
+                if (a >= 0) ba[a] = ba0 + gamma * (e - lam_b * ba0);
             }
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 const int d = lane + 32 * s;
                 if (d < D) {
-                    qi[d] += gamma * (e * pe[s] - lam_f * qi[d]);
-                    if (qa) qa[d] += gamma * (e * pe[s] - lam_f * qa[d]);
+                    qi[d] = qiv[s] + gamma * (e * pe[s] - lam_f * qiv[s]);
+                    if (qa) qa[d] = qav[s] + gamma * (e * pe[s] - lam_f * qav[s]);
                     pu[d] += gamma * (e * qe[s] - lam_f * pe[s]);
                 }
             }
             __syncwarp();
+            if (LOCK && lane == 0) unlock_ids(locks, i, la);
         }
     }
 }
 
+template <bool LOCK>
 __global__ void k_sgd_edges(const int64_t *ec, const int64_t *ep, const double *w, int64_t E,
-                            float *Q, int D, int ld, float gamma, float lam3, float lam4) {
+                            float *Q, int D, int ld, float gamma, float lam3, float lam4,
+                            int32_t *locks) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < E; k += warps) {
         const int64_t c = ec[k], p = ep[k];
         const float wk = (float)w[k];
+        if (LOCK) {   // both endpoints, ascending (mfitr.py:298-320)
+            if (lane == 0) lock_ids(locks, (int)c, (int)p);
+            __syncwarp();
+        }
         for (int d = lane; d < D; d += 32) {
-            float qc = Q[(size_t)c * ld + d], qp = Q[(size_t)p * ld + d];
+            float *pc = Q + (size_t)c * ld + d, *pp = Q + (size_t)p * ld + d;
+            float qc = ld_item<LOCK>(pc), qp = ld_item<LOCK>(pp);
             const float d1 = -2.f * gamma * lam3 * wk * (qc - qp);
             qc += d1;
             qp -= d1;
             const float d2 = -2.f * gamma * lam4 * wk * (qp - qc);
-            const float dc = d1 - d2, dp = d2 - d1;
-            atomicAdd(Q + (size_t)c * ld + d, dc);
-            atomicAdd(Q + (size_t)p * ld + d, dp);
+            if (LOCK) {   // the reference's exact sequence under the locks
+                *pc = qc - d2;
+                *pp = qp + d2;
+            } else {      // Hogwild: concurrent edges of one node add up
+                const float dc = d1 - d2, dp = d2 - d1;
+                atomicAdd(pc, dc);
+                atomicAdd(pp, dp);
+            }
         }
+        if (LOCK) {
+            __syncwarp();
+            if (lane == 0) unlock_ids(locks, (int)c, (int)p);
+        }
+    }
+}
+
+// the LockTable contract itself: `workers` warps each
+// take `iters` ascending-order lock pairs over n_items ids and increment the
+// locked accumulators non-atomically; no update may be lost, no deadlock
+__global__ void k_lock_stress(int32_t *locks, float *acc, int32_t n_items, int32_t workers,
+                              int32_t iters) {
+    const int lane = threadIdx.x & 31;
+    const int wid = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (wid >= workers) return;
+    for (int it = 0; it < iters; ++it) {
+        const int a = (wid + it) % n_items, b = (wid * 7 + it * 3 + 1) % n_items;
+        if (lane == 0) {
+            lock_ids(locks, b, a == b ? -1 : a);
+            const float va = __ldcg(acc + a);
+            __stcg(acc + a, va + 1.f);
+            const float vb = __ldcg(acc + b);
+            __stcg(acc + b, vb + 1.f);
+            unlock_ids(locks, b, a == b ? -1 : a);
+        }
+        __syncwarp();
     }
 }
 
 }  // namespace
 }  // namespace mcf
 
-extern "C" int mcf_mfitr_sgd_epoch(const int64_t *uptr, const int32_t *uidx, const float *uval,
-                                   const int32_t *order, int32_t n_order, int32_t *counter,
-                                   float *P, float *Q, float *b_u, float *b_i,
-                                   const int32_t *art, float *b_a, float *Q_a, float mu,
-                                   int32_t D, float gamma, float lam_bias, float lam_fac,
-                                   const int64_t *ec, const int64_t *ep, const double *w,
-                                   int64_t E, float lam3, float lam4, int32_t workers,
-                                   void *stream) {
+static int sgd_epoch_impl(const int64_t *uptr, const int32_t *uidx, const float *uval,
+                          const int32_t *order, int32_t n_order, int32_t *counter, float *P,
+                          float *Q, float *b_u, float *b_i, const int32_t *art, float *b_a,
+                          float *Q_a, float mu, int32_t D, float gamma, float lam_bias,
+                          float lam_fac, const int64_t *ec, const int64_t *ep, const double *w,
+                          int64_t E, float lam3, float lam4, int32_t workers, int32_t *locks,
+                          void *stream) {
     if (!uptr || !order || !counter || !P || !Q || !b_u || !b_i || D < 1 || D > 128 ||
         n_order < 0 || (art && (!b_a || !Q_a)) || E < 0 || (E > 0 && (!ec || !ep || !w))) {
         set_error("mcf_mfitr_sgd_epoch: invalid arguments");
@@ -253,12 +324,66 @@ extern "C" int mcf_mfitr_sgd_epoch(const int64_t *uptr, const int32_t *uidx, con
     // workers = concurrent user warps; 1 = the reference's single-thread order
     // (users and ratings strictly sequential), <= 0 = the whole GPU
     const int warps = workers > 0 ? std::min(workers, 148 * 64) : 148 * 64;
-    if (n_order > 0)
-        k_sgd_users<<<(warps + 7) / 8, std::min(warps, 8) * 32, 0, s>>>(uptr, uidx, uval, order, n_order, counter, P, Q, b_u,
-                                            b_i, art, b_a, Q_a, mu, D, ld, gamma, lam_bias,
-                                            lam_fac);
-    if (E > 0 && (lam3 != 0.f || lam4 != 0.f))
-        k_sgd_edges<<<(warps + 7) / 8, std::min(warps, 8) * 32, 0, s>>>(ec, ep, w, E, Q, D, ld,
-                                                                         gamma, lam3, lam4);
+    const unsigned grid = (warps + 7) / 8, block = std::min(warps, 8) * 32;
+    if (n_order > 0) {
+        if (locks)
+            k_sgd_users<true><<<grid, block, 0, s>>>(uptr, uidx, uval, order, n_order, counter, P,
+                                                     Q, b_u, b_i, art, b_a, Q_a, mu, D, ld, gamma,
+                                                     lam_bias, lam_fac, locks);
+        else
+            k_sgd_users<false><<<grid, block, 0, s>>>(uptr, uidx, uval, order, n_order, counter,
+                                                      P, Q, b_u, b_i, art, b_a, Q_a, mu, D, ld,
+                                                      gamma, lam_bias, lam_fac, nullptr);
+    }
+    if (E > 0 && (lam3 != 0.f || lam4 != 0.f)) {
+        if (locks)
+            k_sgd_edges<true><<<grid, block, 0, s>>>(ec, ep, w, E, Q, D, ld, gamma, lam3, lam4,
+                                                     locks);
+        else
+            k_sgd_edges<false><<<grid, block, 0, s>>>(ec, ep, w, E, Q, D, ld, gamma, lam3, lam4,
+                                                      nullptr);
+    }
     return check_launch("mcf_mfitr_sgd_epoch");
+}
+
+extern "C" int mcf_mfitr_sgd_epoch(const int64_t *uptr, const int32_t *uidx, const float *uval,
+                                   const int32_t *order, int32_t n_order, int32_t *counter,
+                                   float *P, float *Q, float *b_u, float *b_i,
+                                   const int32_t *art, float *b_a, float *Q_a, float mu,
+                                   int32_t D, float gamma, float lam_bias, float lam_fac,
+                                   const int64_t *ec, const int64_t *ep, const double *w,
+                                   int64_t E, float lam3, float lam4, int32_t workers,
+                                   void *stream) {
+    return sgd_epoch_impl(uptr, uidx, uval, order, n_order, counter, P, Q, b_u, b_i, art, b_a,
+                          Q_a, mu, D, gamma, lam_bias, lam_fac, ec, ep, w, E, lam3, lam4, workers,
+                          nullptr, stream);
+}
+
+extern "C" int mcf_mfitr_sgd_epoch_locked(const int64_t *uptr, const int32_t *uidx,
+                                          const float *uval, const int32_t *order,
+                                          int32_t n_order, int32_t *counter, float *P, float *Q,
+                                          float *b_u, float *b_i, const int32_t *art, float *b_a,
+                                          float *Q_a, float mu, int32_t D, float gamma,
+                                          float lam_bias, float lam_fac, const int64_t *ec,
+                                          const int64_t *ep, const double *w, int64_t E,
+                                          float lam3, float lam4, int32_t workers, int32_t *locks,
+                                          void *stream) {
+    if (!locks) {
+        set_error("mcf_mfitr_sgd_epoch_locked: locks (int32[num_items], zeroed) is required");
+        return MCF_E_ARG;
+    }
+    return sgd_epoch_impl(uptr, uidx, uval, order, n_order, counter, P, Q, b_u, b_i, art, b_a,
+                          Q_a, mu, D, gamma, lam_bias, lam_fac, ec, ep, w, E, lam3, lam4, workers,
+                          locks, stream);
+}
+
+extern "C" int mcf_lock_stress(int32_t *locks, float *acc, int32_t n_items, int32_t workers,
+                               int32_t iters, void *stream) {
+    if (!locks || !acc || n_items < 1 || workers < 1 || iters < 0) {
+        set_error("mcf_lock_stress: invalid arguments");
+        return MCF_E_ARG;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    k_lock_stress<<<(unsigned)((workers + 7) / 8), 256, 0, s>>>(locks, acc, n_items, workers, iters);
+    return check_launch("mcf_lock_stress");
 }

@@ -467,7 +467,7 @@ def train_mfitr_sgd(kind: str, train_data: Dataset, validation: Dataset | None,
                     graph: TaxonomyGraph, hyper: MfitrHyper, seed: int = 0,
                     ew: TaxonomyEdgeWeights | None = None, num_users: int | None = None,
                     num_items: int | None = None, *, device=None, objective: bool = True,
-                    workers: int = 0) -> tuple[MfitrModel, list[EpochStats]]:
+                    workers: int = 0, conflicts: str = "locks") -> tuple[MfitrModel, list[EpochStats]]:
     """The reference's own MFITR trainer on device:
     mfitr.train_mfitr (mfitr.py:347-371) with sgd_epoch_mfitr per epoch --
     the same seeded init (init_mfitr), the same per-epoch user shuffle
@@ -475,9 +475,14 @@ def train_mfitr_sgd(kind: str, train_data: Dataset, validation: Dataset | None,
     user's ratings then the edge pass (mcf_mfitr_sgd_epoch, Hogwild across
     users), gamma *= decay after every epoch; one EpochStats row per epoch
     with loss_mfitr and the clipped validation RMSE.  workers: concurrent
-    user warps -- 0 (default) the whole GPU (Hogwild; on a small problem the
-    users then see each other's updates much later than in the reference's
-    sequential pass), 1 the reference's single-thread order exactly."""
+    user warps -- 0 (default) the whole GPU, 1 the reference's single-thread
+    order exactly.  conflicts: "locks" (default) keeps the reference's
+    LockTable contract across concurrent users (one lock per item id, the
+    (item, artist) pair in ascending order per rating, both endpoints per
+    edge -- parallel.py:21-49, mcf_mfitr_sgd_epoch_locked); "hogwild" updates
+    shared item state without locks."""
+    if conflicts not in ("locks", "hogwild"):
+        raise ConfigError(f"conflicts must be 'locks' or 'hogwild', got {conflicts!r}")
     hyper = dataclasses.replace(hyper)
     model = init_mfitr(kind, train_data, graph, hyper, seed, num_users=num_users,
                        num_items=num_items)
@@ -501,6 +506,8 @@ def train_mfitr_sgd(kind: str, train_data: Dataset, validation: Dataset | None,
     lay = r.by_user
     deg = lay.degrees().cpu().numpy()
     counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    locks = (torch.zeros(base.num_items, dtype=torch.int32, device=dev)
+             if conflicts == "locks" else None)
     shuffle = np.random.default_rng([seed, 2])
     eng = AlsEngine(r, D)            # prediction / loss helpers
     vu = vi = vs = None
@@ -522,13 +529,16 @@ def train_mfitr_sgd(kind: str, train_data: Dataset, validation: Dataset | None,
         perm = shuffle.permutation(base.num_users)
         active = perm[deg[perm] > 0].astype(np.int32)
         order = torch.as_tensor(active, device=dev)
-        check(L.mcf_mfitr_sgd_epoch(ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(order),
-                                    int(order.numel()), ptr(counter), ptr(P), ptr(Q), ptr(bu),
-                                    ptr(bi), ptr(art), ptr(ba), ptr(Qa), float(base.mu), D,
-                                    float(hyper.gamma), float(hyper.lam1), float(hyper.lam2),
-                                    ptr(ec), ptr(ep), ptr(w), int(ec.numel()), float(hyper.lam3),
-                                    float(hyper.lam4), int(workers), stream_ptr(dev)),
-              "mcf_mfitr_sgd_epoch")
+        args = (ptr(lay.ptr), ptr(lay.idx), ptr(lay.val), ptr(order), int(order.numel()),
+                ptr(counter), ptr(P), ptr(Q), ptr(bu), ptr(bi), ptr(art), ptr(ba), ptr(Qa),
+                float(base.mu), D, float(hyper.gamma), float(hyper.lam1), float(hyper.lam2),
+                ptr(ec), ptr(ep), ptr(w), int(ec.numel()), float(hyper.lam3), float(hyper.lam4),
+                int(workers))
+        if locks is not None:
+            check(L.mcf_mfitr_sgd_epoch_locked(*args, ptr(locks), stream_ptr(dev)),
+                  "mcf_mfitr_sgd_epoch_locked")
+        else:
+            check(L.mcf_mfitr_sgd_epoch(*args, stream_ptr(dev)), "mcf_mfitr_sgd_epoch")
         base.epochs_done += 1
         hyper.gamma *= hyper.decay
         obj = float("nan")
@@ -569,11 +579,13 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
                 num_users: int | None = None, num_items: int | None = None, *, init=None,
                 device=None, as_torch: bool = False, objective: bool = True,
                 blocks: str = "full", method: str = "als", sgd_workers: int = 0,
-                devices=None) -> tuple[MfitrModel, list[EpochStats]]:
+                sgd_conflicts: str = "locks", devices=None) -> tuple[MfitrModel, list[EpochStats]]:
     """hyper.iters ALS-MFITR sweeps; one EpochStats row per sweep with
     loss_mfitr and the clipped validation RMSE (mfitr.py:347-371 signature).
 
-    method="sgd": the reference's own SGD trainer instead (train_mfitr_sgd).
+    method="sgd": the reference's own SGD trainer instead (train_mfitr_sgd;
+    sgd_workers concurrent user warps, sgd_conflicts "locks" = the
+    reference's per-item LockTable contract, or "hogwild").
     blocks="full" (default): every parameter of the reference's MFITR model
     (mfitr.py:92-149) -- [q_i|b_i] per taxonomy layer, [q_a|b_a] per artist,
     [p_u|b_u] (MfitrFullSolver); blocks="q": factors only, biases and q_a
@@ -587,7 +599,7 @@ def train_mfitr(kind: str, train_data: Dataset, validation: Dataset | None,
     if method == "sgd":   # the reference's own trainer (mfitr.py:347-371), on device
         return train_mfitr_sgd(kind, train_data, validation, graph, hyper, seed, ew,
                                num_users, num_items, device=device, objective=objective,
-                               workers=sgd_workers)
+                               workers=sgd_workers, conflicts=sgd_conflicts)
     if method != "als":
         raise ConfigError(f"method must be 'als' or 'sgd', got {method!r}")
     if blocks not in ("full", "q"):
