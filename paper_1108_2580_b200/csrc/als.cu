@@ -2300,8 +2300,9 @@ extern "C" int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t
     return check_launch("mcf_als_plan");
 }
 
-extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D) {
-    if (D < 1 || n_list < 0 || slots < 0) return 0;
+extern "C" size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, int32_t D,
+                                                int64_t n_fixed) {
+    if (D < 1 || n_list < 0 || slots < 0 || n_fixed < 0) return 0;
     size_t per = use_pair(D) ? pair_gram(D) : pstride_of(D);
     if (D >= 2 && D - 1 <= 20) {   // a bias-last system may run as D - 1 + Schur (+ u, d)
         const int nb = (D - 1 + 3) / 4;
@@ -2310,8 +2311,14 @@ extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t
     }
     const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
     size_t part = sizeof(float) * (size_t)slots * per;
-    if (D >= 64 && D <= 128) part = std::max(part, tc_workspace_bytes(D, slots));
+    if (D >= 64 && D <= 128 && n_fixed > 0) part = std::max(part, tc_workspace_bytes(D, slots, n_fixed));
     return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) + part;
+}
+
+// without the fixed-table size the tensor-core path has no room for its
+// split tables: the CUDA-core kernels run (same results to the tolerance)
+extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D) {
+    return mcf_als_workspace_bytes_fixed(n_list, slots, D, 0);
 }
 
 static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *val,
@@ -2392,6 +2399,10 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         return MCF_E_WORKSPACE;
     }
     p.partials = reinterpret_cast<float *>(static_cast<char *>(ws) + fixed_part);
+    // the tensor-core path (64 <= D <= 128, no weights) when the workspace holds
+    // its split tables (mcf_als_workspace_bytes_fixed), else the CUDA-core kernels
+    const bool use_tc = tc_path(p.D, wts != nullptr) && !p.schur &&
+                        ws_bytes >= fixed_part + tc_workspace_bytes(p.D, plan_info[3], n_fixed);
     {   // the partial-Gram slots of the hot-row chunks must fit too
         size_t per;
         if (p.schur) {
@@ -2401,10 +2412,8 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
             per = use_pair(p.D) ? pair_gram(p.D) : pstride_of(p.D);
         }
         const size_t slots = (size_t)std::max<int64_t>(plan_info[3], plan_info[1]);
-        size_t need = sizeof(float) * slots * per;
-        if (tc_path(p.D, wts != nullptr) && !p.schur)
-            need = tc_workspace_bytes(p.D, plan_info[3]);
-        if (ws_bytes < fixed_part + need) {
+        const size_t need = sizeof(float) * slots * per;
+        if (!use_tc && ws_bytes < fixed_part + need) {
             set_error("mcf_als_half_step: workspace too small for the partial slots");
             return MCF_E_WORKSPACE;
         }
@@ -2431,7 +2440,7 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         }
         return wts ? dispatch_pair<true>(p, q, s) : dispatch_pair<false>(p, q, s);
     }
-    if (tc_path(p.D, wts != nullptr) && !p.schur) {   // tensor-core wide path
+    if (use_tc) {   // tensor-core wide path
         PairPlan q{};
         q.task_row = L.task_row;
         q.task_k0 = L.task_k0;

@@ -41,10 +41,13 @@
 // every scaled diagonal entry stays below 2^30: all panel values then fit
 // fp16 (|L_ij| <= sqrt(A_ii) < 2^15) and the result is exact rescaling.
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "als_params.cuh"
 #include "../../include/mcf.h"
@@ -62,26 +65,32 @@ __host__ __device__ constexpr int tc_pow2_cols(int c) {
 template <int NBLK>
 struct TcCfg {
     static constexpr int DP = 16 * NBLK;           // padded dimension (features = rows of L)
-    static constexpr int NCH = DP / 8;             // 16-byte fp16 chunks per operand row
-    static constexpr int KG = NCH * 128;           // bytes per 8-rating k-group (MN-major)
-    static constexpr int TILE = 2 * KG;            // 16 ratings
+    static constexpr int NA = (DP + 63) / 64;      // 64-feature SWIZZLE_128B atoms per operand row
+    static constexpr int TW = 64 * NA;             // split-table row width (fp16)
+    static constexpr int HT = 2 * NA * 1024;       // H (or L) tile: 2 k-groups x NA atoms x 1 KB
     static constexpr int YT = 512;                 // rating tile: 16 ratings x 16 cols (y_h, y_l)
-    static constexpr int STAGE = 2 * TILE + YT;    // H | L | Y
-    static constexpr int PT = 2 * KG;              // panel tile: DP rows x 16 k, K-major
+    static constexpr int STAGE = 2 * HT + 1024;    // H | L | Y (1 KB-aligned)
+    static constexpr int NST = 5;                  // Gram stage ring (3 gathers + 2 MMA stages in flight)
+    static constexpr int MMA_DEPTH = 2;
+    static constexpr int KGP = (DP / 8) * 128;     // panel tile k-chunk stride (K-major, no swizzle)
+    static constexpr int PT = 2 * KGP;             // panel tile: DP rows x 16 k
     static constexpr int COLS = DP + 16;           // TMEM columns per team: Gram | rhs
-    static constexpr int OFF_PH = TC_NST * STAGE;
+    static constexpr int LS_BYTES = DP * (DP + 1) / 2 * 4;
+    // the stage ring (Gram) and the packed L (Cholesky .. back substitution)
+    // are never live together: one region
+    static constexpr int RING = NST * STAGE > LS_BYTES ? NST * STAGE : LS_BYTES;
+    static constexpr int OFF_L = 0;
+    static constexpr int OFF_PH = (RING + 1023) / 1024 * 1024;
     static constexpr int OFF_PL = OFF_PH + PT;
     static constexpr int OFF_LJJ = OFF_PL + PT;    // L_JJ, column-major 16 x 16
     static constexpr int OFF_RD = OFF_LJJ + 1024;  // 1 / L_ii [DP]
     static constexpr int OFF_Z = OFF_RD + DP * 4;  // z = L^{-1} b [DP]
     static constexpr int OFF_X = OFF_Z + DP * 4;   // x [128]
-    static constexpr int OFF_L = OFF_X + 512;      // L, packed rows (row r at r(r+1)/2)
-    static constexpr int TEAM_BYTES = (OFF_L + DP * (DP + 1) / 2 * 4 + 127) / 128 * 128;
-    static constexpr int SLACK = 2048;             // operand over-read past the last team
+    static constexpr int TEAM_BYTES = (OFF_X + 512 + 1023) / 1024 * 1024;
+    static constexpr int SLACK = 2048 + 1024;      // operand over-read past the last team + base alignment
     static constexpr int TEAMS = (4 * TEAM_BYTES + SLACK <= 227 * 1024 && 4 * COLS <= 512) ? 4 : 3;
     static constexpr int SMEM = TEAMS * TEAM_BYTES + SLACK;
     static constexpr int TMEM_COLS = tc_pow2_cols(TEAMS * COLS);
-    static constexpr int ITEMS = (16 * NCH + 127) / 128;   // gather items per thread per stage
     static_assert(SMEM <= 227 * 1024 && TEAMS * COLS <= 512, "tensor-core path resources");
 };
 
@@ -92,6 +101,7 @@ struct TcWs {
     int64_t n_slots;
     unsigned long long *prof;   // phase cycle counters (MCF_TC_PROF) or null
     int team_limit;             // teams per CTA that take work (MCF_TC_TEAMS, experiments)
+    __half *th, *tl;            // split fixed table: s*x = h + l, [n_fixed][TW] fp16
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -124,17 +134,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 // all threads of a warp wait for an mbarrier phase: lane 0 polls (no
 // suspend), the warp follows
 __device__ __forceinline__ void warp_mbar_wait(uint32_t bar, uint32_t parity) {
-    if ((threadIdx.x & 31) == 0) {
-        uint32_t done = 0;
-        do {
-            asm volatile(
-                "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; "
-                "selp.u32 %0, 1, 0, p; }"
-                : "=r"(done)
-                : "r"(bar), "r"(parity)
-                : "memory");
-        } while (!done);
-    }
+    if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);   // try_wait: suspends in hardware
     __syncwarp();
 }
 __device__ __forceinline__ void tc_fence_before() {
@@ -259,6 +259,47 @@ __device__ __forceinline__ void lds16(const float *p, float (&v)[16]) {
 // shuffled to every lane, each lane solves the 8 x 8 diagonal block
 // redundantly (rdiag = 1 / L_ii), then updates its own rows.
 //   UPPER: L^T x = z, x -> out[128];   else L z = r, z -> zr (in place).
+// the per-call scales (powers of two, see the header comment)
+__device__ __forceinline__ void tc_scales(const AlsParams &p, const TcWs &w, float &s, float &sy) {
+    const float xmax = __uint_as_float(w.scal[0]), ymax = __uint_as_float(w.scal[1]);
+    const float nmax = (float)w.scal[2], smax = __uint_as_float(w.scal[3]);
+    const float regmax = p.lam_c + p.lam_n * nmax + smax + 1.f +
+                         (p.bias_dim >= 0 ? p.bias_lam_c + p.bias_lam_n * nmax : 0.f);
+    s = tc_scale(nmax * xmax * xmax + regmax);
+    sy = ymax > 0.f ? exp2f(floorf(log2f(16384.f / ymax))) : 1.f;
+}
+
+// fixed table -> fp16 split tables (s*x = h + l), zero beyond D: the TMA
+// gathers of the Gram read these rows
+__global__ void k_tc_split(AlsParams p, TcWs w, int TW) {
+    float s, sy;
+    tc_scales(p, w, s, sy);
+    const int64_t n = p.n_fixed * (int64_t)(TW / 2);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / (TW / 2);
+        const int f = 2 * (int)(e - r * (TW / 2));
+        const float a = f < p.D ? __ldg(p.fixed + r * p.ld + f) * s : 0.f;
+        const float b = f + 1 < p.D ? __ldg(p.fixed + r * p.ld + f + 1) * s : 0.f;
+        uint32_t h, l;
+        split2(a, b, h, l);
+        reinterpret_cast<uint32_t *>(w.th)[e] = h;
+        reinterpret_cast<uint32_t *>(w.tl)[e] = l;
+    }
+}
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int col, int r0,
+                                            int r1, int r2, int r3, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return sdesc(addr, lbo, sbo) | (2ull << 61);
+}
+
 template <int DP, bool UPPER>
 __device__ __forceinline__ void warp_trsv(float (&zr)[4], const float *Ls, const float *rdiag,
                                           int lane, float *out) {
@@ -354,31 +395,38 @@ __device__ __noinline__ void trsv_back(float4 z, const float *Ls, const float *r
 }
 
 template <int NBLK>
-__global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs w) {
+__global__ void __launch_bounds__(512, 1)
+    k_als_tc(AlsParams p, PairPlan q, TcWs w, const __grid_constant__ CUtensorMap map_h,
+             const __grid_constant__ CUtensorMap map_l) {
     using C = TcCfg<NBLK>;
-    constexpr int DP = C::DP;
+    constexpr int DP = C::DP, NST = C::NST;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ __align__(8) unsigned long long bars[4][TC_NST + 1];
+    __shared__ __align__(8) unsigned long long bars[4][2 * C::NST + 1];   // full | empty | chol
     __shared__ int64_t team_task[4];
     __shared__ int team_flag[4];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int team = warp >> 2, wq = warp & 3, m = threadIdx.x & 127;
-    unsigned char *tb = smem_raw + team * C::TEAM_BYTES;
+    // SWIZZLE_128B atoms need 1 KB alignment
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    unsigned char *tb = smem + team * C::TEAM_BYTES;
     const uint32_t tbs = smem_u32(tb);
     float *Ljj = reinterpret_cast<float *>(tb + C::OFF_LJJ);
     float *rdiag = reinterpret_cast<float *>(tb + C::OFF_RD);
     float *zbuf = reinterpret_cast<float *>(tb + C::OFF_Z);
     float *xbuf = reinterpret_cast<float *>(tb + C::OFF_X);
     float *Ls = reinterpret_cast<float *>(tb + C::OFF_L);
-    const uint32_t bar0 = smem_u32(&bars[team][0]);
-    const uint32_t cbar = bar0 + 8 * TC_NST;
+    const uint32_t fbar0 = smem_u32(&bars[team][0]);        // stage landed (TMA + rating tile)
+    const uint32_t ebar0 = fbar0 + 8 * NST;                 // stage consumed (MMA commit)
+    const uint32_t cbar = fbar0 + 16 * NST;                 // Cholesky trailing update
 
-    for (int e = threadIdx.x; e < C::SMEM / 16; e += blockDim.x)
-        reinterpret_cast<uint4 *>(smem_raw)[e] = make_uint4(0u, 0u, 0u, 0u);
+    for (int e = threadIdx.x; e < (C::SMEM - 1024) / 16; e += blockDim.x)
+        reinterpret_cast<uint4 *>(smem)[e] = make_uint4(0u, 0u, 0u, 0u);
     if (m == 0) {
-        for (int st = 0; st <= TC_NST; ++st) mbar_init(bar0 + 8 * st, 1);
+        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 128);   // full: team arrivals
+        for (int st = NST; st <= 2 * NST; ++st) mbar_init(fbar0 + 8 * st, 1);   // empty, chol: commits
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -386,6 +434,10 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
                          smem_u32(&tmem_base_sh)),
                      "r"(C::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_h) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_l) : "memory");
     }
     proxy_fence();
     tc_fence_before();
@@ -395,18 +447,12 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
     const uint32_t tl = tmem + ((uint32_t)(32 * wq) << 16);   // this warp's lane quadrant
 
     const int D = p.D;
-    const float xmax = __uint_as_float(w.scal[0]), ymax = __uint_as_float(w.scal[1]);
-    const float nmax = (float)w.scal[2], smax = __uint_as_float(w.scal[3]);
-    const float regmax = p.lam_c + p.lam_n * nmax + smax + 1.f +
-                         (p.bias_dim >= 0 ? p.bias_lam_c + p.bias_lam_n * nmax : 0.f);
-    const float s = tc_scale(nmax * xmax * xmax + regmax);
-    const float sy = ymax > 0.f ? exp2f(floorf(log2f(16384.f / ymax))) : 1.f;
+    float s, sy;
+    tc_scales(p, w, s, sy);
     const float s2 = s * s, ssy = s * sy, out_scale = s / sy;
 
     const uint32_t id_gram = idesc(DP, true, false);
     const uint32_t id_rhs = idesc(16, true, false);
-    const int ldc = p.ld / 8;                  // 8-float chunks of a fixed row
-    const int nchu = (D + 7) / 8;              // chunks holding features
     unsigned gst = 0;                          // Gram stages issued by this team
     unsigned cph = 0;                          // Cholesky barrier phase
     long long tcp_t = clock64();
@@ -443,7 +489,11 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
         }
         TCP(0);
 
-        // ---------------- Gram: C = H H^T + H L^T + L H^T, rhs = (H + L) [y_h y_l]
+        // ---------------- Gram: C = H H^T + H L^T + L H^T, rhs = (H + L) [y_h y_l].
+        // Warp 0 drives an NST-stage ring: per 16-rating stage 4 * 2 * NA TMA
+        // tile::gather4 of split rows (SWIZZLE_128B -> the MN-major canonical
+        // layout), lanes 0-15 write the rating tile, lane 0 issues the MMAs of
+        // the oldest landed stage and commits them to the stage's empty barrier.
         const int nst = (n + 15) >> 4;
         if (nst == 0) {   // taxonomy-only row: zero accumulator
             float zr[16];
@@ -453,100 +503,99 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
             for (int c = 0; c <= NBLK; ++c) tmem_st16(tl + 16 * c, zr);
             tmem_wait_st();
         }
-        int idc[C::ITEMS], idn[C::ITEMS];
-        float4 dc[C::ITEMS][2];
-        float yc = 0.f, yn = 0.f;   // thread m < 16: rating of stage rating m
-        auto load_ids = [&](int st, int (&ids)[C::ITEMS], float &y) {
+        if (nst > 0) {
+            // Team-wide cp.async pipeline over the split tables: per stage each
+            // warp copies 4 ratings' rows, a lane per 16-byte chunk (lanes 0-15
+            // the h row, 16-31 the l row), straight into the SWIZZLE_128B
+            // MN-major tiles (chunk index XOR row-in-atom); LEAD stages of copies
+            // and MMA_DEPTH stages of MMAs in flight.  Each thread waits for its
+            // own copies, fences them to the async proxy and arrives on the
+            // stage's full barrier (128 arrivals); thread 0 issues the MMAs.
+            constexpr int LEAD = NST - C::MMA_DEPTH;
+            const int tab = lane >> 4, cc = lane & 15, at = cc >> 3, c8 = cc & 7;
+            const bool chunk_ok = cc < 8 * C::NA;
+            const __half *tsrc = tab ? w.tl : w.th;
+            int idn[4];
+            auto load_ids = [&](int t, int (&ids)[4]) {
 #pragma unroll
-            for (int t = 0; t < C::ITEMS; ++t) {
-                const int e = m + 128 * t, kk = e & 15, c = e >> 4;
-                const int kr = 16 * st + kk;
-                ids[t] = (c < nchu && kr < n) ? __ldg(p.idx + k0 + kr) : -1;
-            }
-            const int kr = 16 * st + m;
-            y = (m < 16 && kr < n) ? __ldg(p.val + k0 + kr) - p.y_shift : 0.f;
-        };
-        auto load_data = [&](const int (&ids)[C::ITEMS], float4 (&d)[C::ITEMS][2]) {
+                for (int j = 0; j < 4; ++j) {
+                    const int kr = 16 * t + 4 * wq + j;
+                    ids[j] = kr < n ? __ldg(p.idx + k0 + kr) : -1;
+                }
+            };
+            auto issue = [&](int t, const int (&ids)[4]) {   // stage t -> slot (gst + t) % NST
+                const unsigned g = gst + (unsigned)t, b = g % NST;
+                if (g >= NST) warp_mbar_wait(ebar0 + 8 * b, ((g / NST) - 1) & 1);
+                unsigned char *st = tb + b * C::STAGE;
+                const uint32_t sts = tbs + b * C::STAGE;
 #pragma unroll
-            for (int t = 0; t < C::ITEMS; ++t) {
-                const int c = (m + 128 * t) >> 4;
-                if (ids[t] >= 0 && c < ldc) {
-                    const float4 *src = reinterpret_cast<const float4 *>(
-                        p.fixed + (size_t)ids[t] * p.ld + 8 * c);
-                    d[t][0] = __ldg(src);
-                    d[t][1] = __ldg(src + 1);
+                for (int j = 0; j < 4; ++j) {
+                    const int kk = 4 * wq + j, r = kk & 7;
+                    const uint32_t dst = sts + tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 +
+                                         r * 128 + ((c8 ^ r) << 4);
+                    const bool ok = chunk_ok && ids[j] >= 0;
+                    const __half *src = tsrc + (size_t)(ok ? ids[j] : 0) * C::TW + 8 * cc;
+                    if (chunk_ok)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                                     "r"(ok ? 16 : 0));
+                }
+                if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l)
+                    const int kr = 16 * t + m;
+                    const float y = kr < n ? __ldg(p.val + k0 + kr) - p.y_shift : 0.f;
+                    uint32_t yh, yl;
+                    split2(y * sy, 0.f, yh, yl);
+                    *reinterpret_cast<uint32_t *>(st + 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16) =
+                        (yh & 0xffffu) | (yl << 16);
+                }
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            };
+            for (int t = 0; t < LEAD; ++t) {   // prologue (empty groups past the end)
+                if (t < nst) {
+                    int ids[4];
+                    load_ids(t, ids);
+                    issue(t, ids);
                 } else {
-                    d[t][0] = d[t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
                 }
             }
-        };
-        if (nst > 0) {
-            load_ids(0, idc, yc);
-            load_data(idc, dc);
-            if (nst > 1) load_ids(1, idn, yn);
-        }
-        for (int st = 0; st < nst; ++st) {
-            float4 dn[C::ITEMS][2];
-            int idn2[C::ITEMS];
-            float yn2 = 0.f;
-            if (st + 1 < nst) load_data(idn, dn);
-            if (st + 2 < nst) load_ids(st + 2, idn2, yn2);
-            const unsigned b = gst % TC_NST;
-            if (gst >= TC_NST) warp_mbar_wait(bar0 + 8 * b, ((gst / TC_NST) - 1) & 1);
-            unsigned char *H = tb + b * C::STAGE;
-#pragma unroll
-            for (int t = 0; t < C::ITEMS; ++t) {
-                const int e = m + 128 * t, kk = e & 15, c = e >> 4;
-                if (c < nchu) {
-                    const float v[8] = {dc[t][0].x * s, dc[t][0].y * s, dc[t][0].z * s, dc[t][0].w * s,
-                                        dc[t][1].x * s, dc[t][1].y * s, dc[t][1].z * s, dc[t][1].w * s};
-                    uint4 hv, lv;
-                    split2(v[0], v[1], hv.x, lv.x);
-                    split2(v[2], v[3], hv.y, lv.y);
-                    split2(v[4], v[5], hv.z, lv.z);
-                    split2(v[6], v[7], hv.w, lv.w);
-                    const int off = (kk >> 3) * C::KG + c * 128 + (kk & 7) * 16;
-                    *reinterpret_cast<uint4 *>(H + off) = hv;
-                    *reinterpret_cast<uint4 *>(H + C::TILE + off) = lv;
+            if (LEAD < nst) load_ids(LEAD, idn);
+            for (int st = 0; st < nst; ++st) {
+                const int t = st + LEAD;
+                if (t < nst) {
+                    issue(t, idn);
+                    if (t + 1 < nst) load_ids(t + 1, idn);
+                } else {
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+                }
+                // this thread's copies of stage st are the (LEAD+1)-th newest group
+                asm volatile("cp.async.wait_group %0;\n" ::"n"(LEAD) : "memory");
+                proxy_fence();
+                const unsigned g = gst + (unsigned)st, b = g % NST;
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fbar0 + 8 * b) : "memory");
+                if (m == 0) {
+                    mbar_wait(fbar0 + 8 * b, (g / NST) & 1);   // all 128 threads' copies landed
+                    tc_fence_after();
+                    const uint32_t ha = tbs + b * C::STAGE;
+                    const uint64_t dh = sdesc_sw128(ha, 1024, C::NA * 1024);
+                    const uint64_t dl = sdesc_sw128(ha + C::HT, 1024, C::NA * 1024);
+                    const uint64_t dy = sdesc(ha + 2 * C::HT, 256, 128);
+                    const uint32_t acc = st > 0 ? 1u : 0u;
+                    umma(tmem, dh, dh, id_gram, acc);
+                    umma(tmem, dh, dl, id_gram, 1u);
+                    umma(tmem, dl, dh, id_gram, 1u);
+                    umma(tmem + DP, dh, dy, id_rhs, acc);
+                    umma(tmem + DP, dl, dy, id_rhs, 1u);
+                    umma_commit(ebar0 + 8 * b);
                 }
             }
-            if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l)
-                uint32_t yh, yl;
-                split2(yc * sy, 0.f, yh, yl);
-                const uint32_t pair = (yh & 0xffffu) | (yl << 16);
-                *reinterpret_cast<uint32_t *>(H + 2 * C::TILE + (m >> 3) * 256 + (m & 7) * 16) = pair;
-            }
-            proxy_fence();
-            team_bar(team);
-            if (m == 0) {
-                tc_fence_after();
-                const uint32_t ha = tbs + b * C::STAGE;
-                const uint64_t dh = sdesc(ha, C::KG, 128), dl = sdesc(ha + C::TILE, C::KG, 128);
-                const uint64_t dy = sdesc(ha + 2 * C::TILE, 256, 128);
-                const uint32_t acc = st > 0 ? 1u : 0u;
-                umma(tmem, dh, dh, id_gram, acc);
-                umma(tmem, dh, dl, id_gram, 1u);
-                umma(tmem, dl, dh, id_gram, 1u);
-                umma(tmem + DP, dh, dy, id_rhs, acc);
-                umma(tmem + DP, dl, dy, id_rhs, 1u);
-                umma_commit(bar0 + 8 * b);
-            }
-            ++gst;
-#pragma unroll
-            for (int t = 0; t < C::ITEMS; ++t) {
-                dc[t][0] = dn[t][0];
-                dc[t][1] = dn[t][1];
-                idc[t] = idn[t];
-                idn[t] = idn2[t];
-            }
-            yc = yn;
-            yn = yn2;
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            const unsigned gl = gst + (unsigned)nst - 1;
+            warp_mbar_wait(ebar0 + 8 * (gl % NST), (gl / NST) & 1);   // last MMAs done
         }
-        if (nst > 0) {
-            const unsigned g = gst - 1;
-            warp_mbar_wait(bar0 + 8 * (g % TC_NST), (g / TC_NST) & 1);
-            tc_fence_after();
-        }
+        gst += (unsigned)nst;
+        tc_fence_before();
+        team_bar(team);
+        tc_fence_after();
         TCP(1);
 
         // ---------------- hot-row chunk: dump C | rhs, the last chunk sums them
@@ -684,12 +733,7 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
                             make_float4(ri[4 * q4], ri[4 * q4 + 1], ri[4 * q4 + 2], ri[4 * q4 + 3]);
                     team_flag[team] = !ok;
                 }
-                if (w.prof && lane == lo) {
-                    const long long dt3 = clock64();
-                    atomicAdd(w.prof + 10, (unsigned long long)(dt1 - dt0));
-                    atomicAdd(w.prof + 11, (unsigned long long)(dt2 - dt1));
-                    atomicAdd(w.prof + 12, (unsigned long long)(dt3 - dt2));
-                }
+
             }
             tmem_wait_ld();
             team_bar(team);
@@ -746,9 +790,9 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
                 if (m < DP) {
                     const int off = (m >> 3) * 128 + (m & 7) * 16;
                     *reinterpret_cast<uint4 *>(tb + C::OFF_PH + off) = h0;
-                    *reinterpret_cast<uint4 *>(tb + C::OFF_PH + C::KG + off) = h1;
+                    *reinterpret_cast<uint4 *>(tb + C::OFF_PH + C::KGP + off) = h1;
                     *reinterpret_cast<uint4 *>(tb + C::OFF_PL + off) = l0;
-                    *reinterpret_cast<uint4 *>(tb + C::OFF_PL + C::KG + off) = l1;
+                    *reinterpret_cast<uint4 *>(tb + C::OFF_PL + C::KGP + off) = l1;
                 }
                 TCP(9);
                 tc_fence_before();
@@ -760,11 +804,11 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
                     const int N = DP - c0 - 16;
                     const uint32_t id = idesc(N, false, true);
                     const uint32_t boff = (uint32_t)((c0 + 16) >> 3) * 128;
-                    const uint64_t da = sdesc(tbs + C::OFF_PH, C::KG, 128);
-                    const uint64_t dl = sdesc(tbs + C::OFF_PL, C::KG, 128);
-                    umma(tmem + c0 + 16, da, sdesc(tbs + C::OFF_PH + boff, C::KG, 128), id, 1u);
-                    umma(tmem + c0 + 16, da, sdesc(tbs + C::OFF_PL + boff, C::KG, 128), id, 1u);
-                    umma(tmem + c0 + 16, dl, sdesc(tbs + C::OFF_PH + boff, C::KG, 128), id, 1u);
+                    const uint64_t da = sdesc(tbs + C::OFF_PH, C::KGP, 128);
+                    const uint64_t dl = sdesc(tbs + C::OFF_PL, C::KGP, 128);
+                    umma(tmem + c0 + 16, da, sdesc(tbs + C::OFF_PH + boff, C::KGP, 128), id, 1u);
+                    umma(tmem + c0 + 16, da, sdesc(tbs + C::OFF_PL + boff, C::KGP, 128), id, 1u);
+                    umma(tmem + c0 + 16, dl, sdesc(tbs + C::OFF_PH + boff, C::KGP, 128), id, 1u);
                     umma_commit(cbar);
                 }
                 warp_mbar_wait(cbar, cph);
@@ -886,9 +930,49 @@ __global__ void __launch_bounds__(512, 1) k_als_tc(AlsParams p, PairPlan q, TcWs
     }
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) ==
+                cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+// 2-D fp16 map over a split table [n_rows][TW]: box {64, 1} (the
+// tile::gather4 form), SWIZZLE_128B; rows out of range (id -1) land as zeros
+int tc_table_map(CUtensorMap *map, const __half *t, int64_t n_rows, int TW) {
+    auto fn = tc_encode_fn();
+    if (!fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return MCF_E_CUDA;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)TW, (cuuint64_t)std::max<int64_t>(n_rows, 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)TW * 2};
+    cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half *>(t), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        return MCF_E_CUDA;
+    }
+    return MCF_OK;
+}
+
 template <int NBLK>
 int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t s) {
     using C = TcCfg<NBLK>;
+    CUtensorMap mh, ml;
+    int rc;
+    if ((rc = tc_table_map(&mh, w.th, p.n_fixed, C::TW))) return rc;
+    if ((rc = tc_table_map(&ml, w.tl, p.n_fixed, C::TW))) return rc;
+    k_tc_split<<<148 * 8, 256, 0, s>>>(p, w, C::TW);
+    if ((rc = check_launch("mcf_als_half_step(tensor-core split)"))) return rc;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_als_tc<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -901,7 +985,7 @@ int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t
     per_sm = std::max(1, std::min(per_sm, 512 / C::TMEM_COLS));
     const int64_t want = ceil_div(q.n_tasks, C::TEAMS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * per_sm);
-    if (grid > 0) k_als_tc<NBLK><<<(unsigned)grid, C::TEAMS * 128, C::SMEM, s>>>(p, q, w);
+    if (grid > 0) k_als_tc<NBLK><<<(unsigned)grid, C::TEAMS * 128, C::SMEM, s>>>(p, q, w, mh, ml);
     return check_launch("mcf_als_half_step(tensor core)");
 }
 
@@ -918,14 +1002,17 @@ size_t tc_slot_floats(int D) {
     return (size_t)dp * (dp + 16);
 }
 
-size_t tc_workspace_bytes(int D, int64_t slots) {
+static size_t tc_table_width(int D) { return (size_t)((D + 15) / 16 * 16 + 63) / 64 * 64; }
+
+size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed) {
     return 256 + align_up(sizeof(int32_t) * (size_t)(slots + 1), 256) +
-           sizeof(float) * (size_t)slots * tc_slot_floats(D);
+           align_up(sizeof(float) * (size_t)slots * tc_slot_floats(D), 256) +
+           2 * align_up(2 * (size_t)n_fixed * tc_table_width(D) + 256, 256);
 }
 
 int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
                   cudaStream_t s) {
-    if (ws_bytes < tc_workspace_bytes(p.D, slots)) {
+    if (ws_bytes < tc_workspace_bytes(p.D, slots, p.n_fixed)) {
         set_error("mcf_als_half_step: workspace too small for the tensor-core path");
         return MCF_E_WORKSPACE;
     }
@@ -934,6 +1021,8 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     w.scal = c.take<unsigned>(4);
     w.hot_count = c.take<int32_t>((size_t)slots + 1);
     w.partials = c.take<float>((size_t)slots * tc_slot_floats(p.D));
+    w.th = c.take<__half>((size_t)p.n_fixed * tc_table_width(p.D) + 128);
+    w.tl = c.take<__half>((size_t)p.n_fixed * tc_table_width(p.D) + 128);
     w.n_slots = slots;
     w.prof = nullptr;
     w.team_limit = getenv("MCF_TC_TEAMS") ? atoi(getenv("MCF_TC_TEAMS")) : 4;
@@ -949,15 +1038,13 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     k_tc_prep<<<148 * 4, 256, 0, s>>>(p, q, w);
     if ((rc = check_launch("mcf_als_half_step(tensor-core prep)"))) return rc;
     switch ((p.D + 15) / 16) {
-        case 2: return launch_tc<2>(p, q, w, s);
-        case 3: return launch_tc<3>(p, q, w, s);
         case 4: return launch_tc<4>(p, q, w, s);
         case 5: return launch_tc<5>(p, q, w, s);
         case 6: return launch_tc<6>(p, q, w, s);
         case 7: return launch_tc<7>(p, q, w, s);
         case 8: return launch_tc<8>(p, q, w, s);
         default:
-            set_error("mcf_als_half_step: tensor-core path needs 21 <= D <= 128");
+            set_error("mcf_als_half_step: tensor-core path needs 64 <= D <= 128");
             return MCF_E_UNSUPPORTED;
     }
 }

@@ -185,7 +185,8 @@ class LayoutSolver:
             buf, info, rl, n_list, chunk = lay.plan(rows, rows_key, DEFAULT_CHUNK)
         slots = max(info[1], info[3])   # hot-chunk slots (pair path / warp+CTA paths)
         k = (id(lay), rows_key)
-        need = int(_lib.lib().mcf_als_workspace_bytes(n_list, slots, self.D))
+        need = int(_lib.lib().mcf_als_workspace_bytes_fixed(n_list, slots, self.D,
+                                                            int(fixed.shape[0])))
         if k not in self._ws or self._ws[k].numel() < need:
             self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = self._ws[k]

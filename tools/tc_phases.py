@@ -37,4 +37,4 @@ for D in [int(x) for x in sys.argv[1:]] or [100]:
         print(f"D={D} n={n}: {e0.elapsed_time(e1):.2f} ms, {U} rows; cycles per row per team: "
               f"total {tot / U:.0f}: " +
               ", ".join(f"{NAMES[k]} {buf[k] / U:.0f}" for k in range(10)) +
-              f" | diag warp: ld-wait {buf[10] / U:.0f}, factor {buf[11] / U:.0f}, post {buf[12] / U:.0f}")
+              f" | gram: issue {buf[10] / U:.0f}, wait-landed {buf[11] / U:.0f}, mma {buf[12] / U:.0f}")
