@@ -76,9 +76,17 @@ struct TcCfg {
     static constexpr int PT = 2 * KGP;             // panel tile: DP rows x 16 k
     static constexpr int COLS = DP + 16;           // TMEM columns per team: Gram | rhs
     static constexpr int LS_BYTES = DP * (DP + 1) / 2 * 4;
+    // dual form (rows with n <= DUAL_MAX < D ratings): the gathered rows as
+    // K-major tiles (8-row core matrices, 16-byte feature chunks DLBO apart),
+    // after the (at most 64 x 64) packed L
+    static constexpr int DUAL_MAX = 64;
+    static constexpr int DLBO = DUAL_MAX / 8 * 128;
+    static constexpr int DTILE = DP / 8 * DLBO;
+    static constexpr int OFF_DX = 9216;
     // the stage ring (Gram) and the packed L (Cholesky .. back substitution)
     // are never live together: one region
-    static constexpr int RING = NST * STAGE > LS_BYTES ? NST * STAGE : LS_BYTES;
+    static constexpr int RING0 = NST * STAGE > LS_BYTES ? NST * STAGE : LS_BYTES;
+    static constexpr int RING = RING0 > OFF_DX + 2 * DTILE ? RING0 : OFF_DX + 2 * DTILE;
     static constexpr int OFF_L = 0;
     static constexpr int OFF_PH = (RING + 1023) / 1024 * 1024;
     static constexpr int OFF_PL = OFF_PH + PT;
@@ -302,7 +310,7 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr, uint32_t lbo, uin
 
 template <int DP, bool UPPER>
 __device__ __forceinline__ void warp_trsv(float (&zr)[4], const float *Ls, const float *rdiag,
-                                          int lane, float *out) {
+                                          int lane, float *out, int dim = DP) {
     float xr[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
@@ -311,7 +319,7 @@ __device__ __forceinline__ void warp_trsv(float (&zr)[4], const float *Ls, const
 #pragma unroll
     for (int gq = 0; gq < 4; ++gq) {
         const int l0 = 8 * (UPPER ? 3 - gq : gq), i0 = 32 * qs + l0;
-        if (i0 >= DP) continue;
+        if (i0 >= DP || i0 >= dim) continue;
         // all loads of the group first (their latency overlaps the shuffles)
         float lb[8][8], lu[4][8], rd[8];
 #pragma unroll
@@ -382,16 +390,17 @@ __device__ __forceinline__ void warp_trsv(float (&zr)[4], const float *Ls, const
 
 // the refinement's two solves, out of line (keeps the kernel's registers)
 template <int DP>
-__device__ __noinline__ float4 trsv_fwd(float4 z, const float *Ls, const float *rdiag, int lane) {
+__device__ __noinline__ float4 trsv_fwd(float4 z, const float *Ls, const float *rdiag, int lane,
+                                        int dim) {
     float zr[4] = {z.x, z.y, z.z, z.w};
-    warp_trsv<DP, false>(zr, Ls, rdiag, lane, nullptr);
+    warp_trsv<DP, false>(zr, Ls, rdiag, lane, nullptr, dim);
     return make_float4(zr[0], zr[1], zr[2], zr[3]);
 }
 template <int DP>
 __device__ __noinline__ void trsv_back(float4 z, const float *Ls, const float *rdiag, int lane,
-                                       float *out) {
+                                       float *out, int dim) {
     float zr[4] = {z.x, z.y, z.z, z.w};
-    warp_trsv<DP, true>(zr, Ls, rdiag, lane, out);
+    warp_trsv<DP, true>(zr, Ls, rdiag, lane, out, dim);
 }
 
 template <int NBLK>
@@ -488,6 +497,13 @@ __global__ void __launch_bounds__(512, 1)
             continue;
         }
         TCP(0);
+        // dual form for short rows: (X X^T + lam I) alpha = y, x = X^T alpha
+        // (push-through identity) -- an n x n system instead of D x D
+        const bool dual = slot < 0 && nrow > 0 && nrow <= C::DUAL_MAX && nrow < D && !p.tax_T &&
+                          p.bias_dim < 0 && Srow == 0.f;
+        const int dim = dual ? (int)((nrow + 15) & ~15) : DP;
+        const int nblk = dim / 16;
+        if (!dual) {
 
         // ---------------- Gram: C = H H^T + H L^T + L H^T, rhs = (H + L) [y_h y_l].
         // Warp 0 drives an NST-stage ring: per 16-rating stage 4 * 2 * NA TMA
@@ -596,6 +612,45 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_before();
         team_bar(team);
         tc_fence_after();
+        } else {
+            // ---------------- dual Gram K = X X^T (n x n): the n gathered split
+            // rows as K-major tiles (ratings = M/N, features = K), 3 MMAs per 16
+            // features
+            int *ids = reinterpret_cast<int *>(xbuf);
+            if (m < dim) ids[m] = m < n ? __ldg(p.idx + k0 + m) : -1;
+            team_bar(team);
+            const uint32_t dx = tbs + C::OFF_DX;
+            const int items = 2 * (DP / 8) * dim;
+            for (int e = m; e < items; e += 128) {
+                const int r = e % dim, rest = e / dim, c = rest % (DP / 8), t2 = rest / (DP / 8);
+                const int id = ids[r];
+                const bool ok = id >= 0;
+                const __half *src = (t2 ? w.tl : w.th) + (size_t)(ok ? id : 0) * C::TW + 8 * c;
+                const uint32_t dst = dx + t2 * C::DTILE + c * C::DLBO + (r >> 3) * 128 + (r & 7) * 16;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                             "r"(ok ? 16 : 0));
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            proxy_fence();
+            tc_fence_before();
+            team_bar(team);
+            if (m == 0) {
+                tc_fence_after();
+                const uint32_t idd = idesc(dim, false, false);
+                for (int kk = 0; kk < DP / 16; ++kk) {
+                    const uint64_t dh = sdesc(dx + 2 * kk * C::DLBO, C::DLBO, 128);
+                    const uint64_t dl = sdesc(dx + C::DTILE + 2 * kk * C::DLBO, C::DLBO, 128);
+                    umma(tmem, dh, dh, idd, kk > 0 ? 1u : 0u);
+                    umma(tmem, dh, dl, idd, 1u);
+                    umma(tmem, dl, dh, idd, 1u);
+                }
+                umma_commit(cbar);
+            }
+            warp_mbar_wait(cbar, cph);
+            cph ^= 1u;
+            tc_fence_after();
+        }
         TCP(1);
 
         // ---------------- hot-row chunk: dump C | rhs, the last chunk sums them
@@ -656,7 +711,10 @@ __global__ void __launch_bounds__(512, 1)
         // s^2, L = s I there, z = x = 0 -- every block runs the same code.
         float rg = s2;   // this row's regulariser (scaled)
         float r;         // rhs b_m, reduced by the finished blocks (forward subst.)
-        {
+        if (dual) {      // (s^2 (X X^T + lam I)) alpha' = s_y y
+            rg = m < n ? (p.lam_c + p.lam_n * (float)nrow) * s2 : s2;
+            r = m < n ? (__ldg(p.val + k0 + m) - p.y_shift) * sy : 0.f;
+        } else {
             const float diag = p.lam_c + p.lam_n * (float)nrow + p.tau * Srow;
             if (m < D) rg = diag_at(p, m, diag, (float)nrow) * s2;
             uint32_t rb[2];
@@ -670,7 +728,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         bool failed = false;
 #pragma unroll 1
-        for (int J = 0; J < NBLK; ++J) {
+        for (int J = 0; J < nblk; ++J) {
             const int c0 = 16 * J;
             const int dw = c0 >> 5, lo = c0 & 31, ime = lane - lo;
             const bool inblk = wq == dw && ime >= 0 && ime < 16;
@@ -742,7 +800,7 @@ __global__ void __launch_bounds__(512, 1)
                 failed = true;
                 break;
             }
-            if (m >= c0 + 16 && m < DP) {   // panel rows: x L_JJ^T = a (right-looking), r -= x.z_J
+            if (m >= c0 + 16 && m < dim) {   // panel rows: x L_JJ^T = a (right-looking), r -= x.z_J
                 float rd[16], zj[16];
                 lds16(rdiag + c0, rd);
                 lds16(zbuf + c0, zj);
@@ -776,8 +834,8 @@ __global__ void __launch_bounds__(512, 1)
                 for (int j = 0; j < 16; ++j) Lr[j] = a[j];
             }
             TCP(4);
-            if (c0 + 16 < DP) {   // panel tiles, K-major: rows >= c0 + 16 carry L, others 0
-                const bool pr = m >= c0 + 16 && m < DP;
+            if (c0 + 16 < dim) {   // panel tiles, K-major: rows >= c0 + 16 carry L, others 0
+                const bool pr = m >= c0 + 16 && m < dim;
                 uint4 h0, l0, h1, l1;
                 split2(pr ? a[0] : 0.f, pr ? a[1] : 0.f, h0.x, l0.x);
                 split2(pr ? a[2] : 0.f, pr ? a[3] : 0.f, h0.y, l0.y);
@@ -801,7 +859,7 @@ __global__ void __launch_bounds__(512, 1)
                 // trailing update C -= P_h P_h^T + P_h P_l^T + P_l P_h^T
                 if (m == 0) {
                     tc_fence_after();
-                    const int N = DP - c0 - 16;
+                    const int N = dim - c0 - 16;
                     const uint32_t id = idesc(N, false, true);
                     const uint32_t boff = (uint32_t)((c0 + 16) >> 3) * 128;
                     const uint64_t da = sdesc(tbs + C::OFF_PH, C::KGP, 128);
@@ -829,20 +887,79 @@ __global__ void __launch_bounds__(512, 1)
         // per step: their right-hand sides are shuffled to every lane, each lane
         // solves the 4 x 4 diagonal block redundantly, then updates its own rows
         // (lane l holds rows l, l + 32, l + 64, l + 96); result -> xbuf
-        auto back_sub = [&](float (&zr)[4]) { warp_trsv<DP, true>(zr, Ls, rdiag, lane, xbuf); };
+        auto back_sub = [&](float (&zr)[4]) { warp_trsv<DP, true>(zr, Ls, rdiag, lane, xbuf, dim); };
         team_bar(team);
         if (wq == 0) {
             float zr[4];
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
                 const int mq = lane + 32 * q4;
-                zr[q4] = mq < DP ? zbuf[mq] : 0.f;
+                zr[q4] = mq < dim ? zbuf[mq] : 0.f;
             }
             back_sub(zr);
         }
         team_bar(team);
         TCP(6);
         float xo = (m < DP ? xbuf[m] : 0.f) * out_scale;
+        if (dual) {   // x = out_scale (s X)^T alpha' from the tiles
+            float acc = 0.f;
+            if (m < D) {
+                const unsigned char *Ht = tb + C::OFF_DX, *Lt = Ht + C::DTILE;
+                const int base = (m >> 3) * C::DLBO + (m & 7) * 2;
+                for (int rr = 0; rr < n; ++rr) {
+                    const int off = base + (rr >> 3) * 128 + (rr & 7) * 16;
+                    const float v = __half2float(*reinterpret_cast<const __half *>(Ht + off)) +
+                                    __half2float(*reinterpret_cast<const __half *>(Lt + off));
+                    acc = fmaf(xbuf[rr], v, acc);
+                }
+            }
+            xo = acc * out_scale;
+            // one refinement step in the dual space: rho_r = y_r - x_r.x - lam alpha_r,
+            // alpha += (X X^T + lam I)^{-1} rho, x += X^T (that correction)
+            const float alpha_m = m < n ? xbuf[m] * (s2 / sy) : 0.f;
+            team_bar(team);   // xbuf (alpha') is rewritten below
+            if (m < DP) zbuf[m] = m < D ? xo : 0.f;   // x
+            float *rho = reinterpret_cast<float *>(tb + C::OFF_PH);
+            const float lam2 = p.lam_c + p.lam_n * (float)nrow;
+            team_bar(team);
+            if (m < dim) {
+                float rh = 0.f;
+                if (m < n) {
+                    const int id = __ldg(p.idx + k0 + m);
+                    const float4 *xr4 = reinterpret_cast<const float4 *>(p.fixed + (size_t)id * p.ld);
+                    float d0 = 0.f, d1 = 0.f;
+                    for (int c4 = 0; c4 < p.ld / 4; ++c4) {
+                        const float4 u = __ldg(xr4 + c4);
+                        const float4 xv = *reinterpret_cast<const float4 *>(zbuf + 4 * c4);
+                        d0 = fmaf(u.x, xv.x, d0); d1 = fmaf(u.y, xv.y, d1);
+                        d0 = fmaf(u.z, xv.z, d0); d1 = fmaf(u.w, xv.w, d1);
+                    }
+                    rh = (__ldg(p.val + k0 + m) - p.y_shift) - (d0 + d1) - lam2 * alpha_m;
+                }
+                rho[m] = rh;
+            }
+            team_bar(team);
+            if (wq == 0) {
+                float zr[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int mq = lane + 32 * q4;
+                    zr[q4] = mq < dim ? rho[mq] : 0.f;
+                }
+                const float4 w4 = trsv_fwd<DP>(make_float4(zr[0], zr[1], zr[2], zr[3]), Ls, rdiag,
+                                               lane, dim);
+                trsv_back<DP>(w4, Ls, rdiag, lane, xbuf, dim);
+            }
+            team_bar(team);
+            if (m < D) {   // x += X^T (s^2 w)
+                float acc2 = 0.f;
+                for (int rr = 0; rr < n; ++rr) {
+                    const int id = __ldg(p.idx + k0 + rr);
+                    acc2 = fmaf(xbuf[rr], __ldg(p.fixed + (size_t)id * p.ld + m), acc2);
+                }
+                xo = fmaf(s2, acc2, xo);
+            }
+        }
         // ---------------- one step of iterative refinement for short rows
         // (n < D): fp32 rounding of the Gram times cond(A) (up to ~1e4 at
         // D = 100: the partner factors share a dominant mean direction, the
@@ -850,7 +967,7 @@ __global__ void __launch_bounds__(512, 1)
         // 1e-4 budget there; r = b - A x0 is formed from the ratings
         // (e_k = y_k - x_k.x0, r = sum x_k e_k + tau T - reg x0) and
         // x1 = x0 + A^{-1} r reuses the factorisation.
-        if (slot < 0 && nrow < D && nrow > 0) {
+        if (!dual && slot < 0 && nrow < D && nrow > 0) {
             xbuf[m] = m < D ? xo : 0.f;   // x0, original units (own element)
             team_bar(team);
             // residuals e_k, a thread per rating (n < D <= 128)
@@ -901,8 +1018,9 @@ __global__ void __launch_bounds__(512, 1)
                     const int mq = lane + 32 * q4;
                     zr[q4] = mq < DP ? zbuf[mq] : 0.f;
                 }
-                const float4 w4 = trsv_fwd<DP>(make_float4(zr[0], zr[1], zr[2], zr[3]), Ls, rdiag, lane);
-                trsv_back<DP>(w4, Ls, rdiag, lane, xbuf);
+                const float4 w4 = trsv_fwd<DP>(make_float4(zr[0], zr[1], zr[2], zr[3]), Ls, rdiag,
+                                               lane, DP);
+                trsv_back<DP>(w4, Ls, rdiag, lane, xbuf, DP);
             }
             team_bar(team);
             if (m < D) xo = fmaf(s2, xbuf[m], xo);
