@@ -529,15 +529,19 @@ __global__ void __launch_bounds__(512, 1)
             // stage's full barrier (128 arrivals); thread 0 issues the MMAs.
             constexpr int LEAD = NST - C::MMA_DEPTH;
             const int tab = lane >> 4, cc = lane & 15, at = cc >> 3, c8 = cc & 7;
-            const bool chunk_ok = cc < 8 * C::NA;
+            // chunks past DP only feed Gram rows / columns >= DP (never read): not copied
+            const bool chunk_ok = cc < DP / 8;
             const __half *tsrc = tab ? w.tl : w.th;
             int idn[4];
+            float yv = 0.f;   // thread m < 16: rating m of the prefetched stage
             auto load_ids = [&](int t, int (&ids)[4]) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int kr = 16 * t + 4 * wq + j;
                     ids[j] = kr < n ? __ldg(p.idx + k0 + kr) : -1;
                 }
+                const int kr = 16 * t + m;
+                yv = (m < 16 && kr < n) ? __ldg(p.val + k0 + kr) - p.y_shift : 0.f;
             };
             auto issue = [&](int t, const int (&ids)[4]) {   // stage t -> slot (gst + t) % NST
                 const unsigned g = gst + (unsigned)t, b = g % NST;
@@ -556,10 +560,8 @@ __global__ void __launch_bounds__(512, 1)
                                      "r"(ok ? 16 : 0));
                 }
                 if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l)
-                    const int kr = 16 * t + m;
-                    const float y = kr < n ? __ldg(p.val + k0 + kr) - p.y_shift : 0.f;
                     uint32_t yh, yl;
-                    split2(y * sy, 0.f, yh, yl);
+                    split2(yv * sy, 0.f, yh, yl);
                     *reinterpret_cast<uint32_t *>(st + 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16) =
                         (yh & 0xffffu) | (yl << 16);
                 }

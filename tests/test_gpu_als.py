@@ -260,6 +260,45 @@ def test_dims_reanchored(D, reg):
     assert torch.all(eng.P[:, D:] == 0) and torch.all(eng.Q[:, D:] == 0)
 
 
+@pytest.mark.parametrize("D", [64, 100])
+def test_wide_ill_conditioned_short_rows(D):
+    """The configuration-3 failure mode, small: partner factors with a
+    dominant mean direction (cond(A) ~ 1e3-1e4) and rows of every length
+    class -- n <= 64 (tensor path, dual n x n form + refinement), 64 < n < D
+    (primal + refinement), n >= D, and a row rated by every item --
+    re-anchored against the float64 oracle at 1e-4 on the tensor-core path
+    (the CUDA-core kernels do not refine: tools/parity_probe.py shows them at
+    2-3e-4 on such rows)."""
+    rng = np.random.default_rng(D)
+    U, I = 3000, 500
+    mid = rng.integers(65, D, 900) if D > 66 else rng.integers(3, 65, 900)
+    deg = np.concatenate([rng.integers(3, 65, 1200), mid,
+                          rng.integers(D, 2 * D + 40, 899), [I]])   # last user: every item
+    u = np.repeat(np.arange(U, dtype=np.int32), deg)
+    i = np.concatenate([rng.choice(I, size=d, replace=False) for d in deg]).astype(np.int32)
+    s = rng.integers(0, 101, u.size).astype(np.float32)
+    perm = rng.permutation(u.size)
+    u, i, s = u[perm], i[perm], s[perm]
+    lam = 0.05
+    for mode in ("tc",):
+        try:
+            eng = _engine(u, i, s, U, I, D, chunk=None)
+            # item factors share a dominant direction (the mean of ALS factors)
+            Q = rng.normal(0, 0.3, (I, D)) + 1.5
+            P = rng.normal(0, 0.1, (U, D))
+            eng.set_factors(P, Q)
+            P64, Q64 = (t.double().cpu().numpy() for t in eng.factors())
+            ref, failed = oracle.als_half_step(P64, Q64, u, i, s, "users", lam_n=lam)
+            assert failed == -1
+            eng.half_step("users", 0.0, lam)
+            eng.check()
+            got = eng.factors()[0].double().cpu().numpy()
+            row, mx = _rel_rows(got, ref)
+            assert row < REL_TOL and mx < REL_TOL, (mode, D, row, mx)
+        finally:
+            os.environ.pop("MCF_NO_TC", None)
+
+
 def test_heavy_row_multi_chunk_and_determinism():
     U, I, D = 20_000, 500, 20
     u, i, s = _random_split(U, I, 400_000, 3, hot=11)
