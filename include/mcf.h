@@ -202,6 +202,8 @@ int mcf_allgather_rows(void *comm, float *table, int32_t ld, const int64_t *offs
  *                       r - mu - b_u - [art(i) >= 0] (b_a + q_a . p_u)
  *   mode 2 (artists layout, row = artist, partner = user u, aux = item i):
  *                       r - mu - b_u - b_i - q_i . p_u
+ *   mode 3 (items layout, the artist terms left to the solve epilogue,
+ *           mcf_als_half_step_mfitr_items): r - mu - b_u
  * (Pa = [p | b_u], Qa = [q | b_i], Aa = [q_a | b_a] indexed by artist id). */
 int mcf_mfitr_fixed(const float *main_t, const float *add_t, const int32_t *art, int64_t n,
                     int32_t D, float *out, void *stream);
@@ -244,6 +246,34 @@ int mcf_mfitr_sgd_epoch_locked(const int64_t *uptr, const int32_t *uidx, const f
  * exactly 2 * workers * iters. */
 int mcf_lock_stress(int32_t *locks, float *acc, int32_t n_items, int32_t workers, int32_t iters,
                     void *stream);
+/* ALS-MFITR every-block sweep, item layers and artists without per-rating
+ * artist passes (D = factor dimension + 1 bias, D + 1 <= 21: the Schur pair
+ * path).  mcf_als_half_step_mfitr_items = mcf_als_half_step_bias (bias in
+ * column D-1, lam_c = 0) that also stores every row's augmented system
+ * [A | c | u | d | n] (packed lower A of the D-1 factor coordinates, rhs c,
+ * u = sum x, d = sum y, n; EMIT stride 256 floats, row r at emit + 256 r)
+ * and removes the row's artist terms from its rhs from its own Gram:
+ * c -= A q_a + u b_a, d -= u.q_a + n b_a with [q_a | b_a] =
+ * corr_tab[corr_idx[r]] (targets: r - mu - b_u, mcf_mfitr_targets mode 3).
+ * mcf_mfitr_artist_step then solves every artist's [q_a | b_a] from those
+ * systems: A_a = sum_i A_i, rhs_a = sum_i (c_i - G_i [q_i | b_i]) over the
+ * artist's items (art_ptr / art_items CSR, fixed order), regularised
+ * lam_n n_a (factors) and bias_lam_n n_a (bias), n_a = cnt_ptr[r+1] -
+ * cnt_ptr[r] for the artist's row r = artist_row[j]; results into Aa. */
+int mcf_als_half_step_mfitr_items(const int64_t *ptr, const int32_t *idx, const float *val,
+                                  const float *fixed, int64_t n_fixed, float *out, int32_t D,
+                                  float lam_n, float y_shift, const float *tax_S,
+                                  const float *tax_T, float tau, const int32_t *row_list,
+                                  int32_t n_list, int32_t chunk, const void *plan,
+                                  const int64_t *plan_info, int64_t *fail_row, void *ws,
+                                  size_t ws_bytes, float bias_lam_n, float *emit,
+                                  const float *corr_tab, const int32_t *corr_idx, void *stream);
+size_t mcf_mfitr_artist_workspace_bytes(int32_t n_artists);
+int mcf_mfitr_artist_step(const int64_t *art_ptr, const int32_t *art_items,
+                          const int32_t *artist_row, int32_t n_artists, const int64_t *cnt_ptr,
+                          const float *emit, const float *Qa, float *Aa, int32_t D, float lam_n,
+                          float bias_lam_n, int64_t *fail_row, void *ws, size_t ws_bytes,
+                          void *stream);
 int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t *idx, const float *val,
                       const int32_t *aux, int32_t n_rows, const float *Pa, const float *Qa,
                       const float *Aa, const int32_t *art, float mu, int32_t D, float *out,

@@ -1422,6 +1422,27 @@ __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float
     constexpr int UOFF = RHS0 + LDK, DOFF = UOFF + LDK;
     const int D = p.D;
     sse = reg = 0.0;
+    if constexpr (SCHUR) {
+        if (p.emit) {   // [A | c | u | d | n] for the artist step (before any correction)
+            float *e = p.emit + (size_t)r * EMIT_STRIDE;
+            for (int i = 0; i < RHS0 + LDK; ++i) e[i] = g[i];
+            for (int i = 0; i < LDK; ++i) e[RHS0 + LDK + i] = g[UOFF + i];
+            e[RHS0 + 2 * LDK] = g[DOFF];
+            e[RHS0 + 2 * LDK + 1] = (float)n;
+        }
+        if (p.corr_idx && p.corr_idx[r] >= 0) {   // the row's artist terms, from its Gram
+            const float *v = p.corr_tab + (size_t)p.corr_idx[r] * p.ld;
+            const float ba = v[D];
+            float ud = 0.f;
+            for (int i = 0; i < D; ++i) {
+                float t = fmaf(g[UOFF + i], ba, 0.f);
+                for (int k = 0; k < D; ++k) t = fmaf(g[i >= k ? pidx(i, k) : pidx(k, i)], v[k], t);
+                g[RHS0 + i] -= t;
+                ud = fmaf(g[UOFF + i], v[i], ud);
+            }
+            g[DOFF] -= fmaf((float)n, ba, ud);
+        }
+    }
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     if (n == 0 && S == 0.f) {
         if (p.lam_c > 0.f || p.lam_n > 0.f) {
@@ -1903,6 +1924,34 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
     float *G = Gs[warp];
     const int D = p.D;
     const int64_t n = p.ptr[r + 1] - p.ptr[r];
+    if constexpr (SCHUR) {
+        if (p.emit) {   // [A | c | u | d | n] for the artist step (before any correction)
+            float *e = p.emit + (size_t)r * EMIT_STRIDE;
+            for (int i = lane; i < C::RHS0 + LDK; i += 32) e[i] = G[i];
+            if (lane < LDK) e[C::RHS0 + LDK + lane] = G[C::PU + lane];
+            if (lane == 0) {
+                e[C::RHS0 + 2 * LDK] = G[C::PD];
+                e[C::RHS0 + 2 * LDK + 1] = (float)n;
+            }
+        }
+        if (p.corr_idx && p.corr_idx[r] >= 0) {   // the row's artist terms, from its Gram
+            const float *v = p.corr_tab + (size_t)p.corr_idx[r] * p.ld;
+            const float ba = v[D];
+            float t = 0.f, ud = 0.f;
+            if (lane < D) {
+                t = G[C::PU + lane] * ba;
+                for (int k = 0; k < D; ++k)
+                    t = fmaf(G[lane >= k ? pidx(lane, k) : pidx(k, lane)], v[k], t);
+                ud = G[C::PU + lane] * v[lane];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ud += __shfl_xor_sync(FULL, ud, o);
+            __syncwarp();
+            if (lane < D) G[C::RHS0 + lane] -= t;
+            if (lane == 0) G[C::PD] -= fmaf((float)n, ba, ud);
+            __syncwarp();
+        }
+    }
     const float S = p.tax_S ? p.tax_S[r] : 0.f;
     const float lam_row = p.lam_c + p.lam_n * (float)n;
     const float diag = lam_row + p.tau * S;
@@ -1987,6 +2036,75 @@ __global__ void __launch_bounds__(256) k_als_heavy(AlsParams p, PairPlan q) {
             p.obj_partial[2 * (p.obj_groups + hr)] = (double)yy - (double)bx - (double)diag * xx;
             p.obj_partial[2 * (p.obj_groups + hr) + 1] = (double)lam_row * xx;
         }
+    }
+}
+
+// --- MFITR artist step from the item layers' emitted systems.  An artist's
+// block [q_a | b_a] has x = [p_u | 1] over the ratings of its items, so its
+// Gram is the sum of its items' Grams and its rhs the sum of the items'
+// base rhs minus G_i [q_i | b_i] (mfitr.py:203-216 with q_i, b_i fixed):
+// one pass over I emitted systems instead of one over every rating.  Warp per
+// artist, items in CSR order (fixed order); the summed system lands in a
+// Schur partial slot (PSTR_S) that k_als_heavy<_, true> then solves.
+template <int NBK>
+__global__ void k_mfitr_artist_reduce(const int64_t *art_ptr, const int32_t *art_items,
+                                      int32_t n_art, const float *emit, const float *Qa, int ld,
+                                      int D, float *slots) {
+    using C = PairGeom<NBK>;
+    constexpr int LDK = C::LDK, RHS0 = C::RHS0;
+    constexpr int NA = (RHS0 + 31) / 32;   // packed A entries per lane
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < n_art; a += warps) {
+        float accA[NA], accC = 0.f, accU = 0.f, accD = 0.f;
+#pragma unroll
+        for (int t = 0; t < NA; ++t) accA[t] = 0.f;
+        for (int64_t k = art_ptr[a]; k < art_ptr[a + 1]; ++k) {
+            const int i = art_items[k];
+            const float *e = emit + (size_t)i * EMIT_STRIDE;
+            const float *v = Qa + (size_t)i * ld;          // [q_i | b_i]
+#pragma unroll
+            for (int t = 0; t < NA; ++t) {
+                const int idx = lane + 32 * t;
+                if (idx < RHS0) accA[t] += __ldg(e + idx);
+            }
+            const float bi = __ldg(v + D);
+            float corr = 0.f, ud = 0.f;
+            if (lane < D) {
+                corr = __ldg(e + RHS0 + LDK + lane) * bi;
+                for (int c = 0; c < D; ++c)
+                    corr = fmaf(__ldg(e + (lane >= c ? pidx(lane, c) : pidx(c, lane))), __ldg(v + c),
+                                corr);
+                accC += __ldg(e + RHS0 + lane) - corr;
+                accU += __ldg(e + RHS0 + LDK + lane);
+                ud = __ldg(e + RHS0 + LDK + lane) * __ldg(v + lane);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ud += __shfl_xor_sync(FULL, ud, o);
+            if (lane == 0)
+                accD += __ldg(e + RHS0 + 2 * LDK) - fmaf(__ldg(e + RHS0 + 2 * LDK + 1), bi, ud);
+        }
+        float *dst = slots + (size_t)a * C::PSTR_S;
+#pragma unroll
+        for (int t = 0; t < NA; ++t) {
+            const int idx = lane + 32 * t;
+            if (idx < RHS0) dst[idx] = accA[t];
+        }
+        if (lane < LDK) {
+            dst[RHS0 + lane] = lane < D ? accC : 0.f;
+            dst[C::PU + lane] = lane < D ? accU : 0.f;
+        }
+        if (lane == 0) {
+            dst[C::GRAM] = 0.f;
+            dst[C::PD] = accD;
+        }
+    }
+}
+
+__global__ void k_iota(int32_t *a, int32_t *b, int32_t n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+        if (i < n) a[i] = i;
+        b[i] = i;
     }
 }
 
@@ -2321,6 +2439,12 @@ extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t
     return mcf_als_workspace_bytes_fixed(n_list, slots, D, 0);
 }
 
+// MFITR item-layer extras for the next half_step_impl call (set by
+// mcf_als_half_step_mfitr_items only)
+static thread_local float *g_emit = nullptr;
+static thread_local const float *g_corr_tab = nullptr;
+static thread_local const int32_t *g_corr_idx = nullptr;
+
 static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *val,
                           const float *wts, const float *fixed, int64_t n_fixed, float *out,
                           int32_t D, float lam_c, float lam_n, float y_shift, const float *tax_S,
@@ -2372,6 +2496,13 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
     }
     p.peer_out = peer_out;
     p.n_peers = peer_out ? n_peers : 0;
+    p.emit = g_emit;
+    p.corr_tab = g_corr_tab;
+    p.corr_idx = g_corr_idx;
+    if ((p.emit || p.corr_idx) && !p.schur) {
+        set_error("mcf_als_half_step_mfitr_items: the row systems did not take the Schur pair path");
+        return MCF_E_UNSUPPORTED;
+    }
     p.mc_out = mc_out;
     if (n_peers < 0 || (n_peers > 0 && !peer_out)) {
         set_error("mcf_als_half_step: peer_out must hold n_peers >= 0 device pointers");
@@ -2519,4 +2650,98 @@ extern "C" int mcf_als_half_step_multicast(const int64_t *ptr, const int32_t *id
     return half_step_impl(ptr, idx, val, wts, fixed, n_fixed, out, D, lam_c, lam_n, y_shift, tax_S,
                           tax_T, tau, row_list, n_list, row_lo, chunk, plan, plan_info, fail_row,
                           obj_out, ws, ws_bytes, stream, -1, 0.f, 0.f, nullptr, 0, mc_out);
+}
+
+// MFITR item layer on the Schur pair path with the artist-step emission and
+// the per-row artist correction (see AlsParams.emit / corr_*).
+extern "C" int mcf_als_half_step_mfitr_items(const int64_t *ptr, const int32_t *idx,
+                                             const float *val, const float *fixed,
+                                             int64_t n_fixed, float *out, int32_t D, float lam_n,
+                                             float y_shift, const float *tax_S,
+                                             const float *tax_T, float tau,
+                                             const int32_t *row_list, int32_t n_list,
+                                             int32_t chunk, const void *plan,
+                                             const int64_t *plan_info, int64_t *fail_row,
+                                             void *ws, size_t ws_bytes, float bias_lam_n,
+                                             float *emit, const float *corr_tab,
+                                             const int32_t *corr_idx, void *stream) {
+    if (D < 2 || D - 1 > 20 || !emit || (corr_idx && !corr_tab) || getenv("MCF_NO_SCHUR")) {
+        set_error("mcf_als_half_step_mfitr_items: needs the Schur pair path (D + 1 <= 21)");
+        return MCF_E_UNSUPPORTED;
+    }
+    g_emit = emit;
+    g_corr_tab = corr_tab;
+    g_corr_idx = corr_idx;
+    const int rc = half_step_impl(ptr, idx, val, nullptr, fixed, n_fixed, out, D, 0.f, lam_n,
+                                  y_shift, tax_S, tax_T, tau, row_list, n_list, 0, chunk, plan,
+                                  plan_info, fail_row, nullptr, ws, ws_bytes, stream, D - 1, 0.f,
+                                  bias_lam_n);
+    g_emit = nullptr;
+    g_corr_tab = nullptr;
+    g_corr_idx = nullptr;
+    return rc;
+}
+
+extern "C" size_t mcf_mfitr_artist_workspace_bytes(int32_t n_artists) {
+    if (n_artists < 0) return 0;
+    using C = PairGeom<5>;
+    return align_up(sizeof(float) * (size_t)n_artists * C::PSTR_S, 256) +
+           2 * align_up(sizeof(int32_t) * ((size_t)n_artists + 1), 256) + 256;
+}
+
+extern "C" int mcf_mfitr_artist_step(const int64_t *art_ptr, const int32_t *art_items,
+                                     const int32_t *artist_row, int32_t n_artists,
+                                     const int64_t *cnt_ptr, const float *emit, const float *Qa,
+                                     float *Aa, int32_t D, float lam_n, float bias_lam_n,
+                                     int64_t *fail_row, void *ws, size_t ws_bytes,
+                                     void *stream) {
+    if (!art_ptr || !art_items || !artist_row || n_artists < 0 || !cnt_ptr || !emit || !Qa ||
+        !Aa || D < 2 || D - 1 > 20 || !fail_row) {
+        set_error("mcf_mfitr_artist_step: invalid arguments (D + 1 <= 21 bias systems)");
+        return MCF_E_ARG;
+    }
+    if (ws_bytes < mcf_mfitr_artist_workspace_bytes(n_artists)) {
+        set_error("mcf_mfitr_artist_step: workspace too small");
+        return MCF_E_WORKSPACE;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc;
+    if ((rc = cuda_status(cudaMemsetAsync(fail_row, 0xff, sizeof(int64_t), s), "memset"))) return rc;
+    if (n_artists == 0) return MCF_OK;
+    const int Df = D - 1;   // factor coordinates; the bias is column Df
+    const int nb = (Df + 3) / 4, nbk = nb <= 1 ? 1 : nb <= 3 ? 3 : 5;   // as dispatch_pair
+    Carve c(ws, ws_bytes);
+    float *slots = c.take<float>((size_t)n_artists * PairGeom<5>::PSTR_S);
+    int32_t *sorted = c.take<int32_t>((size_t)n_artists + 1);
+    int32_t *hoff = c.take<int32_t>((size_t)n_artists + 1);
+    const int ld = mcf_factor_ld(D);
+    const unsigned rgrid = 148 * 8, hgrid = (unsigned)ceil_div(n_artists, 8);
+    if (nbk == 1)
+        k_mfitr_artist_reduce<1><<<rgrid, 256, 0, s>>>(art_ptr, art_items, n_artists, emit, Qa, ld, Df, slots);
+    else if (nbk == 3)
+        k_mfitr_artist_reduce<3><<<rgrid, 256, 0, s>>>(art_ptr, art_items, n_artists, emit, Qa, ld, Df, slots);
+    else
+        k_mfitr_artist_reduce<5><<<rgrid, 256, 0, s>>>(art_ptr, art_items, n_artists, emit, Qa, ld, Df, slots);
+    k_iota<<<(unsigned)ceil_div((int64_t)n_artists + 1, 256), 256, 0, s>>>(sorted, hoff, n_artists);
+    AlsParams p{};
+    p.ptr = cnt_ptr;
+    p.out = Aa;
+    p.D = Df;
+    p.ld = ld;
+    p.lam_n = lam_n;
+    p.row_list = artist_row;
+    p.n_list = n_artists;
+    p.partials = slots;
+    p.fail = reinterpret_cast<unsigned long long *>(fail_row);
+    p.bias_dim = -1;
+    p.bias_lam_n = bias_lam_n;
+    p.schur = 1;
+    PairPlan q{};
+    q.sorted_j = sorted;
+    q.hoff = hoff;
+    q.n_heavy = n_artists;
+    if (nbk == 1) k_als_heavy<1, true><<<hgrid, 256, 0, s>>>(p, q);
+    else if (nbk == 3) k_als_heavy<3, true><<<hgrid, 256, 0, s>>>(p, q);
+    else k_als_heavy<5, true><<<hgrid, 256, 0, s>>>(p, q);
+    return check_launch("mcf_mfitr_artist_step");
 }

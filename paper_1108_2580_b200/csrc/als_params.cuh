@@ -47,7 +47,16 @@ struct AlsParams {
     // the Gram and eliminates b exactly: (A - u u^T/s) f = c - u d/s,
     // b = (d - u.f)/s, s = n + bias regulariser
     int schur;
+    // MFITR item layers (Schur pair path): every row's [A | c | u | d | n]
+    // (before any correction) is stored to emit[r * EMIT_STRIDE] for the
+    // artist step, and the row's artist terms are removed from its rhs:
+    // c -= A q_a + u b_a, d -= u.q_a + n b_a with [q_a | b_a] =
+    // corr_tab[corr_idx[r]] (corr_idx[r] < 0: none)
+    float *emit;
+    const float *corr_tab;
+    const int32_t *corr_idx;
 };
+constexpr int EMIT_STRIDE = 256;
 
 // one element of row r of the solved shard: local table + every peer replica
 __device__ __forceinline__ void put_out(const AlsParams &p, int r, int i, float v) {

@@ -69,7 +69,8 @@ __device__ __forceinline__ float dot_d(const float *a, const float *b, int D) {
 // per-rating targets of one layout, thread per rating (a warp per row
 // serialised the Zipf-hot rows), ratings in CSR order.
 // mode 0 users (partner i), 1 items (partner u, aux = row item),
-// 2 artists (partner u, aux = item).
+// 2 artists (partner u, aux = item), 3 items without the artist terms (those
+// are applied per row from the Gram in the solve epilogue: y - mu - b_u).
 __global__ void k_mfitr_targets(int mode, const int64_t *ptr, const int32_t *idx,
                                 const float *val, const int32_t *aux, int32_t n_rows,
                                 const float *Pa, const float *Qa, const float *Aa,
@@ -91,6 +92,8 @@ __global__ void k_mfitr_targets(int mode, const int64_t *ptr, const int32_t *idx
                 const float *qa = Aa + (size_t)ar * ld;
                 t -= qa[D] + dot_d(qa, pu, D);
             }
+        } else if (mode == 3) {     // j = user
+            t -= Pa[(size_t)j * ld + D];
         } else {                    // j = user, aux = item
             const float *qi = Qa + (size_t)aux[k] * ld;
             const float *pu = Pa + (size_t)j * ld;
@@ -125,8 +128,9 @@ extern "C" int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t
                                  const float *Pa, const float *Qa, const float *Aa,
                                  const int32_t *art, float mu, int32_t D, float *out,
                                  void *stream) {
-    if (mode < 0 || mode > 2 || !ptr || !out || n_rows < 0 || D < 1 || D + 1 > 128 ||
+    if (mode < 0 || mode > 3 || !ptr || !out || n_rows < 0 || D < 1 || D + 1 > 128 ||
         (mode == 0 && (!Qa || !Aa || !art)) || (mode == 1 && (!Pa || !Aa || !art || !aux)) ||
+        (mode == 3 && !Pa) ||
         (mode == 2 && (!Pa || !Qa || !aux))) {
         set_error("mcf_mfitr_targets: invalid arguments");
         return MCF_E_ARG;

@@ -159,7 +159,7 @@ class LayoutSolver:
               y_shift=0.0, tax_S=None, tax_T=None, tau=0.0, rows=None, rows_key=None, wts=None,
               fail: torch.Tensor | None = None, obj_out: torch.Tensor | None = None,
               val: torch.Tensor | None = None, bias=None, peers: torch.Tensor | None = None,
-              chunk: int | None = None, multicast: int | None = None):
+              chunk: int | None = None, multicast: int | None = None, emit=None):
         """bias = (dim, lam_c, lam_n): coordinate `dim` is a bias with its own
         regulariser (mcf_als_half_step_bias); val: per-rating targets in the
         layout's CSR order instead of the ratings; peers: device int64 tensor
@@ -210,6 +210,17 @@ class LayoutSolver:
                 ptr(tax_T), float(tau), ptr(rl), n_list, 0, chunk, ptr(buf), info, ptr(fail),
                 ptr(obj_out), ptr(ws), ws.numel(), ptr(peers), int(peers.numel()),
                 stream_ptr(dev)), "mcf_als_half_step_peers")
+            return fail
+        if emit is not None:   # MFITR item layer: emitted systems + artist correction
+            if bias is None or wts is not None or lam_c != 0.0 or bias[1] != 0.0:
+                raise ConfigError("emit= needs a bias block without weights or lam_c")
+            e, corr_tab, corr_idx = emit
+            check(_lib.lib().mcf_als_half_step_mfitr_items(
+                ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(fixed), fixed.shape[0], ptr(out),
+                self.D, float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau), ptr(rl),
+                n_list, chunk, ptr(buf), info, ptr(fail), ptr(ws), ws.numel(), float(bias[2]),
+                ptr(e), ptr(corr_tab), ptr(corr_idx), stream_ptr(dev)),
+                "mcf_als_half_step_mfitr_items")
             return fail
         if bias is not None:
             check(_lib.lib().mcf_als_half_step_bias(

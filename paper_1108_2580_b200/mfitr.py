@@ -24,6 +24,7 @@ descent on ``loss_mfitr`` (time terms off) with
 from __future__ import annotations
 
 import dataclasses
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -304,22 +305,53 @@ class MfitrFullSolver:
         self.item_rows = torch.repeat_interleave(torch.arange(I, device=dev, dtype=torch.int32),
                                                  ratings.by_item.degrees())
         self.t_users = torch.empty(ratings.nnz, dtype=torch.float32, device=dev)
-        # artist layout: the records whose item has an artist, keyed by artist,
-        # partner = user, aux = item (records rebuilt from the users layout)
         lay = ratings.by_user
-        rec_u = torch.repeat_interleave(torch.arange(U, device=dev, dtype=torch.int32),
-                                        lay.degrees())
-        rec_i, rec_s = lay.idx, lay.val
-        a_of = self.art[rec_i.long()]
-        has = a_of >= 0
-        hu, hi, hs, ha = rec_u[has], rec_i[has], rec_s[has], a_of[has]
-        self.by_artist = SideLayout(ha.contiguous(), hu.contiguous(), hs.contiguous(), I,
-                                    keep_perm=True)
-        self.art_item = hi[self.by_artist.perm.long()].contiguous()
-        self.t_art = torch.empty(self.by_artist.nnz, dtype=torch.float32, device=dev)
+        # fused item / artist steps (D + 1 <= 21, the Schur pair path): the item
+        # layers emit their row systems and drop the artist terms from their rhs
+        # through their own Gram; the artist block is solved from the emitted
+        # systems (mcf_mfitr_artist_step) -- no per-rating artist passes
+        self.fused = (D + 1 <= 21 and not os.environ.get("MCF_MFITR_LEGACY")
+                      and not os.environ.get("MCF_NO_SCHUR"))
+        has_i = self.art >= 0
+        deg_i = ratings.by_item.degrees()
+        cnt = torch.zeros(I, dtype=torch.int64, device=dev)
+        cnt.index_add_(0, self.art[has_i].long(), deg_i[has_i])
+        self.cnt_a = cnt.double()
+        if self.fused:
+            self.cnt_ptr = torch.zeros(I + 1, dtype=torch.int64, device=dev)
+            self.cnt_ptr[1:] = torch.cumsum(cnt, 0)
+            items = torch.nonzero(has_i).flatten()
+            order = torch.argsort(self.art[items].long(), stable=True)
+            self.art_items = items[order].to(torch.int32).contiguous()
+            arts_sorted = self.art[self.art_items.long()].long()
+            self.artist_row, counts = torch.unique_consecutive(arts_sorted, return_counts=True)
+            self.artist_row = self.artist_row.to(torch.int32).contiguous()
+            self.art_ptr = torch.zeros(self.artist_row.numel() + 1, dtype=torch.int64, device=dev)
+            self.art_ptr[1:] = torch.cumsum(counts, 0)
+            self.emit = torch.zeros(I, 256, dtype=torch.float32, device=dev)
+            # rows of q_a / b_a that are not an artist have no ratings: the
+            # block solve leaves them 0 (the per-rating path does the same)
+            not_artist = torch.ones(I, dtype=torch.bool, device=dev)
+            not_artist[self.artist_row.long()] = False
+            self.not_artist = torch.nonzero(not_artist).flatten()
+            n_art = int(self.artist_row.numel())
+            self.art_ws = torch.empty(max(int(_lib.lib().mcf_mfitr_artist_workspace_bytes(n_art)),
+                                          256), dtype=torch.uint8, device=dev)
+        else:
+            # artist layout: the records whose item has an artist, keyed by
+            # artist, partner = user, aux = item (records rebuilt from the users layout)
+            rec_u = torch.repeat_interleave(torch.arange(U, device=dev, dtype=torch.int32),
+                                            lay.degrees())
+            rec_i, rec_s = lay.idx, lay.val
+            a_of = self.art[rec_i.long()]
+            has = a_of >= 0
+            hu, hi, hs, ha = rec_u[has], rec_i[has], rec_s[has], a_of[has]
+            self.by_artist = SideLayout(ha.contiguous(), hu.contiguous(), hs.contiguous(), I,
+                                        keep_perm=True)
+            self.art_item = hi[self.by_artist.perm.long()].contiguous()
+            self.t_art = torch.empty(self.by_artist.nnz, dtype=torch.float32, device=dev)
         self.cnt_u = lay.degrees().double()
-        self.cnt_i = ratings.by_item.degrees().double()
-        self.cnt_a = self.by_artist.degrees().double()
+        self.cnt_i = deg_i.double()
         # taxonomy
         inc_ptr, inc_edge, inc_other = graph.incident_edges(I)
         self.inc_ptr = torch.as_tensor(inc_ptr, device=dev)
@@ -361,7 +393,7 @@ class MfitrFullSolver:
     def _item_prep(self):
         # [p_u | 1] and the item targets depend only on user / artist blocks
         self._fixed(self.Pa, None, None, self.U, self.Xu)
-        self._targets(1, self.r.by_item, self.item_rows, self.t_items)
+        self._targets(3 if self.fused else 1, self.r.by_item, self.item_rows, self.t_items)
 
     def item_layers(self):
         self._item_prep()
@@ -383,10 +415,21 @@ class MfitrFullSolver:
                                        stream_ptr(self.device)), "mcf_taxonomy_terms")
             self.solver.solve(self.r.by_item, self.Xu, self.Qa, 0.0, h.lam2, 0.0, self.S, self.T,
                               self.tau, rows, ("layer", k), None, self.fail, None,
-                              val=self.t_items, bias=self._bias())
+                              val=self.t_items, bias=self._bias(),
+                              emit=(self.emit, self.Aa, self.art) if self.fused else None)
             self._fold(0)
 
     def artists(self):
+        if self.fused:   # from the item layers' emitted systems
+            check(_lib.lib().mcf_mfitr_artist_step(
+                ptr(self.art_ptr), ptr(self.art_items), ptr(self.artist_row),
+                int(self.artist_row.numel()), ptr(self.cnt_ptr), ptr(self.emit), ptr(self.Qa),
+                ptr(self.Aa), self.D + 1, float(self.hyper.lam2), float(self.hyper.lam1),
+                ptr(self.fail), ptr(self.art_ws), self.art_ws.numel(), stream_ptr(self.device)),
+                "mcf_mfitr_artist_step")
+            self.Aa.index_fill_(0, self.not_artist, 0.0)
+            self._fold(1)
+            return
         self._fixed(self.Pa, None, None, self.U, self.Xu)
         self._targets(2, self.by_artist, self.art_item, self.t_art)
         self.solver.solve(self.by_artist, self.Xu, self.Aa, 0.0, self.hyper.lam2, fail=self.fail,

@@ -41,12 +41,16 @@ mark("items: [p|1] table + targets")
 for k in range(len(s.layers)):
     s._solve_layer(k)
     mark(f"items: layer {k} ({int(s.layers[k].numel())} rows)")
-s._fixed(s.Pa, None, None, s.U, s.Xu)
-mark("artists: [p|1] table")
-s._targets(2, s.by_artist, s.art_item, s.t_art)
-mark(f"artists: targets ({s.by_artist.nnz} ratings)")
-s.solver.solve(s.by_artist, s.Xu, s.Aa, 0.0, h.lam2, fail=s.fail, val=s.t_art, bias=s._bias())
-mark("artists: solve")
+if s.fused:
+    s.artists()
+    mark(f"artists: from the emitted item systems ({int(s.artist_row.numel())} artists)")
+else:
+    s._fixed(s.Pa, None, None, s.U, s.Xu)
+    mark("artists: [p|1] table")
+    s._targets(2, s.by_artist, s.art_item, s.t_art)
+    mark(f"artists: targets ({s.by_artist.nnz} ratings)")
+    s.solver.solve(s.by_artist, s.Xu, s.Aa, 0.0, h.lam2, fail=s.fail, val=s.t_art, bias=s._bias())
+    mark("artists: solve")
 s._fixed(s.Qa, s.Aa, s.art, s.I, s.Xi)
 mark("users: [q+q_a|1] table")
 s._targets(0, r.by_user, None, s.t_users)
