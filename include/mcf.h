@@ -246,28 +246,34 @@ int mcf_mfitr_sgd_epoch_locked(const int64_t *uptr, const int32_t *uidx, const f
  * exactly 2 * workers * iters. */
 int mcf_lock_stress(int32_t *locks, float *acc, int32_t n_items, int32_t workers, int32_t iters,
                     void *stream);
-/* ALS-MFITR every-block sweep, item layers and artists without per-rating
- * artist passes (D = factor dimension + 1 bias, D + 1 <= 21: the Schur pair
- * path).  mcf_als_half_step_mfitr_items = mcf_als_half_step_bias (bias in
- * column D-1, lam_c = 0) that also stores every row's augmented system
- * [A | c | u | d | n] (packed lower A of the D-1 factor coordinates, rhs c,
- * u = sum x, d = sum y, n; EMIT stride 256 floats, row r at emit + 256 r)
- * and removes the row's artist terms from its rhs from its own Gram:
- * c -= A q_a + u b_a, d -= u.q_a + n b_a with [q_a | b_a] =
- * corr_tab[corr_idx[r]] (targets: r - mu - b_u, mcf_mfitr_targets mode 3).
+/* ALS-MFITR every-block sweep without per-rating target passes (D = factor
+ * dimension + 1 bias, D <= 21: the Schur pair path).
+ * mcf_als_half_step_mfitr = mcf_als_half_step_bias (bias in column D-1,
+ * lam_c = 0) plus
+ *  - ysub != 0: the partner rows are [x | 1 | t] (mcf_mfitr_fixed_bsub) and
+ *    each rating's target is val - y_shift - t (items: t = b_u; users:
+ *    t = b_i + b_a[art(i)]; val = the raw ratings, y_shift = mu);
+ *  - emit (nullable): every row's augmented system [A | c | u | d | n]
+ *    (packed lower A of the D-1 factor coordinates, rhs c, u = sum x,
+ *    d = sum y, n; stride 256 floats, row r at emit + 256 r), stored before
+ *  - corr_idx (nullable): the row's artist terms removed from its rhs through
+ *    its own Gram: c -= A q_a + u b_a, d -= u.q_a + n b_a, [q_a | b_a] =
+ *    corr_tab[corr_idx[r]] (corr_idx[r] < 0: none).
  * mcf_mfitr_artist_step then solves every artist's [q_a | b_a] from those
  * systems: A_a = sum_i A_i, rhs_a = sum_i (c_i - G_i [q_i | b_i]) over the
  * artist's items (art_ptr / art_items CSR, fixed order), regularised
  * lam_n n_a (factors) and bias_lam_n n_a (bias), n_a = cnt_ptr[r+1] -
  * cnt_ptr[r] for the artist's row r = artist_row[j]; results into Aa. */
-int mcf_als_half_step_mfitr_items(const int64_t *ptr, const int32_t *idx, const float *val,
-                                  const float *fixed, int64_t n_fixed, float *out, int32_t D,
-                                  float lam_n, float y_shift, const float *tax_S,
-                                  const float *tax_T, float tau, const int32_t *row_list,
-                                  int32_t n_list, int32_t chunk, const void *plan,
-                                  const int64_t *plan_info, int64_t *fail_row, void *ws,
-                                  size_t ws_bytes, float bias_lam_n, float *emit,
-                                  const float *corr_tab, const int32_t *corr_idx, void *stream);
+int mcf_mfitr_fixed_bsub(const float *main_t, const float *add_t, const int32_t *art, int64_t n,
+                         int32_t D, float *out, void *stream);
+int mcf_als_half_step_mfitr(const int64_t *ptr, const int32_t *idx, const float *val,
+                            const float *fixed, int64_t n_fixed, float *out, int32_t D,
+                            float lam_n, float y_shift, const float *tax_S, const float *tax_T,
+                            float tau, const int32_t *row_list, int32_t n_list, int32_t chunk,
+                            const void *plan, const int64_t *plan_info, int64_t *fail_row,
+                            void *ws, size_t ws_bytes, float bias_lam_n, float *emit,
+                            const float *corr_tab, const int32_t *corr_idx, int32_t ysub,
+                            void *stream);
 size_t mcf_mfitr_artist_workspace_bytes(int32_t n_artists);
 int mcf_mfitr_artist_step(const int64_t *art_ptr, const int32_t *art_items,
                           const int32_t *artist_row, int32_t n_artists, const int64_t *cnt_ptr,

@@ -59,9 +59,10 @@ SIGNATURES = {
                                            c_f32, c_i32, c_f32, c_f32, c_f32, vp, vp, vp, c_i64,
                                            c_f32, c_f32, c_i32, vp, vp]),
     "mcf_lock_stress": (c_int, [vp, vp, c_i32, c_i32, c_i32, vp]),
-    "mcf_als_half_step_mfitr_items": (c_int, [vp, vp, vp, vp, c_i64, vp, c_i32, c_f32, c_f32, vp,
-                                              vp, c_f32, vp, c_i32, c_i32, vp, vp, vp, vp, c_size,
-                                              c_f32, vp, vp, vp, vp]),
+    "mcf_als_half_step_mfitr": (c_int, [vp, vp, vp, vp, c_i64, vp, c_i32, c_f32, c_f32, vp, vp,
+                                        c_f32, vp, c_i32, c_i32, vp, vp, vp, vp, c_size, c_f32, vp,
+                                        vp, vp, c_i32, vp]),
+    "mcf_mfitr_fixed_bsub": (c_int, [vp, vp, vp, c_i64, c_i32, vp, vp]),
     "mcf_mfitr_artist_workspace_bytes": (c_size, [c_i32]),
     "mcf_mfitr_artist_step": (c_int, [vp, vp, vp, c_i32, vp, vp, vp, vp, c_i32, c_f32, c_f32, vp,
                                       vp, c_size, vp]),

@@ -1325,13 +1325,14 @@ __host__ __device__ constexpr int slot_units(int u) {
     return (u % 8 == 2 || u % 8 == 6) ? u : slot_units(u + 1);
 }
 
-template <int NBK, int R_>
+template <int NBK, int R_, bool YSUB_ = false>
 struct PairCfg : PairGeom<NBK> {
     using G = PairGeom<NBK>;
     static constexpr int LDK = G::LDK;
     static constexpr int R = R_;                   // ratings per pipeline stage per pair
-    // pair slot of one stage: R partner rows | R ratings | R weights
-    static constexpr int RROW = LDK;
+    // pair slot of one stage: R partner rows | R ratings | R weights; with
+    // YSUB the partner rows carry one more 16-byte block (the y subtrahend)
+    static constexpr int RROW = LDK + (YSUB_ ? 4 : 0);
     static constexpr int YOFF = R * RROW;
     static constexpr int WOFF = YOFF + R;
     static constexpr int SLOT = 4 * slot_units((WOFF + R + 3) / 4);   // floats
@@ -1663,10 +1664,10 @@ struct PairAcc {
 // s+NS-1 is issued -- no register ever waits on an in-flight load.
 // L2 policy: the once-read idx/val/weight streams are loaded evict_first,
 // so they do not push the fixed factor rows (50-80 MB at config 1) out of L2.
-template <int NBK, int R, bool HAS_W, bool FULLBLK, bool SCHUR = false>
-__global__ void __launch_bounds__(PairCfg<NBK, R>::WARPS * 32, PairCfg<NBK, R>::MIN_CTAS)
+template <int NBK, int R, bool HAS_W, bool FULLBLK, bool SCHUR = false, bool YSUB = false>
+__global__ void __launch_bounds__(PairCfg<NBK, R, YSUB>::WARPS * 32, PairCfg<NBK, R, YSUB>::MIN_CTAS)
 k_als_pair(AlsParams p, PairPlan q) {
-    using C = PairCfg<NBK, R>;
+    using C = PairCfg<NBK, R, YSUB>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long bars[C::WARPS][C::NS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1682,6 +1683,7 @@ k_als_pair(AlsParams p, PairPlan q) {
     const int *ring_ids = reinterpret_cast<const int *>(wbase + C::RING_AREA) + pair * C::IDSTR;
     const unsigned ring_ids_s = wbase_s + C::RING_AREA + pair * C::IDSTR * 4;
     const int nb_real = FULLBLK ? NBK : (p.D + 3) / 4;
+    const int ysub_blk = YSUB ? (p.D + 1) >> 2 : -1;   // the block holding the y subtrahend
     int boff[NBK];   // float offset of register block b inside a row
 #pragma unroll
     for (int b = 0; b < NBK; ++b) boff[b] = 4 * ((b + h) % NBK);
@@ -1740,10 +1742,10 @@ k_als_pair(AlsParams p, PairPlan q) {
                 // lanes h = 0, 1 copy adjacent 16-byte blocks in one instruction
                 // (one 32-byte sector when the row is sector-aligned)
 #pragma unroll
-                for (int b = h; b < NBK; b += 2)
+                for (int b = h; b < NBK + (YSUB ? 1 : 0); b += 2)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
                                  ::"r"(rs + 16 * b), "l"(src + 4 * b),
-                                 "r"((ok && (FULLBLK || b < nb_real)) ? 16 : 0));
+                                 "r"((ok && (FULLBLK || b < nb_real || b == ysub_blk)) ? 16 : 0));
             }
             // lane h brings the ratings (and weights) of rows h, h+2, ... and
             // the partner ids of the same rows of stage s + NS - 1
@@ -1789,7 +1791,11 @@ k_als_pair(AlsParams p, PairPlan q) {
                 float4 xr[NBK];
 #pragma unroll
                 for (int b = 0; b < NBK; ++b) xr[b] = *reinterpret_cast<const float4 *>(rw + boff[b]);
-                const float y = ys[r] - p.y_shift;
+                float y = ys[r] - p.y_shift;
+                if constexpr (YSUB) y -= rw[p.D + 1];   // [x | 1 | subtrahend] partner rows
+                // padding past the task end: zero rows, and zero targets (the Schur
+                // bias sums d = sum y, so a shifted pad value would leak into it)
+                if constexpr (SCHUR) y = R * t + r < n ? y : 0.f;
                 float4 xa[NBK];
 #pragma unroll
                 for (int b = 0; b < NBK; ++b) xa[b] = xr[b];
@@ -2292,26 +2298,26 @@ PlanLayout carve_plan(void *buf, size_t cap, int32_t n_list, int64_t nnz, int32_
 
 bool use_pair(int D) { return D <= 20; }
 
-template <int NBK, int R, bool W, bool FB, bool SC = false>
+template <int NBK, int R, bool W, bool FB, bool SC = false, bool YS = false>
 int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
-    using C = PairCfg<NBK, R>;
+    using C = PairCfg<NBK, R, YS>;
     const size_t smem = (size_t)C::WARP_BYTES * C::WARPS;
 
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_als_pair<NBK, R, W, FB, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_als_pair<NBK, R, W, FB, SC, YS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, R, W, FB, SC>, C::WARPS * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_pair<NBK, R, W, FB, SC, YS>, C::WARPS * 32,
                                                   smem);
     const int64_t groups = ceil_div(q.n_tasks, C::PAIRS);
     const int64_t want = ceil_div(groups, C::WARPS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_pair<NBK, R, W, FB, SC><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
+    if (grid > 0) k_als_pair<NBK, R, W, FB, SC, YS><<<(unsigned)grid, C::WARPS * 32, smem, s>>>(p, q);
     if (q.n_heavy > 0)
         k_als_heavy<NBK, SC><<<(unsigned)ceil_div(q.n_heavy, 8), 256, 0, s>>>(p, q);
     if (p.obj_partial) k_obj_sum<<<1, 256, 0, s>>>(p.obj_partial, p.obj_groups + q.n_heavy, q.obj_out);
@@ -2321,6 +2327,11 @@ int launch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
 template <bool W>
 int dispatch_pair(const AlsParams &p, const PairPlan &q, cudaStream_t s) {
     const int nb = (p.D + 3) / 4;
+    if (p.schur && p.ysub) {   // ... with [x | 1 | subtrahend] partner rows
+        if (nb <= 1) return launch_pair<1, 4, false, false, true, true>(p, q, s);
+        if (nb <= 3) return launch_pair<3, 4, false, false, true, true>(p, q, s);
+        return launch_pair<5, 4, false, false, true, true>(p, q, s);
+    }
     if (p.schur) {   // [f | b] rows with the bias eliminated in the epilogue (no weights)
         if (nb <= 1) return launch_pair<1, 4, false, false, true>(p, q, s);
         if (nb <= 3) return launch_pair<3, 4, false, false, true>(p, q, s);
@@ -2444,6 +2455,7 @@ extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t
 static thread_local float *g_emit = nullptr;
 static thread_local const float *g_corr_tab = nullptr;
 static thread_local const int32_t *g_corr_idx = nullptr;
+static thread_local int g_ysub = 0;
 
 static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *val,
                           const float *wts, const float *fixed, int64_t n_fixed, float *out,
@@ -2499,7 +2511,8 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
     p.emit = g_emit;
     p.corr_tab = g_corr_tab;
     p.corr_idx = g_corr_idx;
-    if ((p.emit || p.corr_idx) && !p.schur) {
+    p.ysub = g_ysub;
+    if ((p.emit || p.corr_idx || p.ysub) && !p.schur) {
         set_error("mcf_als_half_step_mfitr_items: the row systems did not take the Schur pair path");
         return MCF_E_UNSUPPORTED;
     }
@@ -2652,26 +2665,26 @@ extern "C" int mcf_als_half_step_multicast(const int64_t *ptr, const int32_t *id
                           obj_out, ws, ws_bytes, stream, -1, 0.f, 0.f, nullptr, 0, mc_out);
 }
 
-// MFITR item layer on the Schur pair path with the artist-step emission and
-// the per-row artist correction (see AlsParams.emit / corr_*).
-extern "C" int mcf_als_half_step_mfitr_items(const int64_t *ptr, const int32_t *idx,
-                                             const float *val, const float *fixed,
-                                             int64_t n_fixed, float *out, int32_t D, float lam_n,
-                                             float y_shift, const float *tax_S,
-                                             const float *tax_T, float tau,
-                                             const int32_t *row_list, int32_t n_list,
-                                             int32_t chunk, const void *plan,
-                                             const int64_t *plan_info, int64_t *fail_row,
-                                             void *ws, size_t ws_bytes, float bias_lam_n,
-                                             float *emit, const float *corr_tab,
-                                             const int32_t *corr_idx, void *stream) {
-    if (D < 2 || D - 1 > 20 || !emit || (corr_idx && !corr_tab) || getenv("MCF_NO_SCHUR")) {
-        set_error("mcf_als_half_step_mfitr_items: needs the Schur pair path (D + 1 <= 21)");
+// MFITR block on the Schur pair path (bias last, D - 1 <= 20, no weights):
+// optional emission of the row systems + artist correction (item layers),
+// optional y subtrahend in column D of the partner rows (ysub).
+extern "C" int mcf_als_half_step_mfitr(const int64_t *ptr, const int32_t *idx, const float *val,
+                                       const float *fixed, int64_t n_fixed, float *out, int32_t D,
+                                       float lam_n, float y_shift, const float *tax_S,
+                                       const float *tax_T, float tau, const int32_t *row_list,
+                                       int32_t n_list, int32_t chunk, const void *plan,
+                                       const int64_t *plan_info, int64_t *fail_row, void *ws,
+                                       size_t ws_bytes, float bias_lam_n, float *emit,
+                                       const float *corr_tab, const int32_t *corr_idx,
+                                       int32_t ysub, void *stream) {
+    if (D < 2 || D - 1 > 20 || (corr_idx && !corr_tab) || getenv("MCF_NO_SCHUR")) {
+        set_error("mcf_als_half_step_mfitr: needs the Schur pair path (D <= 21)");
         return MCF_E_UNSUPPORTED;
     }
     g_emit = emit;
     g_corr_tab = corr_tab;
     g_corr_idx = corr_idx;
+    g_ysub = ysub ? 1 : 0;
     const int rc = half_step_impl(ptr, idx, val, nullptr, fixed, n_fixed, out, D, 0.f, lam_n,
                                   y_shift, tax_S, tax_T, tau, row_list, n_list, 0, chunk, plan,
                                   plan_info, fail_row, nullptr, ws, ws_bytes, stream, D - 1, 0.f,
@@ -2679,6 +2692,7 @@ extern "C" int mcf_als_half_step_mfitr_items(const int64_t *ptr, const int32_t *
     g_emit = nullptr;
     g_corr_tab = nullptr;
     g_corr_idx = nullptr;
+    g_ysub = 0;
     return rc;
 }
 

@@ -55,6 +55,9 @@ struct AlsParams {
     float *emit;
     const float *corr_tab;
     const int32_t *corr_idx;
+    // pair Schur path: partner rows [x | 1 | t], the rating's target is
+    // y - y_shift - t (the per-rating MFITR bias terms folded into the gather)
+    int ysub;
 };
 constexpr int EMIT_STRIDE = 256;
 

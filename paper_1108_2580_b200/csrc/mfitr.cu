@@ -20,9 +20,11 @@
 namespace mcf {
 namespace {
 
-// out[r] = [main[r][:D] + (art[r] >= 0 ? add[art[r]][:D] : 0) | 1 | 0 ...]
+// out[r] = [main[r][:D] + (art[r] >= 0 ? add[art[r]][:D] : 0) | 1 | t | 0 ...] with
+// t = main[r][D] + (art[r] >= 0 ? add[art[r]][D] : 0) when bsub (the block's
+// per-rating bias subtrahend, read by the pair kernel's YSUB gather), else 0
 __global__ void k_mfitr_fixed(const float *main_t, const float *add_t, const int32_t *art,
-                              int64_t n, int D, int ld, float *out) {
+                              int64_t n, int D, int ld, float *out, int bsub) {
     const int64_t total = n * ld;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -37,6 +39,12 @@ __global__ void k_mfitr_fixed(const float *main_t, const float *add_t, const int
             }
         } else if (c == D) {
             v = 1.f;
+        } else if (c == D + 1 && bsub) {
+            v = main_t[r * ld + D];
+            if (add_t && art) {
+                const int a = art[r];
+                if (a >= 0) v += add_t[(size_t)a * ld + D];
+            }
         }
         out[e] = v;
     }
@@ -119,8 +127,23 @@ extern "C" int mcf_mfitr_fixed(const float *main_t, const float *add_t, const in
     if (total == 0) return MCF_OK;
     const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 32);
     k_mfitr_fixed<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(main_t, add_t, art, n, D,
-                                                                       ld, out);
+                                                                       ld, out, 0);
     return check_launch("mcf_mfitr_fixed");
+}
+
+extern "C" int mcf_mfitr_fixed_bsub(const float *main_t, const float *add_t, const int32_t *art,
+                                    int64_t n, int32_t D, float *out, void *stream) {
+    if (!main_t || !out || n < 0 || D < 1 || D + 2 > mcf_factor_ld(D + 1)) {
+        set_error("mcf_mfitr_fixed_bsub: invalid arguments (needs a spare column D + 1)");
+        return MCF_E_ARG;
+    }
+    const int ld = mcf_factor_ld(D + 1);
+    const int64_t total = n * ld;
+    if (total == 0) return MCF_OK;
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 32);
+    k_mfitr_fixed<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(main_t, add_t, art, n, D,
+                                                                       ld, out, 1);
+    return check_launch("mcf_mfitr_fixed_bsub");
 }
 
 extern "C" int mcf_mfitr_targets(int32_t mode, const int64_t *ptr, const int32_t *idx,

@@ -211,16 +211,16 @@ class LayoutSolver:
                 ptr(obj_out), ptr(ws), ws.numel(), ptr(peers), int(peers.numel()),
                 stream_ptr(dev)), "mcf_als_half_step_peers")
             return fail
-        if emit is not None:   # MFITR item layer: emitted systems + artist correction
+        if emit is not None:   # MFITR block: (emit, corr_tab, corr_idx, ysub), Schur pair path
             if bias is None or wts is not None or lam_c != 0.0 or bias[1] != 0.0:
                 raise ConfigError("emit= needs a bias block without weights or lam_c")
-            e, corr_tab, corr_idx = emit
-            check(_lib.lib().mcf_als_half_step_mfitr_items(
+            e, corr_tab, corr_idx, ysub = emit
+            check(_lib.lib().mcf_als_half_step_mfitr(
                 ptr(lay.ptr), ptr(lay.idx), ptr(vals), ptr(fixed), fixed.shape[0], ptr(out),
                 self.D, float(lam_n), float(y_shift), ptr(tax_S), ptr(tax_T), float(tau), ptr(rl),
                 n_list, chunk, ptr(buf), info, ptr(fail), ptr(ws), ws.numel(), float(bias[2]),
-                ptr(e), ptr(corr_tab), ptr(corr_idx), stream_ptr(dev)),
-                "mcf_als_half_step_mfitr_items")
+                ptr(e), ptr(corr_tab), ptr(corr_idx), int(bool(ysub)), stream_ptr(dev)),
+                "mcf_als_half_step_mfitr")
             return fail
         if bias is not None:
             check(_lib.lib().mcf_als_half_step_bias(

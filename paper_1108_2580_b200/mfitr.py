@@ -390,10 +390,17 @@ class MfitrFullSolver:
                                            ptr(self.Aa), ptr(self.art), self.mu, self.D, ptr(out),
                                            stream_ptr(self.device)), "mcf_mfitr_targets")
 
+    def _fixed_bsub(self, main, add, art, n, out):
+        check(_lib.lib().mcf_mfitr_fixed_bsub(ptr(main), ptr(add), ptr(art), n, self.D, ptr(out),
+                                              stream_ptr(self.device)), "mcf_mfitr_fixed_bsub")
+
     def _item_prep(self):
         # [p_u | 1] and the item targets depend only on user / artist blocks
+        if self.fused:   # [p_u | 1 | b_u]: the targets are formed in the solve's gather
+            self._fixed_bsub(self.Pa, None, None, self.U, self.Xu)
+            return
         self._fixed(self.Pa, None, None, self.U, self.Xu)
-        self._targets(3 if self.fused else 1, self.r.by_item, self.item_rows, self.t_items)
+        self._targets(1, self.r.by_item, self.item_rows, self.t_items)
 
     def item_layers(self):
         self._item_prep()
@@ -413,10 +420,14 @@ class MfitrFullSolver:
                                        ptr(self.w), ptr(self.Qa), self.I, self.D + 1, ptr(rows),
                                        rows.numel(), ptr(self.S), ptr(self.T),
                                        stream_ptr(self.device)), "mcf_taxonomy_terms")
-            self.solver.solve(self.r.by_item, self.Xu, self.Qa, 0.0, h.lam2, 0.0, self.S, self.T,
-                              self.tau, rows, ("layer", k), None, self.fail, None,
-                              val=self.t_items, bias=self._bias(),
-                              emit=(self.emit, self.Aa, self.art) if self.fused else None)
+            if self.fused:   # raw ratings - mu - b_u (gather); artist terms from the Gram
+                self.solver.solve(self.r.by_item, self.Xu, self.Qa, 0.0, h.lam2, self.mu, self.S,
+                                  self.T, self.tau, rows, ("layer", k), None, self.fail, None,
+                                  bias=self._bias(), emit=(self.emit, self.Aa, self.art, True))
+            else:
+                self.solver.solve(self.r.by_item, self.Xu, self.Qa, 0.0, h.lam2, 0.0, self.S,
+                                  self.T, self.tau, rows, ("layer", k), None, self.fail, None,
+                                  val=self.t_items, bias=self._bias())
             self._fold(0)
 
     def artists(self):
@@ -437,6 +448,12 @@ class MfitrFullSolver:
         self._fold(1)
 
     def users(self):
+        if self.fused:   # [q_i + q_a | 1 | b_i + b_a]: targets formed in the gather
+            self._fixed_bsub(self.Qa, self.Aa, self.art, self.I, self.Xi)
+            self.solver.solve(self.r.by_user, self.Xi, self.Pa, 0.0, self.hyper.lam2, self.mu,
+                              fail=self.fail, bias=self._bias(), emit=(None, None, None, True))
+            self._fold(2)
+            return
         self._fixed(self.Qa, self.Aa, self.art, self.I, self.Xi)
         self._targets(0, self.r.by_user, None, self.t_users)
         self.solver.solve(self.r.by_user, self.Xi, self.Pa, 0.0, self.hyper.lam2, fail=self.fail,

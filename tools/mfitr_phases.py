@@ -51,12 +51,16 @@ else:
     mark(f"artists: targets ({s.by_artist.nnz} ratings)")
     s.solver.solve(s.by_artist, s.Xu, s.Aa, 0.0, h.lam2, fail=s.fail, val=s.t_art, bias=s._bias())
     mark("artists: solve")
-s._fixed(s.Qa, s.Aa, s.art, s.I, s.Xi)
-mark("users: [q+q_a|1] table")
-s._targets(0, r.by_user, None, s.t_users)
-mark("users: targets")
-s.solver.solve(r.by_user, s.Xi, s.Pa, 0.0, h.lam2, fail=s.fail, val=s.t_users, bias=s._bias())
-mark("users: solve")
+if s.fused:
+    s.users()
+    mark("users: [q+q_a|1|b_i+b_a] table + solve")
+else:
+    s._fixed(s.Qa, s.Aa, s.art, s.I, s.Xi)
+    mark("users: [q+q_a|1] table")
+    s._targets(0, r.by_user, None, s.t_users)
+    mark("users: targets")
+    s.solver.solve(r.by_user, s.Xi, s.Pa, 0.0, h.lam2, fail=s.fail, val=s.t_users, bias=s._bias())
+    mark("users: solve")
 torch.cuda.synchronize()
 s.check()
 tot = marks[0][1].elapsed_time(marks[-1][1])
