@@ -113,13 +113,17 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes (or ~10 ms pass) instead of returning every few hundred
+// cycles -- a polling loop of bare try_waits issued ~60 times per wait and
+// took issue slots from the other warps of its SM sub-partition
 __device__ __forceinline__ bool mbar_try(unsigned bar, unsigned parity) {
     unsigned ok;
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; "
         "selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(10000000u)
         : "memory");
     return ok != 0;
 }

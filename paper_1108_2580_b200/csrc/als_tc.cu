@@ -261,12 +261,6 @@ __device__ __forceinline__ void lds16(const float *p, float (&v)[16]) {
     }
 }
 
-// Triangular solve with the packed lower factor L (smem, row r at r(r+1)/2)
-// by one warp, lane l holding rows l, l + 32, l + 64, l + 96 of the
-// right-hand side zr.  8 unknowns per step: their right-hand sides are
-// shuffled to every lane, each lane solves the 8 x 8 diagonal block
-// redundantly (rdiag = 1 / L_ii), then updates its own rows.
-//   UPPER: L^T x = z, x -> out[128];   else L z = r, z -> zr (in place).
 // the per-call scales (powers of two, see the header comment)
 __device__ __forceinline__ void tc_scales(const AlsParams &p, const TcWs &w, float &s, float &sy) {
     const float xmax = __uint_as_float(w.scal[0]), ymax = __uint_as_float(w.scal[1]);
@@ -308,6 +302,12 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr, uint32_t lbo, uin
     return sdesc(addr, lbo, sbo) | (2ull << 61);
 }
 
+// Triangular solve with the packed lower factor L (smem, row r at r(r+1)/2)
+// by one warp, lane l holding rows l, l + 32, l + 64, l + 96 of the
+// right-hand side zr.  8 unknowns per step: their right-hand sides are
+// shuffled to every lane, each lane solves the 8 x 8 diagonal block
+// redundantly (rdiag = 1 / L_ii), then updates its own rows.
+//   UPPER: L^T x = z, x -> out[128];   else L z = r, z -> zr (in place).
 template <int DP, bool UPPER>
 __device__ __forceinline__ void warp_trsv(float (&zr)[4], const float *Ls, const float *rdiag,
                                           int lane, float *out, int dim = DP) {
@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(512, 1)
     unsigned cph = 0;                          // Cholesky barrier phase
     long long tcp_t = clock64();
     unsigned long long tcp_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tcp_fl[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #define TCP(k)                                                       \
     do {                                                             \
         if (w.prof && m == 0) {                                      \
@@ -473,6 +474,16 @@ __global__ void __launch_bounds__(512, 1)
             tcp_acc[k] += (unsigned long long)(t1_ - tcp_t);         \
             tcp_t = t1_;                                             \
         }                                                            \
+    } while (0)
+#define TCP_FLUSH(cls)                                                        \
+    do {                                                                      \
+        if (w.prof && m == 0) {                                               \
+            for (int k_ = 0; k_ < 10; ++k_) {                                 \
+                atomicAdd(w.prof + 16 + 16 * (cls) + k_, tcp_acc[k_] - tcp_fl[k_]); \
+                tcp_fl[k_] = tcp_acc[k_];                                     \
+            }                                                                 \
+            atomicAdd(w.prof + 16 + 16 * (cls) + 10, 1ull);                   \
+        }                                                                     \
     } while (0)
 
     for (;;) {
@@ -506,10 +517,10 @@ __global__ void __launch_bounds__(512, 1)
         if (!dual) {
 
         // ---------------- Gram: C = H H^T + H L^T + L H^T, rhs = (H + L) [y_h y_l].
-        // Warp 0 drives an NST-stage ring: per 16-rating stage 4 * 2 * NA TMA
-        // tile::gather4 of split rows (SWIZZLE_128B -> the MN-major canonical
-        // layout), lanes 0-15 write the rating tile, lane 0 issues the MMAs of
-        // the oldest landed stage and commits them to the stage's empty barrier.
+        // An NST-stage smem ring of 16-rating stages (split rows of the fixed
+        // table + the rating tile), filled by the whole team (below); thread 0
+        // issues the MMAs of the oldest landed stage and commits them to the
+        // stage's empty barrier.
         const int nst = (n + 15) >> 4;
         if (nst == 0) {   // taxonomy-only row: zero accumulator
             float zr[16];
@@ -532,18 +543,16 @@ __global__ void __launch_bounds__(512, 1)
             // chunks past DP only feed Gram rows / columns >= DP (never read): not copied
             const bool chunk_ok = cc < DP / 8;
             const __half *tsrc = tab ? w.tl : w.th;
-            int idn[4];
-            float yv = 0.f;   // thread m < 16: rating m of the prefetched stage
-            auto load_ids = [&](int t, int (&ids)[4]) {
+            // rating ids and values run two stages ahead of the copies (their
+            // loads miss L2 every other stage; one stage of cover exposed them)
+            // (clamped addresses, raw values: nothing consumes a load before
+            // its stage is issued)
+            auto load_ids = [&](int t, int (&ids)[4], float &yv) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int kr = 16 * t + 4 * wq + j;
-                    ids[j] = kr < n ? __ldg(p.idx + k0 + kr) : -1;
-                }
-                const int kr = 16 * t + m;
-                yv = (m < 16 && kr < n) ? __ldg(p.val + k0 + kr) - p.y_shift : 0.f;
+                for (int j = 0; j < 4; ++j) ids[j] = __ldg(p.idx + k0 + min(16 * t + 4 * wq + j, n - 1));
+                yv = __ldg(p.val + k0 + min(16 * t + (m & 15), n - 1));
             };
-            auto issue = [&](int t, const int (&ids)[4]) {   // stage t -> slot (gst + t) % NST
+            auto issue = [&](int t, const int (&ids)[4], float yv) {   // stage t -> slot (gst + t) % NST
                 const unsigned g = gst + (unsigned)t, b = g % NST;
                 if (g >= NST) warp_mbar_wait(ebar0 + 8 * b, ((g / NST) - 1) & 1);
                 unsigned char *st = tb + b * C::STAGE;
@@ -553,35 +562,43 @@ __global__ void __launch_bounds__(512, 1)
                     const int kk = 4 * wq + j, r = kk & 7;
                     const uint32_t dst = sts + tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 +
                                          r * 128 + ((c8 ^ r) << 4);
-                    const bool ok = chunk_ok && ids[j] >= 0;
-                    const __half *src = tsrc + (size_t)(ok ? ids[j] : 0) * C::TW + 8 * cc;
+                    const bool ok = chunk_ok && 16 * t + kk < n;
+                    const __half *src = tsrc + (size_t)ids[j] * C::TW + 8 * cc;
                     if (chunk_ok)
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
                                      "r"(ok ? 16 : 0));
                 }
                 if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l)
                     uint32_t yh, yl;
-                    split2(yv * sy, 0.f, yh, yl);
+                    split2(16 * t + m < n ? (yv - p.y_shift) * sy : 0.f, 0.f, yh, yl);
                     *reinterpret_cast<uint32_t *>(st + 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16) =
                         (yh & 0xffffu) | (yl << 16);
                 }
                 asm volatile("cp.async.commit_group;\n" ::: "memory");
             };
-            for (int t = 0; t < LEAD; ++t) {   // prologue (empty groups past the end)
-                if (t < nst) {
-                    int ids[4];
-                    load_ids(t, ids);
-                    issue(t, ids);
-                } else {
-                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+            {   // prologue: every id load first, then the copies (empty groups past the end)
+                int ids0[LEAD][4];
+                float y0[LEAD];
+#pragma unroll
+                for (int t = 0; t < LEAD; ++t) load_ids(t, ids0[t], y0[t]);
+#pragma unroll
+                for (int t = 0; t < LEAD; ++t) {
+                    if (t < nst) issue(t, ids0[t], y0[t]);
+                    else asm volatile("cp.async.commit_group;\n" ::: "memory");
                 }
             }
-            if (LEAD < nst) load_ids(LEAD, idn);
+            int idn[4], idn2[4];
+            float yn = 0.f, yn2 = 0.f;
+            load_ids(LEAD, idn, yn);
+            load_ids(LEAD + 1, idn2, yn2);
             for (int st = 0; st < nst; ++st) {
                 const int t = st + LEAD;
                 if (t < nst) {
-                    issue(t, idn);
-                    if (t + 1 < nst) load_ids(t + 1, idn);
+                    issue(t, idn, yn);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) idn[j] = idn2[j];
+                    yn = yn2;
+                    if (t + 2 < nst) load_ids(t + 2, idn2, yn2);
                 } else {
                     asm volatile("cp.async.commit_group;\n" ::: "memory");
                 }
@@ -678,7 +695,11 @@ __global__ void __launch_bounds__(512, 1)
             const int nch = (int)((nrow + p.chunk - 1) / p.chunk);
             if (m == 0) team_flag[team] = atomicAdd(w.hot_count + s0, 1) == nch - 1;
             team_bar(team);
-            if (!team_flag[team]) continue;
+            if (!team_flag[team]) {
+                TCP(2);
+                TCP_FLUSH(3);
+                continue;
+            }
             __threadfence();
 #pragma unroll 1
             for (int c = 0; c <= NBLK; ++c) {
@@ -885,11 +906,8 @@ __global__ void __launch_bounds__(512, 1)
         }
         TCP(5);
 
-        // ---------------- triangular solves by warp 0 (L from smem), 4 unknowns
-        // per step: their right-hand sides are shuffled to every lane, each lane
-        // solves the 4 x 4 diagonal block redundantly, then updates its own rows
-        // (lane l holds rows l, l + 32, l + 64, l + 96); result -> xbuf
-        auto back_sub = [&](float (&zr)[4]) { warp_trsv<DP, true>(zr, Ls, rdiag, lane, xbuf, dim); };
+        // ---------------- back substitution L^T x = z by warp 0 (L from smem), 8
+        // unknowns per step; x -> xbuf
         team_bar(team);
         if (wq == 0) {
             float zr[4];
@@ -898,7 +916,7 @@ __global__ void __launch_bounds__(512, 1)
                 const int mq = lane + 32 * q4;
                 zr[q4] = mq < dim ? zbuf[mq] : 0.f;
             }
-            back_sub(zr);
+            warp_trsv<DP, true>(zr, Ls, rdiag, lane, xbuf, dim);
         }
         team_bar(team);
         TCP(6);
@@ -1037,7 +1055,9 @@ __global__ void __launch_bounds__(512, 1)
             put_out(p, row, m, m < D ? xo : 0.f);
         }
         TCP(8);
+        TCP_FLUSH(dual ? 0 : slot >= 0 ? 3 : nrow < D ? 1 : 2);
     }
+#undef TCP_FLUSH
 #undef TCP
     if (w.prof && m == 0)
         for (int k = 0; k < 10; ++k) atomicAdd(w.prof + k, tcp_acc[k]);
@@ -1148,8 +1168,8 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     w.team_limit = getenv("MCF_TC_TEAMS") ? atoi(getenv("MCF_TC_TEAMS")) : 4;
     if (getenv("MCF_TC_PROF")) {
         static unsigned long long *buf = nullptr;
-        if (!buf) cudaMalloc(&buf, 16 * sizeof(unsigned long long));
-        cudaMemset(buf, 0, 16 * sizeof(unsigned long long));
+        if (!buf) cudaMalloc(&buf, 80 * sizeof(unsigned long long));
+        cudaMemset(buf, 0, 80 * sizeof(unsigned long long));
         w.prof = buf;
         g_tc_prof = buf;
     }
@@ -1177,6 +1197,16 @@ extern "C" int mcf_tc_prof_read(unsigned long long *out10) {
     if (!mcf::g_tc_prof) return -1;
     cudaDeviceSynchronize();
     cudaMemcpy(out10, mcf::g_tc_prof, 14 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    cudaMemset(mcf::g_tc_prof, 0, 16 * sizeof(unsigned long long));
+    cudaMemset(mcf::g_tc_prof, 0, 80 * sizeof(unsigned long long));
+    return 0;
+}
+
+// the same counters per task class (16 each: 10 phases, [10] = tasks):
+// 0 dual rows, 1 primal rows with n < D (refined), 2 primal rows, 3 hot chunks
+extern "C" int mcf_tc_prof_read_classes(unsigned long long *out64) {
+    if (!mcf::g_tc_prof) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out64, mcf::g_tc_prof + 16, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(mcf::g_tc_prof, 0, 80 * sizeof(unsigned long long));
     return 0;
 }
