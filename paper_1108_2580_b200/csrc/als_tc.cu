@@ -434,7 +434,8 @@ __global__ void __launch_bounds__(512, 1)
     for (int e = threadIdx.x; e < (C::SMEM - 1024) / 16; e += blockDim.x)
         reinterpret_cast<uint4 *>(smem)[e] = make_uint4(0u, 0u, 0u, 0u);
     if (m == 0) {
-        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 128);   // full: team arrivals
+        // full: 128 cp.async completion arrivals + 16 rating-tile writers
+        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 144);
         for (int st = NST; st <= 2 * NST; ++st) mbar_init(fbar0 + 8 * st, 1);   // empty, chol: commits
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -464,6 +465,9 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t id_rhs = idesc(16, true, false);
     unsigned gst = 0;                          // Gram stages issued by this team
     unsigned cph = 0;                          // Cholesky barrier phase
+    // phase cycle counters (tools/tc_phases*.py): compiled in only with
+    // MCF_TC_PROFILE (tools/variant.sh); the product build carries none
+#ifdef MCF_TC_PROFILE
     long long tcp_t = clock64();
     unsigned long long tcp_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tcp_fl[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -485,6 +489,14 @@ __global__ void __launch_bounds__(512, 1)
             atomicAdd(w.prof + 16 + 16 * (cls) + 10, 1ull);                   \
         }                                                                     \
     } while (0)
+#else
+#define TCP(k) \
+    do {       \
+    } while (0)
+#define TCP_FLUSH(cls) \
+    do {               \
+    } while (0)
+#endif
 
     for (;;) {
         if (team >= w.team_limit) break;
@@ -534,15 +546,23 @@ __global__ void __launch_bounds__(512, 1)
             // Team-wide cp.async pipeline over the split tables: per stage each
             // warp copies 4 ratings' rows, a lane per 16-byte chunk (lanes 0-15
             // the h row, 16-31 the l row), straight into the SWIZZLE_128B
-            // MN-major tiles (chunk index XOR row-in-atom); LEAD stages of copies
-            // and MMA_DEPTH stages of MMAs in flight.  Each thread waits for its
-            // own copies, fences them to the async proxy and arrives on the
-            // stage's full barrier (128 arrivals); thread 0 issues the MMAs.
+            // MN-major tiles (chunk index XOR row-in-atom).  Completion is
+            // tracked by the stage's full barrier (cp.async.mbarrier.arrive:
+            // nobody waits for its own copies); a thread only waits when the
+            // slot it refills still feeds MMAs.  Thread 0 issues the MMAs of
+            // the stage LEAD behind the newest and commits them to the stage's
+            // empty barrier.
             constexpr int LEAD = NST - C::MMA_DEPTH;
             const int tab = lane >> 4, cc = lane & 15, at = cc >> 3, c8 = cc & 7;
             // chunks past DP only feed Gram rows / columns >= DP (never read): not copied
             const bool chunk_ok = cc < DP / 8;
-            const __half *tsrc = tab ? w.tl : w.th;
+            const __half *tsrc = (tab ? w.tl : w.th) + 8 * cc;
+            uint32_t doff[4];   // smem offsets of this thread's 4 chunks in a stage
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int kk = 4 * wq + j, r = kk & 7;
+                doff[j] = tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 + r * 128 + ((c8 ^ r) << 4);
+            }
             // rating ids and values run two stages ahead of the copies (their
             // loads miss L2 every other stage; one stage of cover exposed them)
             // (clamped addresses, raw values: nothing consumes a load before
@@ -555,37 +575,33 @@ __global__ void __launch_bounds__(512, 1)
             auto issue = [&](int t, const int (&ids)[4], float yv) {   // stage t -> slot (gst + t) % NST
                 const unsigned g = gst + (unsigned)t, b = g % NST;
                 if (g >= NST) warp_mbar_wait(ebar0 + 8 * b, ((g / NST) - 1) & 1);
-                unsigned char *st = tb + b * C::STAGE;
                 const uint32_t sts = tbs + b * C::STAGE;
+                if (chunk_ok) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int kk = 4 * wq + j, r = kk & 7;
-                    const uint32_t dst = sts + tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 +
-                                         r * 128 + ((c8 ^ r) << 4);
-                    const bool ok = chunk_ok && 16 * t + kk < n;
-                    const __half *src = tsrc + (size_t)ids[j] * C::TW + 8 * cc;
-                    if (chunk_ok)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
-                                     "r"(ok ? 16 : 0));
+                    for (int j = 0; j < 4; ++j)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sts + doff[j]),
+                                     "l"(tsrc + (size_t)ids[j] * C::TW),
+                                     "r"(16 * t + 4 * wq + j < n ? 16 : 0));
                 }
-                if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l)
+                if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l), generic stores
                     uint32_t yh, yl;
                     split2(16 * t + m < n ? (yv - p.y_shift) * sy : 0.f, 0.f, yh, yl);
-                    *reinterpret_cast<uint32_t *>(st + 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16) =
-                        (yh & 0xffffu) | (yl << 16);
+                    *reinterpret_cast<uint32_t *>(tb + b * C::STAGE + 2 * C::HT + (m >> 3) * 256 +
+                                                  (m & 7) * 16) = (yh & 0xffffu) | (yl << 16);
+                    proxy_fence();
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fbar0 + 8 * b) : "memory");
                 }
-                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar0 + 8 * b)
+                             : "memory");
             };
-            {   // prologue: every id load first, then the copies (empty groups past the end)
+            {   // prologue: every id load first, then the copies
                 int ids0[LEAD][4];
                 float y0[LEAD];
 #pragma unroll
                 for (int t = 0; t < LEAD; ++t) load_ids(t, ids0[t], y0[t]);
 #pragma unroll
-                for (int t = 0; t < LEAD; ++t) {
+                for (int t = 0; t < LEAD; ++t)
                     if (t < nst) issue(t, ids0[t], y0[t]);
-                    else asm volatile("cp.async.commit_group;\n" ::: "memory");
-                }
             }
             int idn[4], idn2[4];
             float yn = 0.f, yn2 = 0.f;
@@ -599,16 +615,10 @@ __global__ void __launch_bounds__(512, 1)
                     for (int j = 0; j < 4; ++j) idn[j] = idn2[j];
                     yn = yn2;
                     if (t + 2 < nst) load_ids(t + 2, idn2, yn2);
-                } else {
-                    asm volatile("cp.async.commit_group;\n" ::: "memory");
                 }
-                // this thread's copies of stage st are the (LEAD+1)-th newest group
-                asm volatile("cp.async.wait_group %0;\n" ::"n"(LEAD) : "memory");
-                proxy_fence();
-                const unsigned g = gst + (unsigned)st, b = g % NST;
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fbar0 + 8 * b) : "memory");
                 if (m == 0) {
-                    mbar_wait(fbar0 + 8 * b, (g / NST) & 1);   // all 128 threads' copies landed
+                    const unsigned g = gst + (unsigned)st, b = g % NST;
+                    mbar_wait(fbar0 + 8 * b, (g / NST) & 1);   // every copy + the rating tile landed
                     tc_fence_after();
                     const uint32_t ha = tbs + b * C::STAGE;
                     const uint64_t dh = sdesc_sw128(ha, 1024, C::NA * 1024);
@@ -623,7 +633,6 @@ __global__ void __launch_bounds__(512, 1)
                     umma_commit(ebar0 + 8 * b);
                 }
             }
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
             const unsigned gl = gst + (unsigned)nst - 1;
             warp_mbar_wait(ebar0 + 8 * (gl % NST), (gl / NST) & 1);   // last MMAs done
         }
@@ -669,6 +678,16 @@ __global__ void __launch_bounds__(512, 1)
             warp_mbar_wait(cbar, cph);
             cph ^= 1u;
             tc_fence_after();
+            // the n fp32 rows (x = X^T alpha and the refinement) into the tile
+            // region, free once the MMAs above completed; they land during the
+            // Cholesky (n * ld floats <= DUAL_MAX * DP = the two tiles)
+            const int ld4 = p.ld >> 2;
+            for (int e = m; e < n * ld4; e += 128) {
+                const int r = e / ld4, c = e - r * ld4;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dx + (uint32_t)e * 16),
+                             "l"(p.fixed + (size_t)ids[r] * p.ld + 4 * c));
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
         TCP(1);
 
@@ -758,9 +777,7 @@ __global__ void __launch_bounds__(512, 1)
             float a[16];
             if (32 * wq + 31 >= c0) tmem_ld16(tl + c0, a);
             if (wq == dw) {
-                const long long dt0 = clock64();
                 tmem_wait_ld();
-                const long long dt1 = clock64();
                 float fa[16], fr = inblk ? r : 0.f;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) fa[i] = inblk ? a[i] + (i == ime ? rg : 0.f) : 0.f;
@@ -786,7 +803,6 @@ __global__ void __launch_bounds__(512, 1)
                     const float frn = fmaf(-t, rv, fr);
                     fr = ime > i ? frn : fr;
                 }
-                const long long dt2 = clock64();
                 bool ok = true;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) ok = ok && piv[i] > 0.f && piv[i] < 3.0e38f;
@@ -921,19 +937,23 @@ __global__ void __launch_bounds__(512, 1)
         team_bar(team);
         TCP(6);
         float xo = (m < DP ? xbuf[m] : 0.f) * out_scale;
-        if (dual) {   // x = out_scale (s X)^T alpha' from the tiles
+        if (dual) {   // x = out_scale s X^T alpha' from the prefetched fp32 rows
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            team_bar(team);
+            const float *rows = reinterpret_cast<const float *>(tb + C::OFF_DX);
+            const int ld = p.ld;
             float acc = 0.f;
             if (m < D) {
-                const unsigned char *Ht = tb + C::OFF_DX, *Lt = Ht + C::DTILE;
-                const int base = (m >> 3) * C::DLBO + (m & 7) * 2;
-                for (int rr = 0; rr < n; ++rr) {
-                    const int off = base + (rr >> 3) * 128 + (rr & 7) * 16;
-                    const float v = __half2float(*reinterpret_cast<const __half *>(Ht + off)) +
-                                    __half2float(*reinterpret_cast<const __half *>(Lt + off));
-                    acc = fmaf(xbuf[rr], v, acc);
+                float acc1 = 0.f;
+                int rr = 0;
+                for (; rr + 1 < n; rr += 2) {
+                    acc = fmaf(xbuf[rr], rows[rr * ld + m], acc);
+                    acc1 = fmaf(xbuf[rr + 1], rows[(rr + 1) * ld + m], acc1);
                 }
+                if (rr < n) acc = fmaf(xbuf[rr], rows[rr * ld + m], acc);
+                acc += acc1;
             }
-            xo = acc * out_scale;
+            xo = acc * (s * out_scale);
             // one refinement step in the dual space: rho_r = y_r - x_r.x - lam alpha_r,
             // alpha += (X X^T + lam I)^{-1} rho, x += X^T (that correction)
             const float alpha_m = m < n ? xbuf[m] * (s2 / sy) : 0.f;
@@ -945,11 +965,10 @@ __global__ void __launch_bounds__(512, 1)
             if (m < dim) {
                 float rh = 0.f;
                 if (m < n) {
-                    const int id = __ldg(p.idx + k0 + m);
-                    const float4 *xr4 = reinterpret_cast<const float4 *>(p.fixed + (size_t)id * p.ld);
+                    const float4 *xr4 = reinterpret_cast<const float4 *>(rows + m * ld);
                     float d0 = 0.f, d1 = 0.f;
-                    for (int c4 = 0; c4 < p.ld / 4; ++c4) {
-                        const float4 u = __ldg(xr4 + c4);
+                    for (int c4 = 0; c4 < ld / 4; ++c4) {
+                        const float4 u = xr4[c4];
                         const float4 xv = *reinterpret_cast<const float4 *>(zbuf + 4 * c4);
                         d0 = fmaf(u.x, xv.x, d0); d1 = fmaf(u.y, xv.y, d1);
                         d0 = fmaf(u.z, xv.z, d0); d1 = fmaf(u.w, xv.w, d1);
@@ -972,12 +991,14 @@ __global__ void __launch_bounds__(512, 1)
             }
             team_bar(team);
             if (m < D) {   // x += X^T (s^2 w)
-                float acc2 = 0.f;
-                for (int rr = 0; rr < n; ++rr) {
-                    const int id = __ldg(p.idx + k0 + rr);
-                    acc2 = fmaf(xbuf[rr], __ldg(p.fixed + (size_t)id * p.ld + m), acc2);
+                float acc2 = 0.f, acc3 = 0.f;
+                int rr = 0;
+                for (; rr + 1 < n; rr += 2) {
+                    acc2 = fmaf(xbuf[rr], rows[rr * ld + m], acc2);
+                    acc3 = fmaf(xbuf[rr + 1], rows[(rr + 1) * ld + m], acc3);
                 }
-                xo = fmaf(s2, acc2, xo);
+                if (rr < n) acc2 = fmaf(xbuf[rr], rows[rr * ld + m], acc2);
+                xo = fmaf(s2, acc2 + acc3, xo);
             }
         }
         // ---------------- one step of iterative refinement for short rows
@@ -1059,8 +1080,10 @@ __global__ void __launch_bounds__(512, 1)
     }
 #undef TCP_FLUSH
 #undef TCP
+#ifdef MCF_TC_PROFILE
     if (w.prof && m == 0)
         for (int k = 0; k < 10; ++k) atomicAdd(w.prof + k, tcp_acc[k]);
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {

@@ -2,7 +2,7 @@
 per half-step and per task class (dual rows, primal rows with n < D, primal
 rows, hot chunks) the clock64 phase counters summed over teams, as a share
 of all team-cycles and as cycles per task.  MCF_TC_PROF=1.  GPU box only.
-    python tools/tc_phases_cfg.py [cfg]"""
+    MCF_TC_PROFILE=1 tools/variant.sh prof -e "" && MCF_LIB=build/var_prof.so python tools/tc_phases_cfg.py [cfg]"""
 import ctypes
 import os
 import sys
