@@ -94,9 +94,11 @@ int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t n_list, in
  * Grams at dimension D (slots = max(plan_info[3], plan_info[1])).
  * _fixed: also room for the tensor-core path (64 <= D <= 128, no
  * observation weights) -- its fp16 split tables of the n_fixed-row fixed
- * side; with the plain query that path falls back to the CUDA-core kernels. */
+ * side and the split ratings of the layout's nnz (plan_info[5]); with the
+ * plain query that path falls back to the CUDA-core kernels. */
 size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D);
-size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, int32_t D, int64_t n_fixed);
+size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, int32_t D, int64_t n_fixed,
+                                     int64_t nnz);
 
 /* Solve every planned row r exactly (Cholesky of the D x D system):
  *   A_r = sum_k w_k x_k x_k^T + (lam_c + lam_n * n_r + tau * S_r) I

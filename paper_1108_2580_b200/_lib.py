@@ -30,7 +30,7 @@ SIGNATURES = {
     "mcf_als_plan": (c_int, [vp, vp, c_i32, c_i32, c_i32, c_i64, vp, c_size,
                              ctypes.POINTER(c_i64), vp]),
     "mcf_als_workspace_bytes": (c_size, [c_i32, c_i64, c_i32]),
-    "mcf_als_workspace_bytes_fixed": (c_size, [c_i32, c_i64, c_i32, c_i64]),
+    "mcf_als_workspace_bytes_fixed": (c_size, [c_i32, c_i64, c_i32, c_i64, c_i64]),
     "mcf_als_half_step": (c_int, [vp, vp, vp, vp, vp, c_i64, vp, c_i32, c_f32, c_f32, c_f32, vp, vp,
                                   c_f32, vp, c_i32, c_i32, c_i32, vp, ctypes.POINTER(c_i64), vp,
                                   vp, vp, c_size, vp]),

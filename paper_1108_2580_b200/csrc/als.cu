@@ -2430,8 +2430,8 @@ extern "C" int mcf_als_plan(const int64_t *ptr, const int32_t *row_list, int32_t
 }
 
 extern "C" size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, int32_t D,
-                                                int64_t n_fixed) {
-    if (D < 1 || n_list < 0 || slots < 0 || n_fixed < 0) return 0;
+                                                int64_t n_fixed, int64_t nnz) {
+    if (D < 1 || n_list < 0 || slots < 0 || n_fixed < 0 || nnz < 0) return 0;
     size_t per = use_pair(D) ? pair_gram(D) : pstride_of(D);
     if (D >= 2 && D - 1 <= 20) {   // a bias-last system may run as D - 1 + Schur (+ u, d)
         const int nb = (D - 1 + 3) / 4;
@@ -2440,14 +2440,14 @@ extern "C" size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, i
     }
     const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
     size_t part = sizeof(float) * (size_t)slots * per;
-    if (D >= 64 && D <= 128 && n_fixed > 0) part = std::max(part, tc_workspace_bytes(D, slots, n_fixed));
+    if (D >= 64 && D <= 128 && n_fixed > 0) part = std::max(part, tc_workspace_bytes(D, slots, n_fixed, nnz));
     return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) + part;
 }
 
 // without the fixed-table size the tensor-core path has no room for its
 // split tables: the CUDA-core kernels run (same results to the tolerance)
 extern "C" size_t mcf_als_workspace_bytes(int32_t n_list, int64_t slots, int32_t D) {
-    return mcf_als_workspace_bytes_fixed(n_list, slots, D, 0);
+    return mcf_als_workspace_bytes_fixed(n_list, slots, D, 0, 0);
 }
 
 // MFITR item-layer extras for the next half_step_impl call (set by
@@ -2546,7 +2546,7 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
     // the tensor-core path (64 <= D <= 128, no weights) when the workspace holds
     // its split tables (mcf_als_workspace_bytes_fixed), else the CUDA-core kernels
     const bool use_tc = tc_path(p.D, wts != nullptr) && !p.schur &&
-                        ws_bytes >= fixed_part + tc_workspace_bytes(p.D, plan_info[3], n_fixed);
+                        ws_bytes >= fixed_part + tc_workspace_bytes(p.D, plan_info[3], n_fixed, plan_info[5]);
     {   // the partial-Gram slots of the hot-row chunks must fit too
         size_t per;
         if (p.schur) {
@@ -2596,7 +2596,7 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         q.n_heavy = plan_info[4];
         q.group_counter = p.counters + n_list;
         if (q.n_tasks == 0) return MCF_OK;
-        return launch_als_tc(p, q, p.partials, ws_bytes - fixed_part, plan_info[3], s);
+        return launch_als_tc(p, q, p.partials, ws_bytes - fixed_part, plan_info[3], plan_info[5], s);
     }
     if (total_items == 0) return MCF_OK;
     return wts ? dispatch<true>(p, s) : dispatch<false>(p, s);

@@ -3,37 +3,35 @@
 // persistent kernel, the system never leaving the SM.
 //
 // Replaces _kernels.als_solve_rows (reference _kernels.py:151-215) for
-// 21 <= D <= 127 without per-observation weights; same plan, same
+// 64 <= D <= 128 without per-observation weights; same plan, same
 // arithmetic contract as als.cu:
 //     A_r = sum_k x_k x_k^T + (lam_c + lam_n n_r + tau S_r) I,
 //     b_r = sum_k (y_k - y_shift) x_k + tau T_r,   out_r = A_r^{-1} b_r.
 //
-// Team = 4 warps (128 threads = the 128 TMEM lanes); 4 teams per CTA, each
-// owning DP = round_up(D + 1, 16) TMEM columns: the augmented system
-// [x | y] [x | y]^T of its current row lives in TMEM (lane m = row m).
-//
-// * Gram: 16 ratings per stage.  The team gathers the partner rows (fp32,
-//   16-byte loads, prefetched one stage ahead, ids two ahead), scales them
-//   by a power of two s (ratings by s_y) and splits every value into fp16
-//   h + l (22 significant bits); the rating rides in column D.  Tiles H and
-//   L2 = 2 l are stored MN-major (no swizzle: 8 ratings x 16 B core
-//   matrices), exactly as gathered -- no transpose.  One thread issues
-//       C' += H H^T + H L2^T      (tcgen05.mma kind::f16, M 128, N DP, K 16)
-//   so that (C'[i][j] + C'[j][i]) / 2 = sum (h_i h_j + h_i l_j + l_i h_j):
-//   fp32-class products from two MMAs (the dropped l l^T term is ~2^-22).
-// * Cholesky: right-looking, 16-column blocks.  Per block the panel is read
-//   from TMEM (tcgen05.ld), symmetrised against the block rows (C' + C'^T)/2,
-//   regularised (lam_c + lam_n n + tau S, scaled), the 16 x 16 diagonal block
-//   factorised by 16 lanes (MUFU.RSQ pivots, the reference's > 0 and finite
-//   test), the panel solved by every row thread, written back to TMEM (L),
-//   split into fp16 h / 2 l K-major tiles, and the trailing update
-//       C' -= P_h P_h^T + P_h (2 P_l)^T
-//   issued as two negated MMAs on the trailing columns only.  The rating
-//   row D is factorised with the rest: its L entries are z = L^{-1} b (the
-//   forward substitution rides along).
-// * Back substitution L^T x = z by 16-row blocks (L read back from TMEM),
-//   rescaled by s / s_y, stored like every other path (put_out).
-// * Hot rows (more than `chunk` ratings): every chunk dumps its C' to a
+// Team = 4 warps (128 threads = the 128 TMEM lanes, thread m = row m of the
+// system); 4 teams per CTA, each owning DP + 16 TMEM columns (Gram | rhs),
+// DP = round_up(D, 16).  Per half-step the fixed table is split once into
+// fp16 tables s x = h + l (k_tc_split, 22 significant bits, s a power of two)
+// and the layout's ratings into (y_h, y_l) pairs.
+// * Gram (rows with n > 64 or n >= D): 16 ratings per stage in a 5-slot smem
+//   ring; the team copies the partner rows' split chunks with 16-byte
+//   cp.async straight into SWIZZLE_128B MN-major tiles (and the ratings with
+//   4-byte cp.async into an N = 16 tile); the stage's full mbarrier counts
+//   the copies' completions, thread 0 issues C += H H^T + H L^T + L H^T and
+//   rhs += (H + L) [y_h y_l] (tcgen05.mma kind::f16, M 128, fp32 in TMEM)
+//   and commits them to the slot's empty barrier.
+// * Dual form (n <= 64 < D, no taxonomy / bias term): (X X^T + lam I)
+//   alpha = y from K-major tiles of the n gathered rows, x = X^T alpha from
+//   the fp32 rows (prefetched into the dead tiles during the Cholesky).
+// * Cholesky: right-looking, 16-column blocks, unscaled.  Per block the
+//   diagonal block is factorised by 16 lanes of one warp (the reference's
+//   > 0 and finite pivot test) with the forward substitution fused, the
+//   panel solved by every row thread (L packed in smem), split into fp16
+//   h / l K-major tiles, and the trailing update issued as three negated
+//   MMAs on the trailing columns.  Back substitution by one warp.
+// * Rows with n < D: one step of iterative refinement from the ratings
+//   (the rank-deficient Gram's fp32 rounding exceeds 1e-4 otherwise).
+// * Hot rows (more than `chunk` ratings): every chunk dumps its C | rhs to a
 //   workspace slot; the last chunk to finish sums the slots in chunk order
 //   (deterministic) into TMEM (tcgen05.st) and solves.
 //
@@ -41,8 +39,6 @@
 // every scaled diagonal entry stays below 2^30: all panel values then fit
 // fp16 (|L_ij| <= sqrt(A_ii) < 2^15) and the result is exact rescaling.
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -52,11 +48,12 @@
 #include "als_params.cuh"
 #include "../../include/mcf.h"
 
+#ifndef TC_DIAG_SMEM
+#define TC_DIAG_SMEM 1   // diagonal-block broadcasts: 1 smem (measured faster), 0 shuffles
+#endif
+
 namespace mcf {
 namespace {
-
-constexpr int TC_TEAMS = 4;   // teams (4 warps each) per CTA
-constexpr int TC_NST = 2;     // Gram pipeline stages per team
 
 __host__ __device__ constexpr int tc_pow2_cols(int c) {
     return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -110,6 +107,7 @@ struct TcWs {
     unsigned long long *prof;   // phase cycle counters (MCF_TC_PROF) or null
     int team_limit;             // teams per CTA that take work (MCF_TC_TEAMS, experiments)
     __half *th, *tl;            // split fixed table: s*x = h + l, [n_fixed][TW] fp16
+    uint32_t *ysp;              // split ratings s_y (y - y_shift) = h + l, (h | l << 16) [nnz]
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -273,7 +271,7 @@ __device__ __forceinline__ void tc_scales(const AlsParams &p, const TcWs &w, flo
 
 // fixed table -> fp16 split tables (s*x = h + l), zero beyond D: the TMA
 // gathers of the Gram read these rows
-__global__ void k_tc_split(AlsParams p, TcWs w, int TW) {
+__global__ void k_tc_split(AlsParams p, PairPlan q, TcWs w, int TW) {
     float s, sy;
     tc_scales(p, w, s, sy);
     const int64_t n = p.n_fixed * (int64_t)(TW / 2);
@@ -288,16 +286,21 @@ __global__ void k_tc_split(AlsParams p, TcWs w, int TW) {
         reinterpret_cast<uint32_t *>(w.th)[e] = h;
         reinterpret_cast<uint32_t *>(w.tl)[e] = l;
     }
+    // the planned ratings (a warp per task), at their CSR positions: the
+    // Gram's rating tiles are 4-byte copies of these
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < q.n_tasks; t += nw) {
+        const int64_t k0 = q.task_k0[t];
+        const int nt = q.task_n[t];
+        for (int i = lane; i < nt; i += 32) {
+            uint32_t h, l;
+            split2((__ldg(p.val + k0 + i) - p.y_shift) * sy, 0.f, h, l);
+            w.ysp[k0 + i] = (h & 0xffffu) | (l << 16);
+        }
+    }
 }
 
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int col, int r0,
-                                            int r1, int r2, int r3, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-        : "memory");
-}
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     return sdesc(addr, lbo, sbo) | (2ull << 61);
 }
@@ -405,8 +408,7 @@ __device__ __noinline__ void trsv_back(float4 z, const float *Ls, const float *r
 
 template <int NBLK>
 __global__ void __launch_bounds__(512, 1)
-    k_als_tc(AlsParams p, PairPlan q, TcWs w, const __grid_constant__ CUtensorMap map_h,
-             const __grid_constant__ CUtensorMap map_l) {
+    k_als_tc(AlsParams p, PairPlan q, TcWs w) {
     using C = TcCfg<NBLK>;
     constexpr int DP = C::DP, NST = C::NST;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -434,8 +436,8 @@ __global__ void __launch_bounds__(512, 1)
     for (int e = threadIdx.x; e < (C::SMEM - 1024) / 16; e += blockDim.x)
         reinterpret_cast<uint4 *>(smem)[e] = make_uint4(0u, 0u, 0u, 0u);
     if (m == 0) {
-        // full: 128 cp.async completion arrivals + 16 rating-tile writers
-        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 144);
+        // full: the team's 128 cp.async completion arrivals
+        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 128);
         for (int st = NST; st <= 2 * NST; ++st) mbar_init(fbar0 + 8 * st, 1);   // empty, chol: commits
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -444,10 +446,6 @@ __global__ void __launch_bounds__(512, 1)
                          smem_u32(&tmem_base_sh)),
                      "r"(C::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (threadIdx.x == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_h) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_l) : "memory");
     }
     proxy_fence();
     tc_fence_before();
@@ -563,16 +561,15 @@ __global__ void __launch_bounds__(512, 1)
                 const int kk = 4 * wq + j, r = kk & 7;
                 doff[j] = tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 + r * 128 + ((c8 ^ r) << 4);
             }
-            // rating ids and values run two stages ahead of the copies (their
-            // loads miss L2 every other stage; one stage of cover exposed them)
-            // (clamped addresses, raw values: nothing consumes a load before
-            // its stage is issued)
-            auto load_ids = [&](int t, int (&ids)[4], float &yv) {
+            // rating ids run two stages ahead of the copies (their loads miss
+            // L2 every other stage; one stage of cover exposed them; clamped
+            // addresses: nothing consumes a load before its stage is issued)
+            auto load_ids = [&](int t, int (&ids)[4]) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) ids[j] = __ldg(p.idx + k0 + min(16 * t + 4 * wq + j, n - 1));
-                yv = __ldg(p.val + k0 + min(16 * t + (m & 15), n - 1));
             };
-            auto issue = [&](int t, const int (&ids)[4], float yv) {   // stage t -> slot (gst + t) % NST
+            const uint32_t *ysrc = w.ysp + k0;
+            auto issue = [&](int t, const int (&ids)[4]) {   // stage t -> slot (gst + t) % NST
                 const unsigned g = gst + (unsigned)t, b = g % NST;
                 if (g >= NST) warp_mbar_wait(ebar0 + 8 * b, ((g / NST) - 1) & 1);
                 const uint32_t sts = tbs + b * C::STAGE;
@@ -583,38 +580,31 @@ __global__ void __launch_bounds__(512, 1)
                                      "l"(tsrc + (size_t)ids[j] * C::TW),
                                      "r"(16 * t + 4 * wq + j < n ? 16 : 0));
                 }
-                if (m < 16) {   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l), generic stores
-                    uint32_t yh, yl;
-                    split2(16 * t + m < n ? (yv - p.y_shift) * sy : 0.f, 0.f, yh, yl);
-                    *reinterpret_cast<uint32_t *>(tb + b * C::STAGE + 2 * C::HT + (m >> 3) * 256 +
-                                                  (m & 7) * 16) = (yh & 0xffffu) | (yl << 16);
-                    proxy_fence();
-                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fbar0 + 8 * b) : "memory");
-                }
+                if (m < 16)   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l); columns 2..15 are never read
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                                     sts + 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16),
+                                 "l"(ysrc + min(16 * t + m, n - 1)), "r"(16 * t + m < n ? 4 : 0));
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar0 + 8 * b)
                              : "memory");
             };
             {   // prologue: every id load first, then the copies
                 int ids0[LEAD][4];
-                float y0[LEAD];
 #pragma unroll
-                for (int t = 0; t < LEAD; ++t) load_ids(t, ids0[t], y0[t]);
+                for (int t = 0; t < LEAD; ++t) load_ids(t, ids0[t]);
 #pragma unroll
                 for (int t = 0; t < LEAD; ++t)
-                    if (t < nst) issue(t, ids0[t], y0[t]);
+                    if (t < nst) issue(t, ids0[t]);
             }
             int idn[4], idn2[4];
-            float yn = 0.f, yn2 = 0.f;
-            load_ids(LEAD, idn, yn);
-            load_ids(LEAD + 1, idn2, yn2);
+            load_ids(LEAD, idn);
+            load_ids(LEAD + 1, idn2);
             for (int st = 0; st < nst; ++st) {
                 const int t = st + LEAD;
                 if (t < nst) {
-                    issue(t, idn, yn);
+                    issue(t, idn);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) idn[j] = idn2[j];
-                    yn = yn2;
-                    if (t + 2 < nst) load_ids(t + 2, idn2, yn2);
+                    if (t + 2 < nst) load_ids(t + 2, idn2);
                 }
                 if (m == 0) {
                     const unsigned g = gst + (unsigned)st, b = g % NST;
@@ -768,6 +758,7 @@ __global__ void __launch_bounds__(512, 1)
             if (m < D && p.tax_T && m != p.bias_dim)
                 r = fmaf(ssy * p.tau, p.tax_T[(size_t)row * p.ld + m], r);
         }
+        if (m < DP) zbuf[m] = rg;   // read by the diagonal warp of m's block
         bool failed = false;
 #pragma unroll 1
         for (int J = 0; J < nblk; ++J) {
@@ -777,60 +768,85 @@ __global__ void __launch_bounds__(512, 1)
             float a[16];
             if (32 * wq + 31 >= c0) tmem_ld16(tl + c0, a);
             if (wq == dw) {
+#ifdef MCF_TC_PROFILE
+                const long long dg0 = clock64();
+#endif
                 tmem_wait_ld();
-                float fa[16], fr = inblk ? r : 0.f;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) fa[i] = inblk ? a[i] + (i == ime ? rg : 0.f) : 0.f;
+#ifdef MCF_TC_PROFILE
+                const long long dg1 = clock64();
+#endif
+                // the block rows' regularisers (written to zbuf by these lanes
+                // before the loop; their z values replace them below)
+                __syncwarp();
+                float rgv[16];
+                lds16(zbuf + c0, rgv);
+                float fr = inblk ? r : 0.f;
+                const int iml = inblk ? ime : -1;   // lanes outside the block keep their rows
                 // right-looking on the unscaled Schur complement: a_mj -= a_mi a_ij / p_i
-                // (rows above the pivot are finished; their upper entries are never read)
-                float piv[16], ri[16];
+                // (the regulariser only enters the pivots; rows at or above the
+                // pivot get t = 0, their entries right of it are never read)
+                float ri[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    float lj[16];
-                    piv[i] = __shfl_sync(FULL, fa[i], lo + i);
+                    float lj[16], pv, rv;
+#if TC_DIAG_SMEM
+                    float *bb = Ljj + 32 * (i & 1);   // broadcast scratch (Ljj is written below)
+                    if (inblk) {
+                        bb[ime] = a[i];
+                        bb[16 + ime] = fr;
+                    }
+                    __syncwarp();
+                    lds16(bb, lj);
+                    pv = lj[i] + rgv[i];
+                    rv = bb[16 + i];
+#else
+                    pv = __shfl_sync(FULL, a[i], lo + i) + rgv[i];
 #pragma unroll
-                    for (int j = i + 1; j < 16; ++j) lj[j] = __shfl_sync(FULL, fa[i], lo + j);
-                    const float rv = __shfl_sync(FULL, fr, lo + i);
-                    const float t = fa[i] * rcp_approx(piv[i]);
-                    ri[i] = rsqrtf(piv[i]);   // off the pivot chain
+                    for (int j = i + 1; j < 16; ++j) lj[j] = __shfl_sync(FULL, a[i], lo + j);
+                    rv = __shfl_sync(FULL, fr, lo + i);
+#endif
+                    const float t = iml > i ? a[i] * rcp_approx(pv) : 0.f;
+                    ri[i] = rsqrtf(pv);   // off the pivot chain
                     int j = i + 1;
-                    if (j & 1) {
-                        fa[j] = fmaf(-t, lj[j], fa[j]);
+                    if (j & 1 && j < 16) {
+                        a[j] = fmaf(-t, lj[j], a[j]);
                         ++j;
                     }
 #pragma unroll
-                    for (; j < 16; j += 2) ffma2(fa[j], fa[j + 1], -t, lj[j], lj[j + 1]);
-                    const float frn = fmaf(-t, rv, fr);
-                    fr = ime > i ? frn : fr;
+                    for (; j < 16; j += 2) ffma2(a[j], a[j + 1], -t, lj[j], lj[j + 1]);
+                    fr = fmaf(-t, rv, fr);
                 }
-                bool ok = true;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) ok = ok && piv[i] > 0.f && piv[i] < 3.0e38f;
-                if (inblk) {   // L row = a_mi / sqrt(p_i) (i < m), sqrt(p_m); z_m = r / sqrt(p_m)
-                    float zm = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float sc = fa[i] * ri[i], dg = piv[i] * ri[i];
-                        fa[i] = i < ime ? sc : (i == ime ? dg : fa[i]);
-                        zm = i == ime ? fr * ri[i] : zm;
-                    }
-                    const int mr = c0 + ime;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) Ljj[j * 16 + ime] = fa[j];   // column-major
-                    float *Lr = Ls + mr * (mr + 1) / 2 + c0;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j <= ime) Lr[j] = fa[j];
-                    zbuf[mr] = zm;
-                }
+                // the reference's pivot test (> 0 and finite) <=> 1 / sqrt(p) in (0, inf)
                 if (lane == 0) {
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4)
                         reinterpret_cast<float4 *>(rdiag + c0)[q4] =
                             make_float4(ri[4 * q4], ri[4 * q4 + 1], ri[4 * q4 + 2], ri[4 * q4 + 3]);
-                    team_flag[team] = !ok;
                 }
-
+                __syncwarp();
+                const float myri = inblk ? rdiag[c0 + ime] : 1.f;
+                const bool bad = __any_sync(FULL, !(myri > 0.f && myri < INFINITY));
+                if (inblk) {   // L row = a_mi / sqrt(p_i) (i < m; the diagonal is never read); z_m = r / sqrt(p_m)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) a[i] *= ri[i];
+                    const int mr = c0 + ime;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) Ljj[j * 16 + ime] = a[j];   // column-major
+                    float *Lr = Ls + mr * (mr + 1) / 2 + c0;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j <= ime) Lr[j] = a[j];
+                    zbuf[mr] = fr * myri;
+                }
+                if (lane == 0) team_flag[team] = bad;
+#ifdef MCF_TC_PROFILE
+                if (w.prof && lane == 0) {   // diagonal warp: TMEM load wait, factorisation
+                    const long long dg2 = clock64();
+                    atomicAdd(w.prof + 11, (unsigned long long)(dg1 - dg0));
+                    atomicAdd(w.prof + 12, (unsigned long long)(dg2 - dg1));
+                    atomicAdd(w.prof + 13, 1ull);
+                }
+#endif
             }
             tmem_wait_ld();
             team_bar(team);
@@ -1093,48 +1109,11 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void *f = nullptr;
-        cudaDriverEntryPointQueryResult qr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) ==
-                cudaSuccess &&
-            qr == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    }
-    return fn;
-}
-
-// 2-D fp16 map over a split table [n_rows][TW]: box {64, 1} (the
-// tile::gather4 form), SWIZZLE_128B; rows out of range (id -1) land as zeros
-int tc_table_map(CUtensorMap *map, const __half *t, int64_t n_rows, int TW) {
-    auto fn = tc_encode_fn();
-    if (!fn) {
-        set_error("cuTensorMapEncodeTiled unavailable");
-        return MCF_E_CUDA;
-    }
-    cuuint64_t dims[2] = {(cuuint64_t)TW, (cuuint64_t)std::max<int64_t>(n_rows, 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)TW * 2};
-    cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half *>(t), dims, strides,
-                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-        return MCF_E_CUDA;
-    }
-    return MCF_OK;
-}
-
 template <int NBLK>
 int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t s) {
     using C = TcCfg<NBLK>;
-    CUtensorMap mh, ml;
     int rc;
-    if ((rc = tc_table_map(&mh, w.th, p.n_fixed, C::TW))) return rc;
-    if ((rc = tc_table_map(&ml, w.tl, p.n_fixed, C::TW))) return rc;
-    k_tc_split<<<148 * 8, 256, 0, s>>>(p, w, C::TW);
+    k_tc_split<<<148 * 8, 256, 0, s>>>(p, q, w, C::TW);
     if ((rc = check_launch("mcf_als_half_step(tensor-core split)"))) return rc;
     static bool attr = false;
     if (!attr) {
@@ -1148,7 +1127,7 @@ int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t
     per_sm = std::max(1, std::min(per_sm, 512 / C::TMEM_COLS));
     const int64_t want = ceil_div(q.n_tasks, C::TEAMS);
     const int64_t grid = std::min<int64_t>(want, (int64_t)sms * per_sm);
-    if (grid > 0) k_als_tc<NBLK><<<(unsigned)grid, C::TEAMS * 128, C::SMEM, s>>>(p, q, w, mh, ml);
+    if (grid > 0) k_als_tc<NBLK><<<(unsigned)grid, C::TEAMS * 128, C::SMEM, s>>>(p, q, w);
     return check_launch("mcf_als_half_step(tensor core)");
 }
 
@@ -1167,15 +1146,16 @@ size_t tc_slot_floats(int D) {
 
 static size_t tc_table_width(int D) { return (size_t)((D + 15) / 16 * 16 + 63) / 64 * 64; }
 
-size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed) {
+size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed, int64_t nnz) {
     return 256 + align_up(sizeof(int32_t) * (size_t)(slots + 1), 256) +
            align_up(sizeof(float) * (size_t)slots * tc_slot_floats(D), 256) +
-           2 * align_up(2 * (size_t)n_fixed * tc_table_width(D) + 256, 256);
+           2 * align_up(2 * (size_t)n_fixed * tc_table_width(D) + 256, 256) +
+           align_up(sizeof(uint32_t) * (size_t)(nnz + 64), 256);
 }
 
 int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
-                  cudaStream_t s) {
-    if (ws_bytes < tc_workspace_bytes(p.D, slots, p.n_fixed)) {
+                  int64_t nnz, cudaStream_t s) {
+    if (ws_bytes < tc_workspace_bytes(p.D, slots, p.n_fixed, nnz)) {
         set_error("mcf_als_half_step: workspace too small for the tensor-core path");
         return MCF_E_WORKSPACE;
     }
@@ -1186,6 +1166,7 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     w.partials = c.take<float>((size_t)slots * tc_slot_floats(p.D));
     w.th = c.take<__half>((size_t)p.n_fixed * tc_table_width(p.D) + 128);
     w.tl = c.take<__half>((size_t)p.n_fixed * tc_table_width(p.D) + 128);
+    w.ysp = c.take<uint32_t>((size_t)nnz + 64);
     w.n_slots = slots;
     w.prof = nullptr;
     w.team_limit = getenv("MCF_TC_TEAMS") ? atoi(getenv("MCF_TC_TEAMS")) : 4;
@@ -1224,12 +1205,14 @@ extern "C" int mcf_tc_prof_read(unsigned long long *out10) {
     return 0;
 }
 
-// the same counters per task class (16 each: 10 phases, [10] = tasks):
-// 0 dual rows, 1 primal rows with n < D (refined), 2 primal rows, 3 hot chunks
-extern "C" int mcf_tc_prof_read_classes(unsigned long long *out64) {
+// all 80 counters: [0..9] phases, [11..13] diagonal warp (TMEM-load wait,
+// factorisation cycles, blocks), then per task class 16 each (10 phases,
+// [10] = tasks): 0 dual rows, 1 primal rows with n < D (refined), 2 primal
+// rows, 3 hot chunks
+extern "C" int mcf_tc_prof_read_classes(unsigned long long *out80) {
     if (!mcf::g_tc_prof) return -1;
     cudaDeviceSynchronize();
-    cudaMemcpy(out64, mcf::g_tc_prof + 16, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out80, mcf::g_tc_prof, 80 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaMemset(mcf::g_tc_prof, 0, 80 * sizeof(unsigned long long));
     return 0;
 }

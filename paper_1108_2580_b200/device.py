@@ -186,7 +186,7 @@ class LayoutSolver:
         slots = max(info[1], info[3])   # hot-chunk slots (pair path / warp+CTA paths)
         k = (id(lay), rows_key)
         need = int(_lib.lib().mcf_als_workspace_bytes_fixed(n_list, slots, self.D,
-                                                            int(fixed.shape[0])))
+                                                            int(fixed.shape[0]), int(info[5])))
         if k not in self._ws or self._ws[k].numel() < need:
             self._ws[k] = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
         ws = self._ws[k]

@@ -25,7 +25,8 @@ eng = AlsEngine(r, cfg.D)
 eng.set_factors(P0, Q0)
 L = _lib.lib()
 L.mcf_tc_prof_read_classes.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
-buf = (ctypes.c_ulonglong * 64)()
+L.mcf_tc_prof_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+buf = (ctypes.c_ulonglong * 80)()
 eng.sweep(0.0, cfg.lam)
 L.mcf_tc_prof_read_classes(buf)
 for side in ("items", "users"):
@@ -35,14 +36,18 @@ for side in ("items", "users"):
     e1.record()
     torch.cuda.synchronize()
     L.mcf_tc_prof_read_classes(buf)
-    tot = sum(buf[16 * c + k] for c in range(4) for k in range(10))
+    cls = buf[16:]
+    tot = sum(cls[16 * c + k] for c in range(4) for k in range(10))
     print(f"== {side} half-step: {e0.elapsed_time(e1):.2f} ms (profiled), "
           f"{tot / 1e9:.2f} G team-cycles")
+    if buf[13]:
+        print(f"  diagonal warp per block: TMEM-load wait {buf[11] / buf[13]:.0f}, "
+              f"factorisation {buf[12] / buf[13]:.0f} cycles ({buf[13]} blocks)")
     for c in range(4):
-        nt = buf[16 * c + 10]
-        ct = sum(buf[16 * c + k] for k in range(10))
+        nt = cls[16 * c + 10]
+        ct = sum(cls[16 * c + k] for k in range(10))
         if nt == 0:
             continue
         print(f"  {CLASSES[c]:<11} {nt:>8} tasks, {100 * ct / tot:5.1f}% of cycles, "
               f"{ct / nt:8.0f} cycles/task: " +
-              ", ".join(f"{NAMES[k]} {buf[16 * c + k] / nt:.0f}" for k in range(10) if buf[16 * c + k]))
+              ", ".join(f"{NAMES[k]} {cls[16 * c + k] / nt:.0f}" for k in range(10) if cls[16 * c + k]))
