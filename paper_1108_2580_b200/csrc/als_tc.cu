@@ -414,7 +414,12 @@ __global__ void __launch_bounds__(512, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ uint32_t tmem_base_sh;
     __shared__ __align__(8) unsigned long long bars[4][2 * C::NST + 1];   // full | empty | chol
-    __shared__ int64_t team_task[4];
+    struct TaskSh {   // a team's next task, fetched ahead by thread PF
+        int64_t task, k0, nrow;
+        int row, n, slot;
+        float S;
+    };
+    __shared__ TaskSh tsh[4];
     __shared__ int team_flag[4];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -496,25 +501,57 @@ __global__ void __launch_bounds__(512, 1)
     } while (0)
 #endif
 
+    // The next task is fetched during the current one by thread PF (warp 3,
+    // idle during warp 0's back substitution): the counter atomic right
+    // after the Gram, the plan and row-pointer loads at the back
+    // substitution; published to tsh for the next iteration.
+    constexpr int PF = 96;
+    int64_t pf_task = 0;
+    bool pf_started = false;
+    auto pf_start = [&]() {
+        if (m == PF && !pf_started) {
+            pf_task = atomicAdd(q.group_counter, 1);
+            pf_started = true;
+        }
+    };
+    auto pf_finish = [&]() {
+        if (m == PF) {
+            if (!pf_started) pf_task = atomicAdd(q.group_counter, 1);
+            pf_started = false;
+            TaskSh t;
+            t.task = pf_task;
+            t.row = 0, t.k0 = 0, t.n = 0, t.slot = -1, t.nrow = 0, t.S = 0.f;
+            if (pf_task < q.n_tasks) {
+                t.row = q.task_row[pf_task];
+                t.k0 = q.task_k0[pf_task];
+                t.n = q.task_n[pf_task];
+                t.slot = q.task_slot[pf_task];
+                t.nrow = p.ptr[t.row + 1] - p.ptr[t.row];
+                t.S = p.tax_S ? p.tax_S[t.row] : 0.f;
+            }
+            tsh[team] = t;
+        }
+    };
+    if (team < w.team_limit) pf_finish();
     for (;;) {
         if (team >= w.team_limit) break;
-        if (m == 0) team_task[team] = atomicAdd(q.group_counter, 1);
         team_bar(team);
-        const int64_t task = team_task[team];
-        if (task >= q.n_tasks) break;
-        const int row = q.task_row[task];
-        const int64_t k0 = q.task_k0[task];
-        const int n = q.task_n[task];
-        const int slot = q.task_slot[task];
-        const int64_t nrow = p.ptr[row + 1] - p.ptr[row];
-        const float Srow = p.tax_S ? p.tax_S[row] : 0.f;
+        const TaskSh cur = tsh[team];
+        if (cur.task >= q.n_tasks) break;
+        const int row = cur.row;
+        const int64_t k0 = cur.k0;
+        const int n = cur.n;
+        const int slot = cur.slot;
+        const int64_t nrow = cur.nrow;
+        const float Srow = cur.S;
         if (nrow == 0 && Srow == 0.f) {   // empty row: 0 with a regulariser, else singular
             if (p.lam_c > 0.f || p.lam_n > 0.f) {
                 if (m < p.ld) put_out(p, row, m, 0.f);
             } else if (m == 0) {
                 report_fail(p.fail, row);
             }
-            team_bar(team);   // team_task is rewritten next
+            team_bar(team);   // every thread has read tsh
+            pf_finish();
             continue;
         }
         TCP(0);
@@ -680,6 +717,7 @@ __global__ void __launch_bounds__(512, 1)
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
         TCP(1);
+        pf_start();
 
         // ---------------- hot-row chunk: dump C | rhs, the last chunk sums them
         if (slot >= 0) {
@@ -707,6 +745,7 @@ __global__ void __launch_bounds__(512, 1)
             if (!team_flag[team]) {
                 TCP(2);
                 TCP_FLUSH(3);
+                pf_finish();
                 continue;
             }
             __threadfence();
@@ -934,13 +973,15 @@ __global__ void __launch_bounds__(512, 1)
         if (failed) {
             if (m == 0) report_fail(p.fail, row);
             team_bar(team);
+            pf_finish();
             continue;
         }
         TCP(5);
 
         // ---------------- back substitution L^T x = z by warp 0 (L from smem), 8
-        // unknowns per step; x -> xbuf
+        // unknowns per step; x -> xbuf (meanwhile thread PF fetches the next task)
         team_bar(team);
+        pf_finish();
         if (wq == 0) {
             float zr[4];
 #pragma unroll
