@@ -1418,12 +1418,12 @@ __device__ __forceinline__ bool thread_solve(float *g, int D, float diag_add, in
 // (yy = sum w y^2 accumulated with the Gram; exact for tau = 0).
 template <int LDK, bool SCHUR = false>
 __device__ void finish_row(const AlsParams &p, float *g, int r, int64_t n, float yy,
-                           double &sse, double &reg) {
+                           double &sse, double &reg, bool emitted = false) {
     constexpr int RHS0 = LDK * (LDK + 1) / 2;
     constexpr int UOFF = RHS0 + LDK, DOFF = UOFF + LDK;
     const int D = p.D;
     sse = reg = 0.0;
-    if constexpr (SCHUR) {
+    if (SCHUR && !emitted) {   // (the pair kernel emits and corrects warp-wide)
         if (p.emit) {   // [A | c | u | d | n] for the artist step (before any correction)
             float *e = p.emit + (size_t)r * EMIT_STRIDE;
             for (int i = 0; i < RHS0 + LDK; ++i) e[i] = g[i];
@@ -1844,6 +1844,54 @@ k_als_pair(AlsParams p, PairPlan q) {
         // scatter the lane's accumulators into the pair's packed [A | b]
         acc.scatter(my_g, h, C::RHS0);
         __syncwarp();
+        if constexpr (SCHUR) {
+            const bool whole = task < q.n_tasks && slot < 0;
+            if (p.emit) {
+                // [A | c | u | d | n] of every whole row of the group for the artist
+                // step (before any correction): the packed system, u and d are
+                // contiguous in a pair's buffer, so the warp copies them row by
+                // row with coalesced stores
+                constexpr int NE = C::RHS0 + 2 * C::LDK + 1;
+                static_assert(NE + 1 <= EMIT_STRIDE, "emit row");
+#pragma unroll 1
+                for (int pp = 0; pp < C::PAIRS; ++pp) {
+                    const bool wp = __shfl_sync(FULL, whole, 2 * pp);
+                    if (!wp) continue;
+                    const int rp = __shfl_sync(FULL, row, 2 * pp);
+                    const int np = __shfl_sync(FULL, n, 2 * pp);
+                    const float *gp = reinterpret_cast<const float *>(wbase) + pp * C::GSTRIDE_S;
+                    float *e = p.emit + (size_t)rp * EMIT_STRIDE;
+                    for (int i = lane; i <= NE; i += 32) e[i] = i < NE ? gp[i] : (float)np;
+                }
+            }
+            if (whole && p.corr_idx && p.corr_idx[row] >= 0) {
+                // the row's artist terms from its own Gram, c -= A q_a + u b_a,
+                // d -= u.q_a + n b_a; lane h takes the rows i = h mod 2
+                const float *v = p.corr_tab + (size_t)p.corr_idx[row] * p.ld;
+                const int D = p.D;
+                const float ba = v[D];
+                float t[(C::LDK + 1) / 2], ud = 0.f;
+#pragma unroll
+                for (int ii = 0; ii < (C::LDK + 1) / 2; ++ii) {
+                    const int i = 2 * ii + h;
+                    t[ii] = 0.f;
+                    if (i < D) {
+                        float a = my_g[C::UOFF + i] * ba;
+                        for (int k = 0; k < D; ++k)
+                            a = fmaf(my_g[i >= k ? pidx(i, k) : pidx(k, i)], v[k], a);
+                        t[ii] = a;
+                        ud = fmaf(my_g[C::UOFF + i], v[i], ud);
+                    }
+                }
+                ud += __shfl_xor_sync(0x3u << (2 * pair), ud, 1);
+                __syncwarp(0x3u << (2 * pair));
+#pragma unroll
+                for (int ii = 0; ii < (C::LDK + 1) / 2; ++ii)
+                    if (2 * ii + h < D) my_g[C::RHS0 + 2 * ii + h] -= t[ii];
+                if (h == 0) my_g[C::DOFF] -= fmaf((float)n, ba, ud);
+            }
+            __syncwarp();
+        }
         double o_sse = 0.0, o_reg = 0.0;
         if (task < q.n_tasks) {
             if (slot >= 0) {
@@ -1854,7 +1902,7 @@ k_als_pair(AlsParams p, PairPlan q) {
                     for (int i = h; i <= C::LDK; i += 2) dst[C::PU + i] = my_g[C::UOFF + i];
                 }
             } else if (h == 0) {
-                finish_row<C::LDK, SCHUR>(p, my_g, row, n, acc.yy, o_sse, o_reg);
+                finish_row<C::LDK, SCHUR>(p, my_g, row, n, acc.yy, o_sse, o_reg, true);
             }
         }
         if (p.obj_partial) {   // fixed-order butterfly: deterministic per group
@@ -2440,7 +2488,7 @@ extern "C" size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, i
     }
     const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
     size_t part = sizeof(float) * (size_t)slots * per;
-    if (D >= 64 && D <= 128 && n_fixed > 0) part = std::max(part, tc_workspace_bytes(D, slots, n_fixed, nnz));
+    if (D >= tc_min_d() && D <= 128 && n_fixed > 0) part = std::max(part, tc_workspace_bytes(D, slots, n_fixed, nnz));
     return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) + part;
 }
 

@@ -134,6 +134,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 
 // tensor-core wide path (als_tc.cu): 21 <= D <= 127, no per-observation weights
 bool tc_path(int D, bool weighted);
+int tc_min_d();
 size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed, int64_t nnz);
 int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
                   int64_t nnz, cudaStream_t s);

@@ -1176,8 +1176,19 @@ int launch_tc(const AlsParams &p, const PairPlan &q, const TcWs &w, cudaStream_t
 
 static unsigned long long *g_tc_prof = nullptr;
 
+// lowest D routed to the tensor-core path (MCF_TC_MIN_D: experiments; the
+// kernel handles any 49 <= D <= 128 -- DP = 64 is its smallest geometry)
+int tc_min_d() {
+    static const int v = [] {
+        const char *e = getenv("MCF_TC_MIN_D");
+        const int d = e ? atoi(e) : 64;
+        return d < 49 ? 49 : d;
+    }();
+    return v;
+}
+
 bool tc_path(int D, bool weighted) {
-    return !weighted && D >= 64 && D <= 128 && !getenv("MCF_NO_TC");
+    return !weighted && D >= tc_min_d() && D <= 128 && !getenv("MCF_NO_TC");
 }
 
 size_t tc_slot_floats(int D) {

@@ -42,7 +42,8 @@ def tc_path(D: int, weighted: bool = False) -> bool:
     """mcf_als_half_step runs the tensor-core wide path (als_tc.cu) for this
     dimension: 64 <= D <= 128 without per-observation weights (MCF_NO_TC=1
     selects the CUDA-core kernels instead)."""
-    return 64 <= D <= 128 and not weighted and not os.environ.get("MCF_NO_TC")
+    lo = max(49, int(os.environ.get("MCF_TC_MIN_D", 64)))   # must agree with tc_min_d() (als_tc.cu)
+    return lo <= D <= 128 and not weighted and not os.environ.get("MCF_NO_TC")
 
 
 def cuda_device(device=None) -> torch.device:
