@@ -424,6 +424,10 @@ __global__ void __launch_bounds__(512, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int team = warp >> 2, wq = warp & 3, m = threadIdx.x & 127;
+    // the team's single-warp work (MMA issue, triangular solves) runs on warp
+    // `lead`: warp id mod 4 selects the SM sub-partition, so the four teams'
+    // serial phases land on four different schedulers
+    const int lead = team & 3;
     // SWIZZLE_128B atoms need 1 KB alignment
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(512, 1)
     // idle during warp 0's back substitution): the counter atomic right
     // after the Gram, the plan and row-pointer loads at the back
     // substitution; published to tsh for the next iteration.
-    constexpr int PF = 96;
+    const int PF = 32 * ((lead + 2) & 3);   // a thread of a warp that idles during the lead warp's solves
     int64_t pf_task = 0;
     bool pf_started = false;
     auto pf_start = [&]() {
@@ -598,56 +602,57 @@ __global__ void __launch_bounds__(512, 1)
                 const int kk = 4 * wq + j, r = kk & 7;
                 doff[j] = tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 + r * 128 + ((c8 ^ r) << 4);
             }
-            // rating ids run two stages ahead of the copies (their loads miss
-            // L2 every other stage; one stage of cover exposed them; clamped
-            // addresses: nothing consumes a load before its stage is issued)
-            auto load_ids = [&](int t, int (&ids)[4]) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) ids[j] = __ldg(p.idx + k0 + min(16 * t + 4 * wq + j, n - 1));
+            // Partner ids: one coalesced load per warp per 8 stages -- lane l holds
+            // the id of rating 4 wq + (l & 3) of stage 8 blk + (l >> 2) -- a block
+            // ahead of its use; a stage's 4 ids are shuffled out of it.  (A load
+            // per id per stage with its clamp and 64-bit address was ~40 of the
+            // ~250 instructions every warp issued per stage: the Gram loop was
+            // issue-bound, 16 warps x 250 instructions per 16 ratings.)
+            auto load_idblk = [&](int blk) {
+                const int k = 16 * (8 * blk + (lane >> 2)) + 4 * wq + (lane & 3);
+                return __ldg(p.idx + k0 + min(k, n - 1));
             };
+            int idc = load_idblk(0), idnx = load_idblk(1);
             const uint32_t *ysrc = w.ysp + k0;
-            auto issue = [&](int t, const int (&ids)[4]) {   // stage t -> slot (gst + t) % NST
-                const unsigned g = gst + (unsigned)t, b = g % NST;
-                if (g >= NST) warp_mbar_wait(ebar0 + 8 * b, ((g / NST) - 1) & 1);
-                const uint32_t sts = tbs + b * C::STAGE;
+            const uint32_t ydst = 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16;
+            // slot / generation of the next stage to issue and to consume
+            unsigned ib = gst % NST, iq = gst / NST, cb = ib, cq = iq;
+            auto issue = [&](int t) {   // stage t -> slot ib
+                if ((t & 7) == 0 && t > 0) {
+                    idc = idnx;
+                    idnx = load_idblk((t >> 3) + 1);
+                }
+                int ids[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) ids[j] = __shfl_sync(FULL, idc, 4 * (t & 7) + j);
+                if (iq > 0) warp_mbar_wait(ebar0 + 8 * ib, (iq - 1) & 1);
+                const uint32_t sts = tbs + ib * C::STAGE;
+                const int rem = n - 16 * t - 4 * wq;   // ratings left for this warp's 4 rows
                 if (chunk_ok) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sts + doff[j]),
-                                     "l"(tsrc + (size_t)ids[j] * C::TW),
-                                     "r"(16 * t + 4 * wq + j < n ? 16 : 0));
+                                     "l"(tsrc + (size_t)ids[j] * C::TW), "r"(j < rem ? 16 : 0));
                 }
                 if (m < 16)   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l); columns 2..15 are never read
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
-                                     sts + 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16),
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sts + ydst),
                                  "l"(ysrc + min(16 * t + m, n - 1)), "r"(16 * t + m < n ? 4 : 0));
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar0 + 8 * b)
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar0 + 8 * ib)
                              : "memory");
-            };
-            {   // prologue: every id load first, then the copies
-                int ids0[LEAD][4];
-#pragma unroll
-                for (int t = 0; t < LEAD; ++t) load_ids(t, ids0[t]);
-#pragma unroll
-                for (int t = 0; t < LEAD; ++t)
-                    if (t < nst) issue(t, ids0[t]);
-            }
-            int idn[4], idn2[4];
-            load_ids(LEAD, idn);
-            load_ids(LEAD + 1, idn2);
-            for (int st = 0; st < nst; ++st) {
-                const int t = st + LEAD;
-                if (t < nst) {
-                    issue(t, idn);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) idn[j] = idn2[j];
-                    if (t + 2 < nst) load_ids(t + 2, idn2);
+                if (++ib == NST) {
+                    ib = 0;
+                    ++iq;
                 }
-                if (m == 0) {
-                    const unsigned g = gst + (unsigned)st, b = g % NST;
-                    mbar_wait(fbar0 + 8 * b, (g / NST) & 1);   // every copy + the rating tile landed
+            };
+#pragma unroll
+            for (int t = 0; t < LEAD; ++t)
+                if (t < nst) issue(t);
+            for (int st = 0; st < nst; ++st) {
+                if (st + LEAD < nst) issue(st + LEAD);
+                if (m == 32 * lead) {
+                    mbar_wait(fbar0 + 8 * cb, cq & 1);   // every copy + the rating tile landed
                     tc_fence_after();
-                    const uint32_t ha = tbs + b * C::STAGE;
+                    const uint32_t ha = tbs + cb * C::STAGE;
                     const uint64_t dh = sdesc_sw128(ha, 1024, C::NA * 1024);
                     const uint64_t dl = sdesc_sw128(ha + C::HT, 1024, C::NA * 1024);
                     const uint64_t dy = sdesc(ha + 2 * C::HT, 256, 128);
@@ -657,11 +662,15 @@ __global__ void __launch_bounds__(512, 1)
                     umma(tmem, dl, dh, id_gram, 1u);
                     umma(tmem + DP, dh, dy, id_rhs, acc);
                     umma(tmem + DP, dl, dy, id_rhs, 1u);
-                    umma_commit(ebar0 + 8 * b);
+                    umma_commit(ebar0 + 8 * cb);
+                }
+                if (++cb == NST) {
+                    cb = 0;
+                    ++cq;
                 }
             }
-            const unsigned gl = gst + (unsigned)nst - 1;
-            warp_mbar_wait(ebar0 + 8 * (gl % NST), (gl / NST) & 1);   // last MMAs done
+            // last MMAs done (the stage before (cb, cq))
+            warp_mbar_wait(ebar0 + 8 * (cb == 0 ? NST - 1 : cb - 1), (cb == 0 ? cq - 1 : cq) & 1);
         }
         gst += (unsigned)nst;
         tc_fence_before();
@@ -690,7 +699,7 @@ __global__ void __launch_bounds__(512, 1)
             proxy_fence();
             tc_fence_before();
             team_bar(team);
-            if (m == 0) {
+            if (m == 32 * lead) {
                 tc_fence_after();
                 const uint32_t idd = idesc(dim, false, false);
                 for (int kk = 0; kk < DP / 16; ++kk) {
@@ -951,7 +960,7 @@ __global__ void __launch_bounds__(512, 1)
                 proxy_fence();
                 team_bar(team);
                 // trailing update C -= P_h P_h^T + P_h P_l^T + P_l P_h^T
-                if (m == 0) {
+                if (m == 32 * lead) {
                     tc_fence_after();
                     const int N = dim - c0 - 16;
                     const uint32_t id = idesc(N, false, true);
@@ -982,7 +991,7 @@ __global__ void __launch_bounds__(512, 1)
         // unknowns per step; x -> xbuf (meanwhile thread PF fetches the next task)
         team_bar(team);
         pf_finish();
-        if (wq == 0) {
+        if (wq == lead) {
             float zr[4];
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
@@ -1035,7 +1044,7 @@ __global__ void __launch_bounds__(512, 1)
                 rho[m] = rh;
             }
             team_bar(team);
-            if (wq == 0) {
+            if (wq == lead) {
                 float zr[4];
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
@@ -1109,7 +1118,7 @@ __global__ void __launch_bounds__(512, 1)
             }
             if (m < DP) zbuf[m] = m < D ? rf : 0.f;
             team_bar(team);
-            if (wq == 0) {
+            if (wq == lead) {
                 float zr[4];
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
