@@ -1082,16 +1082,18 @@ __global__ void __launch_bounds__(512, 1)
                 const int id = __ldg(p.idx + k0 + m);
                 const float4 *xr4 = reinterpret_cast<const float4 *>(p.fixed + (size_t)id * p.ld);
                 float d0 = 0.f, d1 = 0.f;
-                for (int c = 0; c < p.ld / 4; c += 2) {
-                    const float4 u = __ldg(xr4 + c);
-                    const float4 xv = *reinterpret_cast<const float4 *>(xbuf + 4 * c);
-                    d0 = fmaf(u.x, xv.x, d0); d1 = fmaf(u.y, xv.y, d1);
-                    d0 = fmaf(u.z, xv.z, d0); d1 = fmaf(u.w, xv.w, d1);
-                    if (c + 1 < p.ld / 4) {
-                        const float4 u2 = __ldg(xr4 + c + 1);
-                        const float4 xv2 = *reinterpret_cast<const float4 *>(xbuf + 4 * c + 4);
-                        d0 = fmaf(u2.x, xv2.x, d0); d1 = fmaf(u2.y, xv2.y, d1);
-                        d0 = fmaf(u2.z, xv2.z, d0); d1 = fmaf(u2.w, xv2.w, d1);
+                const int nc4 = p.ld >> 2;
+                for (int c = 0; c < nc4; c += 8) {   // 8 independent 16-byte loads in flight
+                    float4 u[8];
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) u[q4] = __ldg(xr4 + min(c + q4, nc4 - 1));
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                        if (c + q4 < nc4) {
+                            const float4 xv = *reinterpret_cast<const float4 *>(xbuf + 4 * (c + q4));
+                            d0 = fmaf(u[q4].x, xv.x, d0); d1 = fmaf(u[q4].y, xv.y, d1);
+                            d0 = fmaf(u[q4].z, xv.z, d0); d1 = fmaf(u[q4].w, xv.w, d1);
+                        }
                     }
                 }
                 zbuf[m] = (__ldg(p.val + k0 + m) - p.y_shift) - (d0 + d1);
@@ -1103,12 +1105,17 @@ __global__ void __launch_bounds__(512, 1)
             if (m < D) {
                 const int *ids = reinterpret_cast<const int *>(tb + C::OFF_PH);
                 float r1 = 0.f;
-                int k = 0;
-                for (; k + 1 < n; k += 2) {
-                    rf = fmaf(__ldg(p.fixed + (size_t)ids[k] * p.ld + m), zbuf[k], rf);
-                    r1 = fmaf(__ldg(p.fixed + (size_t)ids[k + 1] * p.ld + m), zbuf[k + 1], r1);
+                for (int k = 0; k < n; k += 8) {   // 8 independent (coalesced) row loads in flight
+                    float v[8];
+#pragma unroll
+                    for (int q8 = 0; q8 < 8; ++q8)
+                        v[q8] = __ldg(p.fixed + (size_t)ids[min(k + q8, n - 1)] * p.ld + m);
+#pragma unroll
+                    for (int q8 = 0; q8 < 8; q8 += 2) {
+                        if (k + q8 < n) rf = fmaf(v[q8], zbuf[k + q8], rf);
+                        if (k + q8 + 1 < n) r1 = fmaf(v[q8 + 1], zbuf[k + q8 + 1], r1);
+                    }
                 }
-                if (k < n) rf = fmaf(__ldg(p.fixed + (size_t)ids[k] * p.ld + m), zbuf[k], rf);
                 rf += r1;
             }
             team_bar(team);
