@@ -1719,6 +1719,14 @@ k_als_pair(AlsParams p, PairPlan q) {
         const int32_t *idxp = p.idx + k0;
         const float *valp = p.val + k0;
         const float *wtsp = HAS_W ? p.wts + k0 : nullptr;
+        const int k0lo = (int)k0 & 31;
+        // stream bases as opaque 64-bit values: one IMAD.WIDE per copy address
+        // (the compiler otherwise rebuilds base + 4 (k0 + k) from k0 for every copy)
+        unsigned long long valb = reinterpret_cast<unsigned long long>(valp);
+        unsigned long long idxb = reinterpret_cast<unsigned long long>(idxp);
+        unsigned long long wtsb = reinterpret_cast<unsigned long long>(wtsp);
+        asm volatile("" : "+l"(valb), "+l"(idxb));
+        if (HAS_W) asm volatile("" : "+l"(wtsb));
         if (n > 0)
             for (int o = 0; o < min(n, C::PF); o += 32)
                 prefetch_l2(h ? (const void *)(valp + o) : (const void *)(idxp + o));
@@ -1730,48 +1738,59 @@ k_als_pair(AlsParams p, PairPlan q) {
         const unsigned gbase = gst;
         // gathers of stage s (ratings R*s .. R*s+R-1, partner ids in ids[]);
         // also brings the ids of stage s+NS-1 into the ring
+        // (addresses: one IMAD.WIDE per copy off 64-bit bases kept in registers;
+        // padded ratings keep a valid id and copy 0 bytes -- the issue block is
+        // ~1/3 of the warp's instructions and all dependent integer chains)
+        const char *fixed_h = reinterpret_cast<const char *>(p.fixed + 4 * h);
+        const unsigned ldb = (unsigned)p.ld * 4u;
         auto issue = [&](int s, const int (&ids)[R]) {
             const unsigned gs = gbase + (unsigned)s;
-            const unsigned ss = my_slot_s + (gs % C::NS) * C::STAGE_BYTES;
+            const unsigned slot = gs % C::NS;
+            unsigned ss = my_slot_s + slot * C::STAGE_BYTES;
+            asm volatile("" : "+r"(ss));
+            const int nv = n - R * s;   // ratings of this stage that exist
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int col = ids[r];
-                const bool ok = col >= 0;
-                const float *src = p.fixed + (size_t)(ok ? col : 0) * p.ld;
-                const unsigned rs = ss + r * C::RROW * 4;
+                const bool ok = r < nv;
+                const char *src = fixed_h + (size_t)(unsigned)ids[r] * ldb;
+                const unsigned rs = ss + r * C::RROW * 4 + 16 * h;
                 // lanes h = 0, 1 copy adjacent 16-byte blocks in one instruction
                 // (one 32-byte sector when the row is sector-aligned)
 #pragma unroll
-                for (int b = h; b < NBK + (YSUB ? 1 : 0); b += 2)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
-                                 ::"r"(rs + 16 * b), "l"(src + 4 * b),
-                                 "r"((ok && (FULLBLK || b < nb_real || b == ysub_blk)) ? 16 : 0));
+                for (int b2 = 0; b2 < (NBK + (YSUB ? 1 : 0) + 1) / 2; ++b2) {
+                    const int b = 2 * b2 + h;
+                    if (2 * b2 + 1 < NBK + (YSUB ? 1 : 0) || h == 0)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
+                                     ::"r"(rs + 32 * b2), "l"(src + 32 * b2),
+                                     "r"((ok && (FULLBLK || b < nb_real || b == ysub_blk)) ? 16 : 0));
+                }
             }
             // lane h brings the ratings (and weights) of rows h, h+2, ... and
             // the partner ids of the same rows of stage s + NS - 1
             const unsigned ids_dst = ring_ids_s + 4 * (R * ((gs + C::NS - 1) % C::NR));
 #pragma unroll
-            for (int r = h; r < R; r += 2) {
-                const int k = R * s + r;
-                const bool okv = k < n;
+            for (int r2 = 0; r2 < R / 2; ++r2) {
+                const int r = 2 * r2 + h;
+                const bool okv = r < nv;
+                const unsigned k = okv ? (unsigned)(R * s + r) : 0u;
                 asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                             ::"r"(ss + 4 * (C::YOFF + r)), "l"(valp + (okv ? k : 0)),
+                             ::"r"(ss + 4 * (C::YOFF + r)), "l"(valb + 4ull * k),
                              "r"(okv ? 4 : 0), "l"(pol_stream));
                 if (HAS_W)
                     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                                 ::"r"(ss + 4 * (C::WOFF + r)), "l"(wtsp + (okv ? k : 0)),
+                                 ::"r"(ss + 4 * (C::WOFF + r)), "l"(wtsb + 4ull * k),
                                  "r"(okv ? 4 : 0), "l"(pol_stream));
-                const int ku = R * (s + C::NS - 1) + r;
-                const bool oku = ku < n;
+                const bool oku = r + R * (C::NS - 1) < nv;
+                const unsigned ku = oku ? (unsigned)(R * (s + C::NS - 1) + r) : 0u;
                 asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n"
-                             ::"r"(ids_dst + 4 * r), "l"(idxp + (oku ? ku : 0)), "r"(oku ? 4 : 0),
+                             ::"r"(ids_dst + 4 * r), "l"(idxb + 4ull * ku), "r"(oku ? 4 : 0),
                              "l"(pol_stream));
             }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar0 + 8 * (gs % C::NS))
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar0 + 8 * slot)
                          : "memory");
             const int pf = R * s + C::PF;
-            if (pf < n && ((k0 + pf) & 31) < R)
-                prefetch_l2(h ? (const void *)(valp + pf) : (const void *)(idxp + pf));
+            if (pf < n && ((k0lo + pf) & 31) < R)
+                prefetch_l2(reinterpret_cast<const void *>((h ? valb : idxb) + 4ull * (unsigned)pf));
         };
         auto consume = [&](int t) {
             const unsigned gs = gbase + (unsigned)t;
@@ -1817,7 +1836,7 @@ k_als_pair(AlsParams p, PairPlan q) {
         for (int s = 0; s < C::NS - 1 && s < nst; ++s) {
             int ids[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) ids[r] = R * s + r < n ? idxp[R * s + r] : -1;
+            for (int r = 0; r < R; ++r) ids[r] = R * s + r < n ? idxp[R * s + r] : 0;
             issue(s, ids);
         }
         for (int t = 0; t < nst; ++t) {
@@ -1833,9 +1852,7 @@ k_als_pair(AlsParams p, PairPlan q) {
                     const int2 v = *reinterpret_cast<const int2 *>(rid);
                     ids[0] = v.x; ids[1] = v.y;
                 }
-                // a zero-filled id (past the task end) reads as 0: mask by the task length
-#pragma unroll
-                for (int r = 0; r < R; ++r) ids[r] = R * s + r < n ? ids[r] : -1;
+                // (an id past the task end was zero-filled: row 0, copied with size 0)
                 issue(s, ids);
             }
         }
@@ -2644,7 +2661,10 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         q.n_heavy = plan_info[4];
         q.group_counter = p.counters + n_list;
         if (q.n_tasks == 0) return MCF_OK;
-        return launch_als_tc(p, q, p.partials, ws_bytes - fixed_part, plan_info[3], plan_info[5], s);
+        const int cut = als_dual_cut(p, wts != nullptr);
+        if ((rc = launch_als_tc(p, q, p.partials, ws_bytes - fixed_part, plan_info[3], plan_info[5], cut, s)))
+            return rc;
+        return launch_als_dual(p, q, p.counters + n_list + 3, cut, s);
     }
     if (total_items == 0) return MCF_OK;
     return wts ? dispatch<true>(p, s) : dispatch<false>(p, s);

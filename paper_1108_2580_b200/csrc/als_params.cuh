@@ -137,6 +137,12 @@ bool tc_path(int D, bool weighted);
 int tc_min_d();
 size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed, int64_t nnz);
 int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
-                  int64_t nnz, cudaStream_t s);
+                  int64_t nnz, int dual_cut, cudaStream_t s);
+
+// short rows of the wide path on CUDA cores in the dual form (als_dual.cu):
+// light tasks with at most als_dual_cut() ratings (0: call not eligible) are
+// left by the tensor-core kernel and taken from the end of the task list
+int als_dual_cut(const AlsParams &p, bool weighted);
+int launch_als_dual(const AlsParams &p, const PairPlan &q, int *counter, int cut, cudaStream_t s);
 
 }  // namespace mcf

@@ -106,6 +106,7 @@ struct TcWs {
     int64_t n_slots;
     unsigned long long *prof;   // phase cycle counters (MCF_TC_PROF) or null
     int team_limit;             // teams per CTA that take work (MCF_TC_TEAMS, experiments)
+    int dual_cut;               // light tasks with n <= dual_cut are left to k_als_dual (0: none)
     __half *th, *tl;            // split fixed table: s*x = h + l, [n_fixed][TW] fp16
     uint32_t *ysp;              // split ratings s_y (y - y_shift) = h + l, (h | l << 16) [nnz]
 };
@@ -542,6 +543,8 @@ __global__ void __launch_bounds__(512, 1)
         team_bar(team);
         const TaskSh cur = tsh[team];
         if (cur.task >= q.n_tasks) break;
+        // the list is sorted by length: every later task is k_als_dual's too
+        if (w.dual_cut > 0 && cur.slot < 0 && cur.n <= w.dual_cut) break;
         const int row = cur.row;
         const int64_t k0 = cur.k0;
         const int n = cur.n;
@@ -1222,7 +1225,7 @@ size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed, int64_t nnz) {
 }
 
 int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
-                  int64_t nnz, cudaStream_t s) {
+                  int64_t nnz, int dual_cut, cudaStream_t s) {
     if (ws_bytes < tc_workspace_bytes(p.D, slots, p.n_fixed, nnz)) {
         set_error("mcf_als_half_step: workspace too small for the tensor-core path");
         return MCF_E_WORKSPACE;
@@ -1238,6 +1241,7 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     w.n_slots = slots;
     w.prof = nullptr;
     w.team_limit = getenv("MCF_TC_TEAMS") ? atoi(getenv("MCF_TC_TEAMS")) : 4;
+    w.dual_cut = dual_cut;
     if (getenv("MCF_TC_PROF")) {
         static unsigned long long *buf = nullptr;
         if (!buf) cudaMalloc(&buf, 80 * sizeof(unsigned long long));
