@@ -446,8 +446,8 @@ __global__ void __launch_bounds__(512, 1)
     for (int e = threadIdx.x; e < (C::SMEM - 1024) / 16; e += blockDim.x)
         reinterpret_cast<uint4 *>(smem)[e] = make_uint4(0u, 0u, 0u, 0u);
     if (m == 0) {
-        // full: the team's 128 cp.async completion arrivals
-        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 128);
+        // full: the 96 cp.async completion arrivals of the team's three copying warps
+        for (int st = 0; st < NST; ++st) mbar_init(fbar0 + 8 * st, 96);
         for (int st = NST; st <= 2 * NST; ++st) mbar_init(fbar0 + 8 * st, 1);   // empty, chol: commits
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -585,95 +585,90 @@ __global__ void __launch_bounds__(512, 1)
             tmem_wait_st();
         }
         if (nst > 0) {
-            // Team-wide cp.async pipeline over the split tables: per stage each
-            // warp copies 4 ratings' rows, a lane per 16-byte chunk (lanes 0-15
-            // the h row, 16-31 the l row), straight into the SWIZZLE_128B
-            // MN-major tiles (chunk index XOR row-in-atom).  Completion is
-            // tracked by the stage's full barrier (cp.async.mbarrier.arrive:
-            // nobody waits for its own copies); a thread only waits when the
-            // slot it refills still feeds MMAs.  Thread 0 issues the MMAs of
-            // the stage LEAD behind the newest and commits them to the stage's
-            // empty barrier.
-            constexpr int LEAD = NST - C::MMA_DEPTH;
+            // cp.async pipeline over the split tables, warp-specialised.  The
+            // team's lead warp only issues MMAs: it waits for a stage's full
+            // barrier, issues C += H H^T + H L^T + L H^T and rhs += (H + L) [y_h y_l]
+            // and commits them to the slot's empty barrier -- never waiting for an
+            // MMA to finish.  The three other warps copy: warp rank c takes
+            // ratings c, c + 3, ... of a stage, a lane per 16-byte chunk (lanes 0-15
+            // the h row, 16-31 the l row), straight into the SWIZZLE_128B MN-major
+            // tiles (chunk index XOR row-in-atom), rank 0 also the rating tile;
+            // they run up to NST stages ahead, gated only by the empty barrier
+            // of the slot they refill.  Completion is tracked by the stage's full
+            // barrier (cp.async.mbarrier.arrive, 96 arrivals).
             const int tab = lane >> 4, cc = lane & 15, at = cc >> 3, c8 = cc & 7;
             // chunks past DP only feed Gram rows / columns >= DP (never read): not copied
             const bool chunk_ok = cc < DP / 8;
             const __half *tsrc = (tab ? w.tl : w.th) + 8 * cc;
-            uint32_t doff[4];   // smem offsets of this thread's 4 chunks in a stage
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int kk = 4 * wq + j, r = kk & 7;
-                doff[j] = tab * C::HT + (kk >> 3) * (C::NA * 1024) + at * 1024 + r * 128 + ((c8 ^ r) << 4);
-            }
-            // Partner ids: one coalesced load per warp per 8 stages -- lane l holds
-            // the id of rating 4 wq + (l & 3) of stage 8 blk + (l >> 2) -- a block
-            // ahead of its use; a stage's 4 ids are shuffled out of it.  (A load
-            // per id per stage with its clamp and 64-bit address was ~40 of the
-            // ~250 instructions every warp issued per stage: the Gram loop was
-            // issue-bound, 16 warps x 250 instructions per 16 ratings.)
-            auto load_idblk = [&](int blk) {
-                const int k = 16 * (8 * blk + (lane >> 2)) + 4 * wq + (lane & 3);
-                return __ldg(p.idx + k0 + min(k, n - 1));
-            };
-            int idc = load_idblk(0), idnx = load_idblk(1);
-            const uint32_t *ysrc = w.ysp + k0;
-            const uint32_t ydst = 2 * C::HT + (m >> 3) * 256 + (m & 7) * 16;
-            // slot / generation of the next stage to issue and to consume
-            unsigned ib = gst % NST, iq = gst / NST, cb = ib, cq = iq;
-            auto issue = [&](int t) {   // stage t -> slot ib
-                if ((t & 7) == 0 && t > 0) {
-                    idc = idnx;
-                    idnx = load_idblk((t >> 3) + 1);
+            const int crank = (wq - lead - 1) & 3;   // 0..2 for the copying warps
+            unsigned sb = gst % NST, sq = gst / NST;   // slot / generation of the warp's next stage
+            if (wq == lead) {
+                for (int st = 0; st < nst; ++st) {
+                    if (lane == 0) {
+                        mbar_wait(fbar0 + 8 * sb, sq & 1);   // every copy + the rating tile landed
+                        tc_fence_after();
+                        const uint32_t ha = tbs + sb * C::STAGE;
+                        const uint64_t dh = sdesc_sw128(ha, 1024, C::NA * 1024);
+                        const uint64_t dl = sdesc_sw128(ha + C::HT, 1024, C::NA * 1024);
+                        const uint64_t dy = sdesc(ha + 2 * C::HT, 256, 128);
+                        const uint32_t acc = st > 0 ? 1u : 0u;
+                        umma(tmem, dh, dh, id_gram, acc);
+                        umma(tmem, dh, dl, id_gram, 1u);
+                        umma(tmem, dl, dh, id_gram, 1u);
+                        umma(tmem + DP, dh, dy, id_rhs, acc);
+                        umma(tmem + DP, dl, dy, id_rhs, 1u);
+                        umma_commit(ebar0 + 8 * sb);
+                    }
+                    if (++sb == NST) {
+                        sb = 0;
+                        ++sq;
+                    }
                 }
-                int ids[4];
+                __syncwarp();
+            } else {
+                uint32_t doff[6];   // smem offsets of this thread's chunks in a stage
 #pragma unroll
-                for (int j = 0; j < 4; ++j) ids[j] = __shfl_sync(FULL, idc, 4 * (t & 7) + j);
-                if (iq > 0) warp_mbar_wait(ebar0 + 8 * ib, (iq - 1) & 1);
-                const uint32_t sts = tbs + ib * C::STAGE;
-                const int rem = n - 16 * t - 4 * wq;   // ratings left for this warp's 4 rows
-                if (chunk_ok) {
+                for (int j = 0; j < 6; ++j) {
+                    const int kk = crank + 3 * j, r = kk & 7;
+                    doff[j] = tab * C::HT + ((kk >> 3) & 1) * (C::NA * 1024) + at * 1024 + r * 128 + ((c8 ^ r) << 4);
+                }
+                // Partner ids: one coalesced load per warp per 2 stages (lane l holds
+                // rating 32 blk + l), two blocks ahead of its use; a stage's ids are
+                // shuffled out of the block
+                auto load_idblk = [&](int blk) { return __ldg(p.idx + k0 + min(32 * blk + lane, n - 1)); };
+                int ida = load_idblk(0), idb = load_idblk(1), idc = load_idblk(2);
+                const uint32_t *ysrc = w.ysp + k0;
+                const uint32_t ydst = 2 * C::HT + (lane >> 3) * 256 + (lane & 7) * 16;
+                for (int t = 0; t < nst; ++t) {
+                    if ((t & 1) == 0 && t > 0) {
+                        ida = idb;
+                        idb = idc;
+                        idc = load_idblk((t >> 1) + 2);
+                    }
+                    if (sq > 0) warp_mbar_wait(ebar0 + 8 * sb, (sq - 1) & 1);   // the slot's MMAs are done
+                    const uint32_t sts = tbs + sb * C::STAGE;
+                    const int l0 = 16 * (t & 1) + crank, rem = n - 16 * t - crank;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sts + doff[j]),
-                                     "l"(tsrc + (size_t)ids[j] * C::TW), "r"(j < rem ? 16 : 0));
-                }
-                if (m < 16)   // rating tile: (k = m, n = 0 / 1) = (y_h, y_l); columns 2..15 are never read
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sts + ydst),
-                                 "l"(ysrc + min(16 * t + m, n - 1)), "r"(16 * t + m < n ? 4 : 0));
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar0 + 8 * ib)
-                             : "memory");
-                if (++ib == NST) {
-                    ib = 0;
-                    ++iq;
-                }
-            };
-#pragma unroll
-            for (int t = 0; t < LEAD; ++t)
-                if (t < nst) issue(t);
-            for (int st = 0; st < nst; ++st) {
-                if (st + LEAD < nst) issue(st + LEAD);
-                if (m == 32 * lead) {
-                    mbar_wait(fbar0 + 8 * cb, cq & 1);   // every copy + the rating tile landed
-                    tc_fence_after();
-                    const uint32_t ha = tbs + cb * C::STAGE;
-                    const uint64_t dh = sdesc_sw128(ha, 1024, C::NA * 1024);
-                    const uint64_t dl = sdesc_sw128(ha + C::HT, 1024, C::NA * 1024);
-                    const uint64_t dy = sdesc(ha + 2 * C::HT, 256, 128);
-                    const uint32_t acc = st > 0 ? 1u : 0u;
-                    umma(tmem, dh, dh, id_gram, acc);
-                    umma(tmem, dh, dl, id_gram, 1u);
-                    umma(tmem, dl, dh, id_gram, 1u);
-                    umma(tmem + DP, dh, dy, id_rhs, acc);
-                    umma(tmem + DP, dl, dy, id_rhs, 1u);
-                    umma_commit(ebar0 + 8 * cb);
-                }
-                if (++cb == NST) {
-                    cb = 0;
-                    ++cq;
+                    for (int j = 0; j < 6; ++j) {
+                        const int id = __shfl_sync(FULL, ida, (l0 + 3 * j) & 31);
+                        if (chunk_ok && crank + 3 * j < 16)
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sts + doff[j]),
+                                         "l"(tsrc + (size_t)id * C::TW), "r"(3 * j < rem ? 16 : 0));
+                    }
+                    if (crank == 0 && lane < 16)
+                        // rating tile: (k = lane, n = 0 / 1) = (y_h, y_l); columns 2..15 are never read
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sts + ydst),
+                                     "l"(ysrc + min(16 * t + lane, n - 1)), "r"(16 * t + lane < n ? 4 : 0));
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar0 + 8 * sb)
+                                 : "memory");
+                    if (++sb == NST) {
+                        sb = 0;
+                        ++sq;
+                    }
                 }
             }
-            // last MMAs done (the stage before (cb, cq))
-            warp_mbar_wait(ebar0 + 8 * (cb == 0 ? NST - 1 : cb - 1), (cb == 0 ? cq - 1 : cq) & 1);
+            // last MMAs done (the stage before (sb, sq))
+            warp_mbar_wait(ebar0 + 8 * (sb == 0 ? NST - 1 : sb - 1), (sb == 0 ? sq - 1 : sq) & 1);
         }
         gst += (unsigned)nst;
         tc_fence_before();
