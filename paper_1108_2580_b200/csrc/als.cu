@@ -881,6 +881,7 @@ __device__ __forceinline__ void tile_warp_item(const AlsParams &p, int64_t item,
     using C = TileWarpCfg<NB8>;
     constexpr int S = C::S, LDK = C::LDK, BT = C::BT;
     const ItemInfo it = item_info(p, item);
+    if (p.skip_min_n > 0 && it.n >= p.skip_min_n) return;   // the tensor-core kernel's row
     const int D = p.D;
     const int nb4_real = (D + 3) / 4;
 
@@ -2505,7 +2506,8 @@ extern "C" size_t mcf_als_workspace_bytes_fixed(int32_t n_list, int64_t slots, i
     }
     const size_t obj = sizeof(double) * 2 * ((size_t)n_list + (size_t)slots + 64);
     size_t part = sizeof(float) * (size_t)slots * per;
-    if (D >= tc_min_d() && D <= 128 && n_fixed > 0) part = std::max(part, tc_workspace_bytes(D, slots, n_fixed, nnz));
+    if ((D >= tc_min_d() || tc_hybrid_min_n(D, false) > 0) && D <= 128 && n_fixed > 0)
+        part = std::max(part, tc_workspace_bytes(D, slots, n_fixed, nnz));
     return align_up(sizeof(int32_t) * ((size_t)n_list + 64), 256) + align_up(obj, 256) + part;
 }
 
@@ -2667,6 +2669,27 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         return launch_als_dual(p, q, p.counters + n_list + 3, cut, s);
     }
     if (total_items == 0) return MCF_OK;
+    // hybrid (49 <= D < 64, workspace with the split tables): long rows on the
+    // tensor-core kernel, the rest on the CUDA-core kernels
+    // (a row longer than the plan's chunk is a hot row: its chunks are tensor-core tasks)
+    const int hyb = (!p.schur && p.D > 28) ? std::min(tc_hybrid_min_n(p.D, wts != nullptr), chunk + 1) : 0;
+    if (hyb > 0 && ws_bytes >= fixed_part + tc_workspace_bytes(p.D, plan_info[3], n_fixed, plan_info[5]) &&
+        plan_info[2] > 0) {
+        PairPlan q{};
+        q.task_row = L.task_row;
+        q.task_k0 = L.task_k0;
+        q.task_n = L.task_n;
+        q.task_slot = L.task_slot;
+        q.n_tasks = plan_info[2];
+        q.sorted_j = L.sorted_j;
+        q.hoff = L.hch;
+        q.n_heavy = plan_info[4];
+        q.group_counter = p.counters + n_list;
+        if ((rc = launch_als_tc(p, q, p.partials, ws_bytes - fixed_part, plan_info[3], plan_info[5],
+                                hyb - 1, s)))
+            return rc;
+        p.skip_min_n = hyb;
+    }
     return wts ? dispatch<true>(p, s) : dispatch<false>(p, s);
 }
 

@@ -58,6 +58,9 @@ struct AlsParams {
     // pair Schur path: partner rows [x | 1 | t], the rating's target is
     // y - y_shift - t (the per-rating MFITR bias terms folded into the gather)
     int ysub;
+    // hybrid wide path (49 <= D < 64): rows with at least skip_min_n ratings are
+    // solved by the tensor-core kernel, the CUDA-core kernels skip them (0: none)
+    int skip_min_n;
 };
 constexpr int EMIT_STRIDE = 256;
 
@@ -135,6 +138,8 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 // tensor-core wide path (als_tc.cu): 21 <= D <= 127, no per-observation weights
 bool tc_path(int D, bool weighted);
 int tc_min_d();
+// 49 <= D < tc_min_d(): rows this long go to the tensor-core kernel (0: hybrid off)
+int tc_hybrid_min_n(int D, bool weighted);
 size_t tc_workspace_bytes(int D, int64_t slots, int64_t n_fixed, int64_t nnz);
 int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_bytes, int64_t slots,
                   int64_t nnz, int dual_cut, cudaStream_t s);

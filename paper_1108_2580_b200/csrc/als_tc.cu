@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(512, 1)
         team_bar(team);
         const TaskSh cur = tsh[team];
         if (cur.task >= q.n_tasks) break;
-        // the list is sorted by length: every later task is k_als_dual's too
+        // the list is sorted by length: every later task is within the cut too
         if (w.dual_cut > 0 && cur.slot < 0 && cur.n <= w.dual_cut) break;
         const int row = cur.row;
         const int64_t k0 = cur.k0;
@@ -1199,6 +1199,19 @@ int tc_min_d() {
         return d < 49 ? 49 : d;
     }();
     return v;
+}
+
+// Hybrid experiment for 49 <= D < tc_min_d(): rows with at least
+// MCF_TC_HYBRID_MIN_N ratings (and every hot-row chunk) take the tensor-core
+// kernel, the others the CUDA-core tile-warp kernel.  Off by default (0):
+// measured at config 4 (D = 50) 267 ms against 254 ms for the tile-warp kernel
+// alone -- at DP = 64 the tensor-core Gram is bound by its per-stage cost,
+// not by the gather bandwidth (profiles/r2_tc_path_notes.txt).
+int tc_hybrid_min_n(int D, bool weighted) {
+    const char *e = getenv("MCF_TC_HYBRID_MIN_N");
+    const int v = e ? atoi(e) : 0;
+    if (weighted || D < 49 || D >= tc_min_d() || getenv("MCF_NO_TC")) return 0;
+    return v > 0 ? std::max(v, 2) : 0;
 }
 
 bool tc_path(int D, bool weighted) {

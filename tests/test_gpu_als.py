@@ -318,6 +318,71 @@ def test_heavy_row_multi_chunk_and_determinism():
         assert row < REL_TOL and mx < REL_TOL, (row, mx)
 
 
+@pytest.mark.parametrize("D,chunk", [(50, None), (56, 512), (63, 2048)])
+def test_hybrid_wide_path_long_rows_on_tensor_cores(D, chunk):
+    """49 <= D < 64 with MCF_TC_HYBRID_MIN_N=256: rows with >= 256 ratings (and
+    every hot-row chunk) take the tensor-core kernel, the others the tile-warp
+    kernel; both half-steps vs the float64 oracle, and against the default
+    (CUDA-core-only) run."""
+    U, I = 6000, 60
+    u, i, s = _random_split(U, I, 150_000, 7, hot=5)     # items ~2500 ratings, users ~25
+    rng = np.random.default_rng(4)
+    P0, Q0 = rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D))
+    outs = {}
+    for mode in ("hybrid", "cuda"):
+        if mode == "hybrid":
+            os.environ["MCF_TC_HYBRID_MIN_N"] = "256"   # an experiment knob: off by default
+        try:
+            eng = _engine(u, i, s, U, I, D, chunk=chunk)
+            eng.set_factors(P0, Q0)
+            eng.half_step("items", 0.0, 0.065)
+            eng.check()
+            Q1 = eng.factors()[1].double().cpu().numpy()
+            eng.half_step("users", 0.0, 0.065)
+            eng.check()
+            outs[mode] = (Q1, eng.factors()[0].double().cpu().numpy())
+        finally:
+            os.environ.pop("MCF_TC_HYBRID_MIN_N", None)
+    P32 = torch.as_tensor(P0, dtype=torch.float32).double().numpy()
+    refQ, _ = oracle.als_half_step(P32, outs["hybrid"][0], u, i, s, "items", lam_n=0.065)
+    refP, _ = oracle.als_half_step(P32, outs["hybrid"][0], u, i, s, "users", lam_n=0.065)
+    for mode, (Q1, P1) in outs.items():
+        row, mx = _rel_rows(Q1, refQ)
+        assert row < REL_TOL and mx < REL_TOL, (mode, "items", row, mx)
+    row, mx = _rel_rows(outs["hybrid"][1], refP)
+    assert row < REL_TOL and mx < REL_TOL, ("users", row, mx)
+    assert not np.array_equal(outs["hybrid"][0], outs["cuda"][0])   # the long rows did change kernels
+
+
+@pytest.mark.parametrize("D", [64, 100, 128])
+def test_short_rows_dual_warp_kernel(D):
+    """D >= 64: rows with n <= 32 ratings are solved by k_als_dual (dual form,
+    warp per row); n in 33..64 by the tensor-core kernel's dual form; checked
+    against the float64 oracle and the run without the warp kernel."""
+    U, I = 3000, 400
+    u, i, s = _random_split(U, I, 60_000, 9, hot=3)      # users ~20 ratings, items ~150
+    rng = np.random.default_rng(5)
+    P0, Q0 = rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D))
+    outs = {}
+    for mode in ("dual", "tc"):
+        if mode == "tc":
+            os.environ["MCF_NO_DUAL_WARP"] = "1"
+        try:
+            eng = _engine(u, i, s, U, I, D)
+            eng.set_factors(P0, Q0)
+            eng.half_step("users", 0.0, 0.065)
+            eng.check()
+            outs[mode] = eng.factors()[0].double().cpu().numpy()
+        finally:
+            os.environ.pop("MCF_NO_DUAL_WARP", None)
+    Q32 = torch.as_tensor(Q0, dtype=torch.float32).double().numpy()
+    ref, _ = oracle.als_half_step(np.zeros((U, D)), Q32, u, i, s, "users", lam_n=0.065)
+    for mode, P1 in outs.items():
+        row, mx = _rel_rows(P1, ref)
+        assert row < REL_TOL and mx < REL_TOL, (mode, row, mx)
+    assert not np.array_equal(outs["dual"], outs["tc"])
+
+
 def test_empty_rows_and_zero_rating_rows():
     U, I, D = 50, 40, 6
     u, i, s = _random_split(U - 10, I - 10, 600, 5)      # last 10 users / items empty
