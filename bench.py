@@ -139,7 +139,8 @@ def kernel_name(D: int) -> str:
     from paper_1108_2580_b200.device import tc_path
     if tc_path(D):
         return ("k_als_tc<NBLK> (tcgen05 kind::f16 Gram, fp16 h/l split, TMEM-resident blocked "
-                "Cholesky with negated-MMA trailing updates; + k_tc_prep)")
+                "Cholesky with negated-MMA trailing updates; + k_tc_prep, k_tc_split; rows with "
+                "n <= 32 ratings: k_als_dual<1>, dual form on CUDA cores)")
     if D <= 20:
         return "k_als_pair<5,4> (fused Gram + lam*n + Cholesky + solve; + k_als_heavy for hot rows)"
     if D <= 28:
@@ -181,13 +182,17 @@ def roofline_for(D, bytes_launch, flops_launch, launch_s, traffic=None, kernel=N
 
 def launches_per_sweep(eng) -> int:
     """libmcf kernels per sweep: per half-step the row kernel, plus the hot-row
-    reduce kernel when the layout has hot rows (D <= 20 path) or the scale
-    pre-pass (tensor-core path)."""
+    reduce kernel when the layout has hot rows (D <= 20 path); on the
+    tensor-core path the scale pre-pass, the table split, the tensor-core
+    kernel and the short-row dual kernel."""
     from paper_1108_2580_b200.device import tc_path
     n = 0
     for lay in (eng.r.by_item, eng.r.by_user):
         info = lay.plan()[1]
-        n += 1 + (1 if (eng.D <= 20 and info[4] > 0) or tc_path(eng.D) else 0)
+        if tc_path(eng.D):
+            n += 4      # k_tc_prep, k_tc_split, k_als_tc, k_als_dual<1>
+        else:
+            n += 1 + (1 if (eng.D <= 20 and info[4] > 0) else 0)
     return n
 
 

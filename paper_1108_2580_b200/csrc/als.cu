@@ -2666,7 +2666,7 @@ static int half_step_impl(const int64_t *ptr, const int32_t *idx, const float *v
         const int cut = als_dual_cut(p, wts != nullptr);
         if ((rc = launch_als_tc(p, q, p.partials, ws_bytes - fixed_part, plan_info[3], plan_info[5], cut, s)))
             return rc;
-        return launch_als_dual(p, q, p.counters + n_list + 3, cut, s);
+        return launch_als_dual(p, q, plan_info[3], p.counters + n_list + 3, cut, s);
     }
     if (total_items == 0) return MCF_OK;
     // hybrid (49 <= D < 64, workspace with the split tables): long rows on the

@@ -4,20 +4,26 @@
 // identity the reference's solve (reference _kernels.py:151-215)
 //     x = (X^T X + lam I)^{-1} X^T y
 // equals x = X^T alpha with (X X^T + lam I) alpha = y, an n x n system
-// instead of D x D.  The tensor-core kernel (als_tc.cu) runs this form for
-// n <= 64, but a 128-thread team per row is latency-bound there (~50 k cycles
-// per row at D = 100, 4 rows per SM in flight).  This kernel takes the rows
-// with n <= DN = 32 -- the tail of the plan's length-sorted task list: one
-// WARP per row, the gathered partner rows transposed into shared memory,
-// K = X X^T accumulated with lane i owning row i of K in registers (FFMA2),
-// Cholesky by shuffles (right-looking, the reference's > 0 and finite pivot
-// test), both substitutions, x = X^T alpha and one refinement step in the
-// dual space (rho = y - X x - lam alpha; the rank-deficient short-row systems
-// have cond ~ 5e3, fp32 rounding of K alone exceeds the 1e-4 budget).
+// instead of D x D.  The tensor-core kernel (als_tc.cu) has this form too,
+// but a 128-thread team per row is latency-bound there (~50-60 k cycles per
+// row at D = 100, 4 rows per SM in flight).  These kernels take the rows with
+// n <= 64 -- the tail of the plan's length-sorted task list: one WARP per
+// row, the gathered partner rows transposed into shared memory, K = X X^T
+// accumulated with lane i owning rows i (and i + 32) of K in registers
+// (FFMA2), Cholesky by shuffles (right-looking, the reference's > 0 and
+// finite pivot test) with the forward substitution fused, back substitution,
+// x = X^T alpha and one refinement step in the dual space (rho = y - X x -
+// lam alpha: the rank-deficient short-row systems have cond ~ 5e3, fp32
+// rounding of K alone exceeds the 1e-4 budget).
+//
+// k_als_dual<1> takes n <= 32 (11 rows per SM in flight at D = 100);
+// k_als_dual<2> (33 <= n <= 64, two row sets per lane, 4 rows per SM) is
+// built but off by default (MCF_DUAL_WARP_MAX=64): at 4 warps per SM it is
+// latency-bound and slower than the tensor-core kernel's dual form.
 //
 // Eligible calls: no taxonomy terms, no bias coordinate, no observation
-// weights, D > DN (so n < D for every row taken).  Tasks are taken from the
-// END of the task list (shortest first) until one is longer than the cut; the
+// weights, every row taken has n < D.  The light tasks are sorted by length:
+// each kernel bisects for its first task and walks towards the tail; the
 // tensor-core kernel stops at the first light task within the cut.
 
 #include <algorithm>
@@ -28,9 +34,13 @@
 namespace mcf {
 namespace {
 
-constexpr int DN = 32;     // longest row on this path (one rating per lane)
-constexpr int XS = 36;     // Xt row stride: 16-byte aligned rows, an odd number of 16-byte units
-constexpr int LSTR = 33;   // L row stride (conflict-free rows and columns)
+template <int S>
+struct DualCfg {
+    static constexpr int N = 32 * S;       // longest row (S ratings per lane)
+    static constexpr int XS = N + 4;       // Xt row stride: 16-byte rows, an odd number of 16-byte units
+    static constexpr int LSTR = N + 1;     // L row stride (conflict-free rows and columns)
+    static size_t smem_bytes(int ld) { return sizeof(float) * (size_t)(ld * XS + N * LSTR + N + 128); }
+};
 
 __device__ __forceinline__ void ffma2d(float &x, float &y, float a, float bx, float by) {
     unsigned long long A, B, C;
@@ -41,37 +51,80 @@ __device__ __forceinline__ void ffma2d(float &x, float &y, float a, float bx, fl
     asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(C));
 }
 
-// K[lane][0 .. 4 NB4) += sum_f Xt[f][lane] * Xt[f][j]
-template <int NB4>
-__device__ __forceinline__ void dual_gram(const float *Xt, int D, int lane, float (&kr)[DN]) {
+// kr[s][0 .. 4 NB4) += sum_f Xt[f][lane + 32 s] * Xt[f][j]; only the lower
+// triangle is used, so row set s stops at column 32 (s + 1)
+template <int S, int NB4>
+__device__ __forceinline__ void dual_gram(const float *Xt, int D, int lane, float (&kr)[S][32 * S]) {
+    constexpr int XS = DualCfg<S>::XS;
 #pragma unroll 2
     for (int f = 0; f < D; ++f) {
-        const float a = Xt[f * XS + lane];
+        float a[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) a[s] = Xt[f * XS + lane + 32 * s];
         const float4 *b = reinterpret_cast<const float4 *>(Xt + f * XS);
 #pragma unroll
         for (int j4 = 0; j4 < NB4; ++j4) {
             const float4 bv = b[j4];
-            ffma2d(kr[4 * j4], kr[4 * j4 + 1], a, bv.x, bv.y);
-            ffma2d(kr[4 * j4 + 2], kr[4 * j4 + 3], a, bv.z, bv.w);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (4 * j4 < 32 * (s + 1)) {
+                    ffma2d(kr[s][4 * j4], kr[s][4 * j4 + 1], a[s], bv.x, bv.y);
+                    ffma2d(kr[s][4 * j4 + 2], kr[s][4 * j4 + 3], a[s], bv.z, bv.w);
+                }
+            }
         }
     }
 }
 
-// L^T a = z, column-oriented from the packed rows in shared memory
-__device__ __forceinline__ float dual_back(float z, const float *Ls, float myinv, int n, int lane) {
-    float a = z;
-    for (int k = n - 1; k >= 0; --k) {
-        const float ak = __shfl_sync(FULL, a, k) * __shfl_sync(FULL, myinv, k);
-        if (lane == k) a = ak;
-        else if (lane < k) a = fmaf(-Ls[k * LSTR + lane], ak, a);
+// value of row k of a lane-distributed vector v[s] (row i = lane + 32 s)
+template <int S>
+__device__ __forceinline__ float row_bcast(const float (&v)[S], int k) {
+    float r = __shfl_sync(FULL, v[0], k & 31);
+#pragma unroll
+    for (int s = 1; s < S; ++s) {
+        const float t = __shfl_sync(FULL, v[s], k & 31);
+        if ((k >> 5) == s) r = t;
     }
-    return a;
+    return r;
 }
 
-// x[lane + 32 c] = sum_j Xt[lane + 32 c][j] * al[j]   (c < 4; rows >= ld read as 0)
-template <bool ADD>
+// L^T a = z, column-oriented from the L rows in shared memory
+template <int S>
+__device__ __forceinline__ void dual_back(float (&a)[S], const float *Ls, const float (&myinv)[S], int n,
+                                          int lane) {
+    constexpr int LSTR = DualCfg<S>::LSTR;
+    for (int k = n - 1; k >= 0; --k) {
+        const float ak = row_bcast<S>(a, k) * row_bcast<S>(myinv, k);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int i = lane + 32 * s;
+            if (i == k) a[s] = ak;
+            else if (i < k) a[s] = fmaf(-Ls[k * LSTR + i], ak, a[s]);
+        }
+    }
+}
+
+// L w = r, column-oriented
+template <int S>
+__device__ __forceinline__ void dual_fwd(float (&r)[S], const float *Ls, const float (&myinv)[S], int n,
+                                         int lane) {
+    constexpr int LSTR = DualCfg<S>::LSTR;
+    for (int k = 0; k < n; ++k) {
+        const float wk = row_bcast<S>(r, k) * row_bcast<S>(myinv, k);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int i = lane + 32 * s;
+            if (i == k) r[s] = wk;
+            else if (i > k) r[s] = fmaf(-Ls[i * LSTR + k], wk, r[s]);
+        }
+    }
+}
+
+// x[lane + 32 c] (+)= sum_j Xt[lane + 32 c][j] * al[j]   (c < 4; rows >= ld read as 0)
+template <int S, bool ADD>
 __device__ __forceinline__ void dual_xt(const float *Xt, const float *al, int nb4, int ld, int lane,
                                         float (&x)[4]) {
+    constexpr int XS = DualCfg<S>::XS;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const int f = lane + 32 * c;
@@ -89,23 +142,36 @@ __device__ __forceinline__ void dual_xt(const float *Xt, const float *al, int nb
     }
 }
 
-// one warp per CTA: ~20 KB of shared memory per row in flight at D = 100, 11 rows per SM
-__global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int *counter, int cut) {
+// One warp per CTA (shared memory per row in flight: ~20 KB for S = 1, ~44 KB
+// for S = 2 at D = 100).  Light tasks are sorted by length, longest first:
+// the warp finds the first task with n <= hi by bisection and takes tasks
+// from there while n > lo.
+template <int S>
+__global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_t first_light,
+                                                 int *counter, int lo, int hi) {
+    using C = DualCfg<S>;
+    constexpr int N = C::N, XS = C::XS, LSTR = C::LSTR;
     extern __shared__ __align__(16) float dsm[];
     const int lane = threadIdx.x & 31;
     const int D = p.D, ld = p.ld;
-    float *Xt = dsm;   // [ld][XS]: Xt[f][j] = feature f of rating j
-    float *Ls = Xt + ld * XS;                   // [DN][LSTR]: L rows
-    float *al = Ls + DN * LSTR;                 // [DN] alpha / its correction (16-byte aligned)
-    float *xs = al + DN;                        // [128] x
+    float *Xt = dsm;                  // [ld][XS]: Xt[f][j] = feature f of rating j
+    float *Ls = Xt + ld * XS;         // [N][LSTR]: L rows
+    float *al = Ls + N * LSTR;        // [N] alpha / its correction (16-byte aligned)
+    float *xs = al + N;               // [128] x
+    int64_t t0 = first_light, t1 = q.n_tasks;   // first light task with n <= hi
+    while (t0 < t1) {
+        const int64_t mid = (t0 + t1) >> 1;
+        if (q.task_n[mid] <= hi) t1 = mid;
+        else t0 = mid + 1;
+    }
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(counter, 1);
         i = __shfl_sync(FULL, i, 0);
-        const int64_t t = q.n_tasks - 1 - (int64_t)i;
-        if (t < 0) break;
+        const int64_t t = t0 + (int64_t)i;
+        if (t >= q.n_tasks) break;
         const int n = q.task_n[t];
-        if (n > cut || q.task_slot[t] >= 0) break;   // the list is sorted: nothing shorter is left
+        if (n <= lo) break;   // sorted: only shorter rows follow
         const int row = q.task_row[t];
         const int64_t k0 = q.task_k0[t];
         if (n == 0) {   // empty row: 0 with a regulariser, else singular (factor.py:535-537)
@@ -117,27 +183,30 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int *c
             continue;
         }
         const float lam_row = p.lam_c + p.lam_n * (float)n;
-        int id = 0;
-        float y = 0.f;
-        if (lane < n) {
-            id = __ldg(p.idx + k0 + lane);
-            y = __ldg(p.val + k0 + lane) - p.y_shift;
-        }
-        // gather: lane j reads its partner row in 16-byte pieces (8 in flight) and
+        float y[S];
+        // gather: lane j reads its partner rows in 16-byte pieces (8 in flight) and
         // stores them transposed (conflict-free: the lanes are consecutive columns)
-        {
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int j = lane + 32 * s;
+            int id = 0;
+            y[s] = 0.f;
+            if (j < n) {
+                id = __ldg(p.idx + k0 + j);
+                y[s] = __ldg(p.val + k0 + j) - p.y_shift;
+            }
             const float4 *src = reinterpret_cast<const float4 *>(p.fixed + (size_t)id * ld);
             const int nc4 = ld >> 2;
-            __syncwarp();
             for (int c = 0; c < nc4; c += 8) {
                 float4 v[8];
 #pragma unroll
                 for (int q4 = 0; q4 < 8; ++q4)
-                    v[q4] = (lane < n && c + q4 < nc4) ? __ldg(src + c + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    v[q4] = (j < n && c + q4 < nc4) ? __ldg(src + c + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int q4 = 0; q4 < 8; ++q4) {
                     if (c + q4 < nc4) {
-                        float *d = Xt + 4 * (c + q4) * XS + lane;
+                        float *d = Xt + 4 * (c + q4) * XS + j;
                         d[0] = v[q4].x;
                         d[XS] = v[q4].y;
                         d[2 * XS] = v[q4].z;
@@ -145,39 +214,68 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int *c
                     }
                 }
             }
-            __syncwarp();
         }
-        // K = X X^T: lane i holds row i
+        __syncwarp();
+        // K = X X^T: lane i holds rows i + 32 s
         const int nb4 = (n + 3) >> 2;
-        float kr[DN];
+        float kr[S][N];
 #pragma unroll
-        for (int j = 0; j < DN; ++j) kr[j] = 0.f;
-        if (nb4 <= 2) dual_gram<2>(Xt, D, lane, kr);
-        else if (nb4 <= 4) dual_gram<4>(Xt, D, lane, kr);
-        else if (nb4 <= 6) dual_gram<6>(Xt, D, lane, kr);
-        else dual_gram<8>(Xt, D, lane, kr);
-        // Cholesky of K + lam I (right-looking; column k of L ends up in kr[k] of the
-        // lanes below k), forward substitution fused
-        float r = y, myinv = 0.f;
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int j = 0; j < N; ++j) kr[s][j] = 0.f;
+        if (S == 1) {
+            if (nb4 <= 2) dual_gram<S, 2>(Xt, D, lane, kr);
+            else if (nb4 <= 4) dual_gram<S, 4>(Xt, D, lane, kr);
+            else if (nb4 <= 6) dual_gram<S, 6>(Xt, D, lane, kr);
+            else dual_gram<S, 8>(Xt, D, lane, kr);
+        } else {
+            if (nb4 <= 10) dual_gram<S, 10>(Xt, D, lane, kr);
+            else if (nb4 <= 12) dual_gram<S, 12>(Xt, D, lane, kr);
+            else if (nb4 <= 14) dual_gram<S, 14>(Xt, D, lane, kr);
+            else dual_gram<S, 16>(Xt, D, lane, kr);
+        }
+        // Cholesky of K + lam I (right-looking; column k of L ends up in kr[.][k] of
+        // the rows below k), forward substitution fused
+        float r[S], myinv[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            r[s] = y[s];
+            myinv[s] = 0.f;
+        }
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < DN; ++k) {
+        for (int k = 0; k < N; ++k) {
             if (k < n) {
-                const float d = __shfl_sync(FULL, kr[k], k) + lam_row;
+                const int ks = k >> 5, kl = k & 31;
+                const float d = __shfl_sync(FULL, kr[ks][k], kl) + lam_row;
                 ok = ok && d > 0.f && d < INFINITY;
                 const float inv = rsqrtf(d);
-                const float lik = kr[k] * inv;
-                if (lane == k) myinv = inv;
-                const float zk = __shfl_sync(FULL, r, k) * inv;
-                if (lane == k) r = zk;
-                else if (lane > k) r = fmaf(-lik, zk, r);
-                kr[k] = lik;
+                if (lane == kl) myinv[ks] = inv;
+                const float zk = __shfl_sync(FULL, r[ks], kl) * inv;
+                float lik[S];
 #pragma unroll
-                for (int jb = 0; jb < DN / 8; ++jb) {
+                for (int s = 0; s < S; ++s) {
+                    if (32 * (s + 1) > k) {   // row set s still has rows at or below k
+                        const int i = lane + 32 * s;
+                        lik[s] = kr[s][k] * inv;
+                        if (i == k) r[s] = zk;
+                        else if (i > k) r[s] = fmaf(-lik[s], zk, r[s]);
+                        kr[s][k] = lik[s];
+                    } else {
+                        lik[s] = 0.f;
+                    }
+                }
+#pragma unroll
+                for (int jb = 0; jb < N / 8; ++jb) {
                     if (8 * jb + 7 > k && 8 * jb < n) {
 #pragma unroll
                         for (int j = 8 * jb; j < 8 * jb + 8; ++j) {
-                            if (j > k) kr[j] = fmaf(-lik, __shfl_sync(FULL, lik, j), kr[j]);
+                            if (j > k) {
+                                const float ljk = __shfl_sync(FULL, lik[j >> 5], j & 31);
+#pragma unroll
+                                for (int s = 0; s < S; ++s)
+                                    if (32 * (s + 1) > j) kr[s][j] = fmaf(-lik[s], ljk, kr[s][j]);
+                            }
                         }
                     }
                 }
@@ -188,36 +286,44 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int *c
             continue;
         }
 #pragma unroll
-        for (int k = 0; k < DN; ++k) Ls[lane * LSTR + k] = kr[k];
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int k = 0; k < 32 * (s + 1); ++k) Ls[(lane + 32 * s) * LSTR + k] = kr[s][k];
         __syncwarp();
-        float a_sol = dual_back(r, Ls, myinv, n, lane);
-        al[lane] = a_sol;
+        float a_sol[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) a_sol[s] = r[s];
+        dual_back<S>(a_sol, Ls, myinv, n, lane);
+#pragma unroll
+        for (int s = 0; s < S; ++s) al[lane + 32 * s] = a_sol[s];
         __syncwarp();
         float x[4];
-        dual_xt<false>(Xt, al, nb4, ld, lane, x);
+        dual_xt<S, false>(Xt, al, nb4, ld, lane, x);
         // one refinement step in the dual space
 #pragma unroll
         for (int c = 0; c < 4; ++c) xs[lane + 32 * c] = x[c];
         __syncwarp();
-        float dot0 = 0.f, dot1 = 0.f;
-        for (int f = 0; f < D; f += 4) {   // D <= ld, ld a multiple of 4; rows D.. of Xt are zero
-            const float4 xv = *reinterpret_cast<const float4 *>(xs + f);
-            dot0 = fmaf(Xt[f * XS + lane], xv.x, dot0);
-            dot1 = fmaf(Xt[(f + 1) * XS + lane], xv.y, dot1);
-            dot0 = fmaf(Xt[(f + 2) * XS + lane], xv.z, dot0);
-            dot1 = fmaf(Xt[(f + 3) * XS + lane], xv.w, dot1);
+        float rr[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int j = lane + 32 * s;
+            float dot0 = 0.f, dot1 = 0.f;
+            for (int f = 0; f < D; f += 4) {   // D <= ld, ld a multiple of 4; rows D.. of Xt are zero
+                const float4 xv = *reinterpret_cast<const float4 *>(xs + f);
+                dot0 = fmaf(Xt[f * XS + j], xv.x, dot0);
+                dot1 = fmaf(Xt[(f + 1) * XS + j], xv.y, dot1);
+                dot0 = fmaf(Xt[(f + 2) * XS + j], xv.z, dot0);
+                dot1 = fmaf(Xt[(f + 3) * XS + j], xv.w, dot1);
+            }
+            rr[s] = j < n ? y[s] - (dot0 + dot1) - lam_row * a_sol[s] : 0.f;
         }
-        float rr = lane < n ? y - (dot0 + dot1) - lam_row * a_sol : 0.f;
-        for (int k = 0; k < n; ++k) {   // L w = rho
-            const float wk = __shfl_sync(FULL, rr, k) * __shfl_sync(FULL, myinv, k);
-            if (lane == k) rr = wk;
-            else if (lane > k) rr = fmaf(-Ls[lane * LSTR + k], wk, rr);
-        }
-        const float da = dual_back(rr, Ls, myinv, n, lane);
+        dual_fwd<S>(rr, Ls, myinv, n, lane);
+        dual_back<S>(rr, Ls, myinv, n, lane);
         __syncwarp();
-        al[lane] = da;
+#pragma unroll
+        for (int s = 0; s < S; ++s) al[lane + 32 * s] = rr[s];
         __syncwarp();
-        dual_xt<true>(Xt, al, nb4, ld, lane, x);
+        dual_xt<S, true>(Xt, al, nb4, ld, lane, x);
         bool fin = true;
 #pragma unroll
         for (int c = 0; c < 4; ++c) fin = fin && isfinite(x[c]);
@@ -233,32 +339,50 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int *c
     }
 }
 
-}  // namespace
-
-// rows with at most this many ratings leave the tensor-core kernel for
-// k_als_dual (0: the call is not eligible)
-int als_dual_cut(const AlsParams &p, bool weighted) {
-    if (weighted || p.tax_T || p.tax_S || p.bias_dim >= 0 || p.schur || p.D <= DN || p.D > 128 ||
-        getenv("MCF_NO_DUAL_WARP"))
-        return 0;
-    return DN;
-}
-
-int launch_als_dual(const AlsParams &p, const PairPlan &q, int *counter, int cut, cudaStream_t s) {
-    if (cut <= 0 || q.n_tasks == 0) return MCF_OK;
-    const size_t smem = sizeof(float) * (size_t)(p.ld * XS + DN * LSTR + DN + 128);
+template <int S>
+int launch_dual(const AlsParams &p, const PairPlan &q, int64_t first_light, int *counter, int lo, int hi,
+                cudaStream_t s) {
+    const size_t smem = DualCfg<S>::smem_bytes(p.ld);
     static size_t attr = 0;
     if (smem > attr) {
-        cudaFuncSetAttribute(k_als_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_als_dual<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_dual, 32, smem);
-    const int64_t grid = std::min<int64_t>(q.n_tasks, (int64_t)sms * std::max(per_sm, 1));
-    k_als_dual<<<(unsigned)grid, 32, smem, s>>>(p, q, counter, cut);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_dual<S>, 32, smem);
+    const int64_t grid = std::min<int64_t>(q.n_tasks - first_light, (int64_t)sms * std::max(per_sm, 1));
+    if (grid > 0) k_als_dual<S><<<(unsigned)grid, 32, smem, s>>>(p, q, first_light, counter, lo, hi);
     return check_launch("mcf_als_half_step(dual rows)");
+}
+
+}  // namespace
+
+// rows with at most this many ratings leave the tensor-core kernel for
+// k_als_dual (0: the call is not eligible).  MCF_DUAL_WARP_MAX: 0 / 32 / 64.
+int als_dual_cut(const AlsParams &p, bool weighted) {
+    // default 32: k_als_dual<2> fits 4 warps per SM (44 KB of shared memory per
+    // row) and is latency-bound there -- config 3: 17 ms per half-step for the
+    // 33..64 rows against ~9 ms on the tensor-core kernel's dual form
+    const char *e = getenv("MCF_DUAL_WARP_MAX");
+    int mx = e ? atoi(e) : 32;
+    if (p.D <= 64) mx = std::min(mx, 32);   // every row taken must have n < D
+    if (weighted || p.tax_T || p.tax_S || p.bias_dim >= 0 || p.schur || p.D <= 32 || p.D > 128 ||
+        getenv("MCF_NO_DUAL_WARP") || mx < 32)
+        return 0;
+    return mx >= 64 ? 64 : 32;
+}
+
+// counters: two zeroed ints (one per kernel); first_light: index of the
+// first light task (= number of hot-row chunks)
+int launch_als_dual(const AlsParams &p, const PairPlan &q, int64_t first_light, int *counters, int cut,
+                    cudaStream_t s) {
+    if (cut <= 0 || q.n_tasks <= first_light) return MCF_OK;
+    int rc = MCF_OK;
+    // the longer rows first (33..64), then the tail
+    if (cut > 32 && (rc = launch_dual<2>(p, q, first_light, counters + 1, 32, 64, s))) return rc;
+    return launch_dual<1>(p, q, first_light, counters, -1, 32, s);
 }
 
 }  // namespace mcf

@@ -148,6 +148,7 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
 // light tasks with at most als_dual_cut() ratings (0: call not eligible) are
 // left by the tensor-core kernel and taken from the end of the task list
 int als_dual_cut(const AlsParams &p, bool weighted);
-int launch_als_dual(const AlsParams &p, const PairPlan &q, int *counter, int cut, cudaStream_t s);
+int launch_als_dual(const AlsParams &p, const PairPlan &q, int64_t first_light, int *counters, int cut,
+                    cudaStream_t s);
 
 }  // namespace mcf

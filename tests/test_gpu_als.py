@@ -354,19 +354,22 @@ def test_hybrid_wide_path_long_rows_on_tensor_cores(D, chunk):
     assert not np.array_equal(outs["hybrid"][0], outs["cuda"][0])   # the long rows did change kernels
 
 
-@pytest.mark.parametrize("D", [64, 100, 128])
-def test_short_rows_dual_warp_kernel(D):
-    """D >= 64: rows with n <= 32 ratings are solved by k_als_dual (dual form,
-    warp per row); n in 33..64 by the tensor-core kernel's dual form; checked
-    against the float64 oracle and the run without the warp kernel."""
+@pytest.mark.parametrize("D,nnz", [(64, 60_000), (100, 60_000), (100, 150_000), (128, 150_000)])
+def test_short_rows_dual_warp_kernel(D, nnz):
+    """D >= 64: rows with n <= 32 ratings are solved by k_als_dual<1>, rows with
+    33..64 (D > 64) by k_als_dual<2> (dual form, warp per row); checked against
+    the float64 oracle and the run without the warp kernels (the tensor-core
+    kernel's own dual form)."""
     U, I = 3000, 400
-    u, i, s = _random_split(U, I, 60_000, 9, hot=3)      # users ~20 ratings, items ~150
+    u, i, s = _random_split(U, I, nnz, 9, hot=3)         # users ~20 / ~50 ratings, items ~150 / ~375
     rng = np.random.default_rng(5)
     P0, Q0 = rng.normal(0, 0.1, (U, D)), rng.normal(0, 0.1, (I, D))
     outs = {}
     for mode in ("dual", "tc"):
         if mode == "tc":
             os.environ["MCF_NO_DUAL_WARP"] = "1"
+        else:
+            os.environ["MCF_DUAL_WARP_MAX"] = "64"   # also k_als_dual<2> (off by default)
         try:
             eng = _engine(u, i, s, U, I, D)
             eng.set_factors(P0, Q0)
@@ -375,6 +378,7 @@ def test_short_rows_dual_warp_kernel(D):
             outs[mode] = eng.factors()[0].double().cpu().numpy()
         finally:
             os.environ.pop("MCF_NO_DUAL_WARP", None)
+            os.environ.pop("MCF_DUAL_WARP_MAX", None)
     Q32 = torch.as_tensor(Q0, dtype=torch.float32).double().numpy()
     ref, _ = oracle.als_half_step(np.zeros((U, D)), Q32, u, i, s, "users", lam_n=0.065)
     for mode, P1 in outs.items():
