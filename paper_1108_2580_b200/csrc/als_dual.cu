@@ -34,11 +34,17 @@
 namespace mcf {
 namespace {
 
-template <int S>
+// S row sets per lane (row i = lane + 32 s), rows of at most N ratings
+// (N = 8, 16, 32 for S = 1: the shared-memory footprint, and with it the
+// number of rows in flight per SM, follows the row length; N = 64 for S = 2)
+template <int S, int N_>
 struct DualCfg {
-    static constexpr int N = 32 * S;       // longest row (S ratings per lane)
+    static constexpr int N = N_;
     static constexpr int XS = N + 4;       // Xt row stride: 16-byte rows, an odd number of 16-byte units
     static constexpr int LSTR = N + 1;     // L row stride (conflict-free rows and columns)
+    static_assert(N % 8 == 0 && N <= 32 * S && N > 32 * (S - 1), "row cap");
+    // columns of K kept by row set s (lower triangle)
+    static constexpr int cols(int s) { return 32 * (s + 1) < N ? 32 * (s + 1) : N; }
     static size_t smem_bytes(int ld) { return sizeof(float) * (size_t)(ld * XS + N * LSTR + N + 128); }
 };
 
@@ -53,9 +59,9 @@ __device__ __forceinline__ void ffma2d(float &x, float &y, float a, float bx, fl
 
 // kr[s][0 .. 4 NB4) += sum_f Xt[f][lane + 32 s] * Xt[f][j]; only the lower
 // triangle is used, so row set s stops at column 32 (s + 1)
-template <int S, int NB4>
-__device__ __forceinline__ void dual_gram(const float *Xt, int D, int lane, float (&kr)[S][32 * S]) {
-    constexpr int XS = DualCfg<S>::XS;
+template <int S, int N, int NB4>
+__device__ __forceinline__ void dual_gram(const float *Xt, int D, int lane, float (&kr)[S][N]) {
+    constexpr int XS = DualCfg<S, N>::XS;
 #pragma unroll 2
     for (int f = 0; f < D; ++f) {
         float a[S];
@@ -67,7 +73,7 @@ __device__ __forceinline__ void dual_gram(const float *Xt, int D, int lane, floa
             const float4 bv = b[j4];
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                if (4 * j4 < 32 * (s + 1)) {
+                if (4 * j4 < DualCfg<S, N>::cols(s)) {
                     ffma2d(kr[s][4 * j4], kr[s][4 * j4 + 1], a[s], bv.x, bv.y);
                     ffma2d(kr[s][4 * j4 + 2], kr[s][4 * j4 + 3], a[s], bv.z, bv.w);
                 }
@@ -89,10 +95,10 @@ __device__ __forceinline__ float row_bcast(const float (&v)[S], int k) {
 }
 
 // L^T a = z, column-oriented from the L rows in shared memory
-template <int S>
+template <int S, int N>
 __device__ __forceinline__ void dual_back(float (&a)[S], const float *Ls, const float (&myinv)[S], int n,
                                           int lane) {
-    constexpr int LSTR = DualCfg<S>::LSTR;
+    constexpr int LSTR = DualCfg<S, N>::LSTR;
     for (int k = n - 1; k >= 0; --k) {
         const float ak = row_bcast<S>(a, k) * row_bcast<S>(myinv, k);
 #pragma unroll
@@ -105,26 +111,26 @@ __device__ __forceinline__ void dual_back(float (&a)[S], const float *Ls, const 
 }
 
 // L w = r, column-oriented
-template <int S>
+template <int S, int N>
 __device__ __forceinline__ void dual_fwd(float (&r)[S], const float *Ls, const float (&myinv)[S], int n,
                                          int lane) {
-    constexpr int LSTR = DualCfg<S>::LSTR;
+    constexpr int LSTR = DualCfg<S, N>::LSTR;
     for (int k = 0; k < n; ++k) {
         const float wk = row_bcast<S>(r, k) * row_bcast<S>(myinv, k);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const int i = lane + 32 * s;
             if (i == k) r[s] = wk;
-            else if (i > k) r[s] = fmaf(-Ls[i * LSTR + k], wk, r[s]);
+            else if (i > k && i < N) r[s] = fmaf(-Ls[i * LSTR + k], wk, r[s]);   // (lanes >= N hold no row)
         }
     }
 }
 
 // x[lane + 32 c] (+)= sum_j Xt[lane + 32 c][j] * al[j]   (c < 4; rows >= ld read as 0)
-template <int S, bool ADD>
+template <int S, int N, bool ADD>
 __device__ __forceinline__ void dual_xt(const float *Xt, const float *al, int nb4, int ld, int lane,
                                         float (&x)[4]) {
-    constexpr int XS = DualCfg<S>::XS;
+    constexpr int XS = DualCfg<S, N>::XS;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const int f = lane + 32 * c;
@@ -146,11 +152,11 @@ __device__ __forceinline__ void dual_xt(const float *Xt, const float *al, int nb
 // for S = 2 at D = 100).  Light tasks are sorted by length, longest first:
 // the warp finds the first task with n <= hi by bisection and takes tasks
 // from there while n > lo.
-template <int S>
+template <int S, int N>
 __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_t first_light,
                                                  int *counter, int lo, int hi) {
-    using C = DualCfg<S>;
-    constexpr int N = C::N, XS = C::XS, LSTR = C::LSTR;
+    using C = DualCfg<S, N>;
+    constexpr int XS = C::XS, LSTR = C::LSTR;
     extern __shared__ __align__(16) float dsm[];
     const int lane = threadIdx.x & 31;
     const int D = p.D, ld = p.ld;
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
                     v[q4] = (j < n && c + q4 < nc4) ? __ldg(src + c + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int q4 = 0; q4 < 8; ++q4) {
-                    if (c + q4 < nc4) {
+                    if (c + q4 < nc4 && j < N) {
                         float *d = Xt + 4 * (c + q4) * XS + j;
                         d[0] = v[q4].x;
                         d[XS] = v[q4].y;
@@ -223,16 +229,18 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
         for (int s = 0; s < S; ++s)
 #pragma unroll
             for (int j = 0; j < N; ++j) kr[s][j] = 0.f;
-        if (S == 1) {
-            if (nb4 <= 2) dual_gram<S, 2>(Xt, D, lane, kr);
-            else if (nb4 <= 4) dual_gram<S, 4>(Xt, D, lane, kr);
-            else if (nb4 <= 6) dual_gram<S, 6>(Xt, D, lane, kr);
-            else dual_gram<S, 8>(Xt, D, lane, kr);
+        if (N <= 8) {
+            dual_gram<S, N, 2>(Xt, D, lane, kr);
+        } else if (N <= 16) {
+            dual_gram<S, N, 4>(Xt, D, lane, kr);
+        } else if (N <= 32) {
+            if (nb4 <= 6) dual_gram<S, N, 6>(Xt, D, lane, kr);
+            else dual_gram<S, N, 8>(Xt, D, lane, kr);
         } else {
-            if (nb4 <= 10) dual_gram<S, 10>(Xt, D, lane, kr);
-            else if (nb4 <= 12) dual_gram<S, 12>(Xt, D, lane, kr);
-            else if (nb4 <= 14) dual_gram<S, 14>(Xt, D, lane, kr);
-            else dual_gram<S, 16>(Xt, D, lane, kr);
+            if (nb4 <= 10) dual_gram<S, N, 10>(Xt, D, lane, kr);
+            else if (nb4 <= 12) dual_gram<S, N, 12>(Xt, D, lane, kr);
+            else if (nb4 <= 14) dual_gram<S, N, 14>(Xt, D, lane, kr);
+            else dual_gram<S, N, 16>(Xt, D, lane, kr);
         }
         // Cholesky of K + lam I (right-looking; column k of L ends up in kr[.][k] of
         // the rows below k), forward substitution fused
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
                 float lik[S];
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    if (32 * (s + 1) > k) {   // row set s still has rows at or below k
+                    if (C::cols(s) > k) {   // row set s still has rows at or below k
                         const int i = lane + 32 * s;
                         lik[s] = kr[s][k] * inv;
                         if (i == k) r[s] = zk;
@@ -274,7 +282,7 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
                                 const float ljk = __shfl_sync(FULL, lik[j >> 5], j & 31);
 #pragma unroll
                                 for (int s = 0; s < S; ++s)
-                                    if (32 * (s + 1) > j) kr[s][j] = fmaf(-lik[s], ljk, kr[s][j]);
+                                    if (C::cols(s) > j) kr[s][j] = fmaf(-lik[s], ljk, kr[s][j]);
                             }
                         }
                     }
@@ -288,17 +296,19 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
 #pragma unroll
         for (int s = 0; s < S; ++s)
 #pragma unroll
-            for (int k = 0; k < 32 * (s + 1); ++k) Ls[(lane + 32 * s) * LSTR + k] = kr[s][k];
+            for (int k = 0; k < C::cols(s); ++k)
+                if (lane + 32 * s < N) Ls[(lane + 32 * s) * LSTR + k] = kr[s][k];
         __syncwarp();
         float a_sol[S];
 #pragma unroll
         for (int s = 0; s < S; ++s) a_sol[s] = r[s];
-        dual_back<S>(a_sol, Ls, myinv, n, lane);
+        dual_back<S, N>(a_sol, Ls, myinv, n, lane);
 #pragma unroll
-        for (int s = 0; s < S; ++s) al[lane + 32 * s] = a_sol[s];
+        for (int s = 0; s < S; ++s)
+            if (lane + 32 * s < N) al[lane + 32 * s] = a_sol[s];
         __syncwarp();
         float x[4];
-        dual_xt<S, false>(Xt, al, nb4, ld, lane, x);
+        dual_xt<S, N, false>(Xt, al, nb4, ld, lane, x);
         // one refinement step in the dual space
 #pragma unroll
         for (int c = 0; c < 4; ++c) xs[lane + 32 * c] = x[c];
@@ -317,13 +327,14 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
             }
             rr[s] = j < n ? y[s] - (dot0 + dot1) - lam_row * a_sol[s] : 0.f;
         }
-        dual_fwd<S>(rr, Ls, myinv, n, lane);
-        dual_back<S>(rr, Ls, myinv, n, lane);
+        dual_fwd<S, N>(rr, Ls, myinv, n, lane);
+        dual_back<S, N>(rr, Ls, myinv, n, lane);
         __syncwarp();
 #pragma unroll
-        for (int s = 0; s < S; ++s) al[lane + 32 * s] = rr[s];
+        for (int s = 0; s < S; ++s)
+            if (lane + 32 * s < N) al[lane + 32 * s] = rr[s];
         __syncwarp();
-        dual_xt<S, true>(Xt, al, nb4, ld, lane, x);
+        dual_xt<S, N, true>(Xt, al, nb4, ld, lane, x);
         bool fin = true;
 #pragma unroll
         for (int c = 0; c < 4; ++c) fin = fin && isfinite(x[c]);
@@ -339,21 +350,21 @@ __global__ void __launch_bounds__(32) k_als_dual(AlsParams p, PairPlan q, int64_
     }
 }
 
-template <int S>
+template <int S, int N>
 int launch_dual(const AlsParams &p, const PairPlan &q, int64_t first_light, int *counter, int lo, int hi,
                 cudaStream_t s) {
-    const size_t smem = DualCfg<S>::smem_bytes(p.ld);
+    const size_t smem = DualCfg<S, N>::smem_bytes(p.ld);
     static size_t attr = 0;
     if (smem > attr) {
-        cudaFuncSetAttribute(k_als_dual<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_als_dual<S, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_dual<S>, 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_als_dual<S, N>, 32, smem);
     const int64_t grid = std::min<int64_t>(q.n_tasks - first_light, (int64_t)sms * std::max(per_sm, 1));
-    if (grid > 0) k_als_dual<S><<<(unsigned)grid, 32, smem, s>>>(p, q, first_light, counter, lo, hi);
+    if (grid > 0) k_als_dual<S, N><<<(unsigned)grid, 32, smem, s>>>(p, q, first_light, counter, lo, hi);
     return check_launch("mcf_als_half_step(dual rows)");
 }
 
@@ -374,15 +385,17 @@ int als_dual_cut(const AlsParams &p, bool weighted) {
     return mx >= 64 ? 64 : 32;
 }
 
-// counters: two zeroed ints (one per kernel); first_light: index of the
+// counters: four zeroed ints (one per kernel); first_light: index of the
 // first light task (= number of hot-row chunks)
 int launch_als_dual(const AlsParams &p, const PairPlan &q, int64_t first_light, int *counters, int cut,
                     cudaStream_t s) {
     if (cut <= 0 || q.n_tasks <= first_light) return MCF_OK;
     int rc = MCF_OK;
-    // the longer rows first (33..64), then the tail
-    if (cut > 32 && (rc = launch_dual<2>(p, q, first_light, counters + 1, 32, 64, s))) return rc;
-    return launch_dual<1>(p, q, first_light, counters, -1, 32, s);
+    // the longer rows first; one kernel per length class (its own counter each)
+    if (cut > 32 && (rc = launch_dual<2, 64>(p, q, first_light, counters + 3, 32, 64, s))) return rc;
+    if ((rc = launch_dual<1, 32>(p, q, first_light, counters, 16, 32, s))) return rc;
+    if ((rc = launch_dual<1, 16>(p, q, first_light, counters + 1, 8, 16, s))) return rc;
+    return launch_dual<1, 8>(p, q, first_light, counters + 2, -1, 8, s);
 }
 
 }  // namespace mcf

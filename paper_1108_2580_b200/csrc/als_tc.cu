@@ -208,13 +208,25 @@ __global__ void k_tc_prep(AlsParams p, PairPlan q, TcWs w) {
     for (int64_t i = tid; i < w.n_slots; i += nthr) w.hot_count[i] = 0;
     float mx = 0.f, my = 0.f, ms = 0.f;
     unsigned mn = 0;
-    const int64_t nf = p.n_fixed * (int64_t)p.ld;
-    for (int64_t i = tid; i < nf; i += nthr) {
-        if ((int)(i % p.ld) < p.D) mx = fmaxf(mx, fabsf(__ldg(p.fixed + i)));
+    // (the padding columns D..ld-1 are zero by the table contract: they cannot raise the maximum)
+    const int64_t nf4 = p.n_fixed * (int64_t)(p.ld >> 2);
+    for (int64_t i = tid; i < nf4; i += nthr) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(p.fixed) + i);
+        mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
     }
-    // ratings: a warp per task, lanes over its ratings
     const int warp = tid >> 5, lane = threadIdx.x & 31, nwarps = nthr >> 5;
-    for (int64_t t = warp; t < q.n_tasks; t += nwarps) {
+    if (!p.row_list) {
+        // a contiguous row range: its ratings are one contiguous span (coalesced pass)
+        const int64_t a = p.ptr[p.row_lo], b = p.ptr[p.row_lo + p.n_list];
+        for (int64_t i = a + tid; i < b; i += nthr) my = fmaxf(my, fabsf(__ldg(p.val + i) - p.y_shift));
+        for (int64_t j = tid; j < p.n_list; j += nthr) {
+            const int64_t r = p.row_lo + j;
+            mn = max(mn, (unsigned)(p.ptr[r + 1] - p.ptr[r]));
+            if (p.tax_S) ms = fmaxf(ms, p.tau * fabsf(p.tax_S[r]));
+        }
+    }
+    // a row list: a warp per task, lanes over its ratings
+    for (int64_t t = p.row_list ? warp : q.n_tasks; t < q.n_tasks; t += nwarps) {
         const int r = q.task_row[t];
         const int64_t k0 = q.task_k0[t];
         const int n = q.task_n[t];
@@ -287,8 +299,19 @@ __global__ void k_tc_split(AlsParams p, PairPlan q, TcWs w, int TW) {
         reinterpret_cast<uint32_t *>(w.th)[e] = h;
         reinterpret_cast<uint32_t *>(w.tl)[e] = l;
     }
-    // the planned ratings (a warp per task), at their CSR positions: the
-    // Gram's rating tiles are 4-byte copies of these
+    // the planned ratings at their CSR positions: the Gram's rating tiles are
+    // 4-byte copies of these.  A contiguous row range is one coalesced span ...
+    if (!p.row_list) {
+        const int64_t a = p.ptr[p.row_lo], b = p.ptr[p.row_lo + p.n_list];
+        for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            uint32_t h, l;
+            split2((__ldg(p.val + i) - p.y_shift) * sy, 0.f, h, l);
+            w.ysp[i] = (h & 0xffffu) | (l << 16);
+        }
+        return;
+    }
+    // ... a row list takes a warp per task
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < q.n_tasks; t += nw) {
