@@ -218,7 +218,19 @@ __global__ void k_tc_prep(AlsParams p, PairPlan q, TcWs w) {
     if (!p.row_list) {
         // a contiguous row range: its ratings are one contiguous span (coalesced pass)
         const int64_t a = p.ptr[p.row_lo], b = p.ptr[p.row_lo + p.n_list];
-        for (int64_t i = a + tid; i < b; i += nthr) my = fmaxf(my, fabsf(__ldg(p.val + i) - p.y_shift));
+        // four independent loads in flight per thread
+        float m1 = 0.f, m2 = 0.f, m3 = 0.f;
+        int64_t i = a + tid;
+        for (; i + 3 * (int64_t)nthr < b; i += 4 * (int64_t)nthr) {
+            const float v0 = __ldg(p.val + i), v1 = __ldg(p.val + i + nthr);
+            const float v2 = __ldg(p.val + i + 2 * (int64_t)nthr), v3 = __ldg(p.val + i + 3 * (int64_t)nthr);
+            my = fmaxf(my, fabsf(v0 - p.y_shift));
+            m1 = fmaxf(m1, fabsf(v1 - p.y_shift));
+            m2 = fmaxf(m2, fabsf(v2 - p.y_shift));
+            m3 = fmaxf(m3, fabsf(v3 - p.y_shift));
+        }
+        for (; i < b; i += nthr) my = fmaxf(my, fabsf(__ldg(p.val + i) - p.y_shift));
+        my = fmaxf(fmaxf(my, m1), fmaxf(m2, m3));
         for (int64_t j = tid; j < p.n_list; j += nthr) {
             const int64_t r = p.row_lo + j;
             mn = max(mn, (unsigned)(p.ptr[r + 1] - p.ptr[r]));
@@ -1282,7 +1294,7 @@ int launch_als_tc(const AlsParams &p, const PairPlan &q, void *ws, size_t ws_byt
     }
     int rc;
     if ((rc = cuda_status(cudaMemsetAsync(w.scal, 0, 4 * sizeof(unsigned), s), "memset"))) return rc;
-    k_tc_prep<<<148 * 4, 256, 0, s>>>(p, q, w);
+    k_tc_prep<<<148 * 8, 256, 0, s>>>(p, q, w);
     if ((rc = check_launch("mcf_als_half_step(tensor-core prep)"))) return rc;
     switch ((p.D + 15) / 16) {
         case 4: return launch_tc<4>(p, q, w, s);
