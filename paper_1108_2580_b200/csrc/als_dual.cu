@@ -35,7 +35,7 @@ namespace mcf {
 namespace {
 
 // S row sets per lane (row i = lane + 32 s), rows of at most N ratings
-// (N = 8, 16, 32 for S = 1: the shared-memory footprint, and with it the
+// (N = 8, 16, 24, 32 for S = 1: the shared-memory footprint, and with it the
 // number of rows in flight per SM, follows the row length; N = 64 for S = 2)
 template <int S, int N_>
 struct DualCfg {
@@ -385,17 +385,18 @@ int als_dual_cut(const AlsParams &p, bool weighted) {
     return mx >= 64 ? 64 : 32;
 }
 
-// counters: four zeroed ints (one per kernel); first_light: index of the
+// counters: five zeroed ints (one per kernel); first_light: index of the
 // first light task (= number of hot-row chunks)
 int launch_als_dual(const AlsParams &p, const PairPlan &q, int64_t first_light, int *counters, int cut,
                     cudaStream_t s) {
     if (cut <= 0 || q.n_tasks <= first_light) return MCF_OK;
     int rc = MCF_OK;
     // the longer rows first; one kernel per length class (its own counter each)
-    if (cut > 32 && (rc = launch_dual<2, 64>(p, q, first_light, counters + 3, 32, 64, s))) return rc;
-    if ((rc = launch_dual<1, 32>(p, q, first_light, counters, 16, 32, s))) return rc;
-    if ((rc = launch_dual<1, 16>(p, q, first_light, counters + 1, 8, 16, s))) return rc;
-    return launch_dual<1, 8>(p, q, first_light, counters + 2, -1, 8, s);
+    if (cut > 32 && (rc = launch_dual<2, 64>(p, q, first_light, counters + 4, 32, 64, s))) return rc;
+    if ((rc = launch_dual<1, 32>(p, q, first_light, counters, 24, 32, s))) return rc;
+    if ((rc = launch_dual<1, 24>(p, q, first_light, counters + 1, 16, 24, s))) return rc;
+    if ((rc = launch_dual<1, 16>(p, q, first_light, counters + 2, 8, 16, s))) return rc;
+    return launch_dual<1, 8>(p, q, first_light, counters + 3, -1, 8, s);
 }
 
 }  // namespace mcf
