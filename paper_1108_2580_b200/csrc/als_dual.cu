@@ -16,7 +16,8 @@
 // lam alpha: the rank-deficient short-row systems have cond ~ 5e3, fp32
 // rounding of K alone exceeds the 1e-4 budget).
 //
-// k_als_dual<1> takes n <= 32 (11 rows per SM in flight at D = 100);
+// k_als_dual<1, N> takes n <= 32 in four length classes (N = 8, 16, 24, 32;
+// 11 rows per SM in flight at D = 100 for the longest, ~40 for the shortest);
 // k_als_dual<2> (33 <= n <= 64, two row sets per lane, 4 rows per SM) is
 // built but off by default (MCF_DUAL_WARP_MAX=64): at 4 warps per SM it is
 // latency-bound and slower than the tensor-core kernel's dual form.
