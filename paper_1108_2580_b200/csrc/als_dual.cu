@@ -63,7 +63,7 @@ __device__ __forceinline__ void ffma2d(float &x, float &y, float a, float bx, fl
 template <int S, int N, int NB4>
 __device__ __forceinline__ void dual_gram(const float *Xt, int D, int lane, float (&kr)[S][N]) {
     constexpr int XS = DualCfg<S, N>::XS;
-#pragma unroll 2
+#pragma unroll 4
     for (int f = 0; f < D; ++f) {
         float a[S];
 #pragma unroll
