@@ -140,7 +140,7 @@ def kernel_name(D: int) -> str:
     if tc_path(D):
         return ("k_als_tc<NBLK> (tcgen05 kind::f16 Gram, fp16 h/l split, TMEM-resident blocked "
                 "Cholesky with negated-MMA trailing updates; + k_tc_prep, k_tc_split; rows with "
-                "n <= 32 ratings: k_als_dual<1>, dual form on CUDA cores)")
+                "n <= 32 ratings: k_als_dual<1, N>, dual form on CUDA cores)")
     if D <= 20:
         return "k_als_pair<5,4> (fused Gram + lam*n + Cholesky + solve; + k_als_heavy for hot rows)"
     if D <= 28:
@@ -190,7 +190,7 @@ def launches_per_sweep(eng) -> int:
     for lay in (eng.r.by_item, eng.r.by_user):
         info = lay.plan()[1]
         if tc_path(eng.D):
-            n += 4      # k_tc_prep, k_tc_split, k_als_tc, k_als_dual<1>
+            n += 7      # k_tc_prep, k_tc_split, k_als_tc, k_als_dual<1, N> for N = 32, 24, 16, 8
         else:
             n += 1 + (1 if (eng.D <= 20 and info[4] > 0) else 0)
     return n
