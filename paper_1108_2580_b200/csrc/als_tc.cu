@@ -299,24 +299,40 @@ __device__ __forceinline__ void tc_scales(const AlsParams &p, const TcWs &w, flo
 __global__ void k_tc_split(AlsParams p, PairPlan q, TcWs w, int TW) {
     float s, sy;
     tc_scales(p, w, s, sy);
-    const int64_t n = p.n_fixed * (int64_t)(TW / 2);
+    // a thread per 4 features: one 16-byte load (ld and D's padding are multiples of 4
+    // floats; the padding columns D..ld-1 are zero), two 8-byte stores; TW is 64 or 128
+    const int sh = TW == 128 ? 5 : 4;   // log2(TW / 4)
+    const int64_t n = p.n_fixed << sh;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / (TW / 2);
-        const int f = 2 * (int)(e - r * (TW / 2));
-        const float a = f < p.D ? __ldg(p.fixed + r * p.ld + f) * s : 0.f;
-        const float b = f + 1 < p.D ? __ldg(p.fixed + r * p.ld + f + 1) * s : 0.f;
-        uint32_t h, l;
-        split2(a, b, h, l);
-        reinterpret_cast<uint32_t *>(w.th)[e] = h;
-        reinterpret_cast<uint32_t *>(w.tl)[e] = l;
+        const int64_t r = e >> sh;
+        const int f = 4 * (int)(e & ((1 << sh) - 1));
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (f < p.ld) v = __ldg(reinterpret_cast<const float4 *>(p.fixed + r * p.ld + f));
+        uint2 h, l;
+        split2(f < p.D ? v.x * s : 0.f, f + 1 < p.D ? v.y * s : 0.f, h.x, l.x);
+        split2(f + 2 < p.D ? v.z * s : 0.f, f + 3 < p.D ? v.w * s : 0.f, h.y, l.y);
+        reinterpret_cast<uint2 *>(w.th)[e] = h;
+        reinterpret_cast<uint2 *>(w.tl)[e] = l;
     }
     // the planned ratings at their CSR positions: the Gram's rating tiles are
     // 4-byte copies of these.  A contiguous row range is one coalesced span ...
     if (!p.row_list) {
         const int64_t a = p.ptr[p.row_lo], b = p.ptr[p.row_lo + p.n_list];
-        for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b;
-             i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+        int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + 3 * nthr < b; i += 4 * nthr) {   // four independent loads in flight per thread
+            float v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = __ldg(p.val + i + k * nthr);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t h, l;
+                split2((v[k] - p.y_shift) * sy, 0.f, h, l);
+                w.ysp[i + k * nthr] = (h & 0xffffu) | (l << 16);
+            }
+        }
+        for (; i < b; i += nthr) {
             uint32_t h, l;
             split2((__ldg(p.val + i) - p.y_shift) * sy, 0.f, h, l);
             w.ysp[i] = (h & 0xffffu) | (l << 16);

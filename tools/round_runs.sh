@@ -13,7 +13,7 @@ python bench.py --config 3 --steps 2 --skip-cpu --skip-e2e > gpurun_out/bench_cf
 python bench.py --config 4 --steps 2 --skip-cpu --skip-e2e > gpurun_out/bench_cfg4.log 2>&1
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:^k_ -c 400 --csv --log-file gpurun_out/launches_cfg1.csv python bench.py --steps 2 --warmup 3 --skip-cpu --skip-e2e --skip-parity > gpurun_out/ncu_launch.log 2>&1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:^k_ -c 64 --csv --log-file gpurun_out/launches_cfg3.csv python bench.py --config 3 --steps 1 --warmup 1 --skip-cpu --skip-e2e --skip-parity > gpurun_out/ncu_launch3.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_als|k_tc" -c 36 --csv --log-file gpurun_out/launches_cfg3.csv python bench.py --config 3 --steps 1 --warmup 1 --skip-cpu --skip-e2e --skip-parity > gpurun_out/ncu_launch3.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_als_pair -c 2 -o /tmp/prof_pair_r2 -f python bench.py --steps 1 --warmup 0 --skip-cpu --skip-e2e --skip-parity > gpurun_out/ncu_pair.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_als_tc -c 2 -o /tmp/prof_tc_r2 -f python bench.py --config 3 --steps 1 --warmup 0 --skip-cpu --skip-e2e --skip-parity > gpurun_out/ncu_tc.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_als_dual -c 2 -o /tmp/prof_dual_r2 -f python bench.py --config 3 --steps 1 --warmup 0 --skip-cpu --skip-e2e --skip-parity > gpurun_out/ncu_dual.log 2>&1
